@@ -1,0 +1,142 @@
+/*
+ * patfft_b200.h -- C ABI of the B200-native NEDNER-NUFFT reconstruction.
+ *
+ * The reference (`patfft`, pure Python) has no FFI; its public entry point
+ * for this path is
+ *
+ *     patfft.recon.reconstruct_nedner(rec, out_dims=None, upsample=1, spec=None)
+ *         /root/reference/pkg/src/patfft/recon.py:358-379
+ *
+ * which builds a NedPlan (nufft.py:345-418), a NerPlan (nufft.py:270-332)
+ * and inverts the spectrum (recon.py:249-260).  This header is what a
+ * ctypes binding of that path binds: plain pointers,
+ * sizes and status codes, no torch or numpy types.
+ *
+ * Conventions
+ *  - Every function returns PATFFT_OK (0) or a PATFFT_ERR_* code; the
+ *    message of the last failure on the calling thread is returned by
+ *    patfft_last_error().  The Python shim maps PARAMETER -> ParameterError,
+ *    DATA -> DataValidationError, everything else -> RuntimeError, i.e. the
+ *    reference's error classes (errors.py:4-13).
+ *  - Input validation that the reference performs in SensorRecord
+ *    (recon.py:115-164) happens in the shim before the ABI is crossed.
+ *  - The caller owns all host buffers.  The plan owns its device buffers,
+ *    cuFFT plans and CUDA stream.  A plan is immutable after creation;
+ *    execute calls on one plan are serialised internally (they share
+ *    scratch), different plans run concurrently.
+ *  - Results are bit-deterministic for a given plan and device (fixed
+ *    per-element accumulation order, no floating-point atomics).
+ */
+#ifndef PATFFT_B200_H
+#define PATFFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PATFFT_OK = 0,
+  PATFFT_ERR_PARAMETER = 1,   /* -> ParameterError (spec / upsample / sizes) */
+  PATFFT_ERR_DATA = 2,        /* -> DataValidationError (record contents)    */
+  PATFFT_ERR_CUDA = 3,        /* CUDA / cuFFT / NCCL runtime failure         */
+  PATFFT_ERR_UNSUPPORTED = 4  /* legal for the reference, not yet on the GPU */
+};
+
+/* Geometry + window of one reconstruction.  Mirrors the arguments of
+ * reconstruct_nedner (recon.py:358-363) after SensorRecord validation. */
+typedef struct patfft_nedner_desc {
+  int32_t n_lat;          /* d-1: number of lateral axes, 1 or 2                  */
+  int32_t out_dims[2];    /* lateral output grid per axis, even (recon.py:372)    */
+  int32_t n_time;         /* N_t, even (recon.py:127)                             */
+  int32_t upsample;       /* integer >= 1 (recon.py:392-394)                      */
+  int32_t n_sensors;      /* M                                                    */
+  double lat_ratio[2];    /* N_t*dy/(n_lateral*dx) per axis (recon.py:340-342)    */
+  double spec_c;          /* WindowSpec.c (nufft.py:109)                          */
+  int32_t spec_K;         /* WindowSpec.K (nufft.py:110)                          */
+  double spec_alpha;      /* WindowSpec.alpha, NaN = resolve at plan time         */
+  double spec_beta;       /* WindowSpec.beta,  NaN = resolve at plan time         */
+} patfft_nedner_desc;
+
+typedef struct patfft_nedner_plan patfft_nedner_plan;
+
+/* Build a plan for fixed sensor positions (replaces NedPlan.__init__ +
+ * spread_matrix, nufft.py:352-398, and NerPlan.__init__, nufft.py:273-285).
+ *   grid_positions : M x n_lat, row-major, in output-grid units, i.e.
+ *                    rec.grid_positions() * out_dims / n_lateral (recon.py:376)
+ *   sensor_scale   : M, h_m / dx^(d-1) (recon.py:374)
+ *   device         : CUDA device ordinal                                     */
+int patfft_nedner_plan_create(const patfft_nedner_desc* desc, const double* grid_positions,
+                              const double* sensor_scale, int device, patfft_nedner_plan** out);
+
+/* Output volume shape (N0*up, N1*up, Nt*up) or (N*up, Nt*up); returns rank. */
+int patfft_nedner_output_shape(const patfft_nedner_plan* plan, int64_t shape[3]);
+
+/* Full drop-in execution from host memory (recon.py:370-379):
+ *   samples : M x N_t float64 host (pinned or pageable), row-major
+ *   image   : output float64 host, C order, lateral axes centred (fftshift)
+ *   imag_residual : optional; receives max|Im|/max|Re| of the inverse FFT.
+ *                   The GPU inverts the Hermitian half spectrum with a C2R
+ *                   transform, so the value is exactly 0.                  */
+int patfft_nedner_execute(patfft_nedner_plan* plan, const double* samples, double* image,
+                          double* imag_residual);
+
+/* Device-resident execution on `stream` (NULL = the plan's own stream):
+ *   samples_dev : M x N_t float32 on the plan's device
+ *   image_dev   : output float32 on the plan's device
+ * Enqueues work and returns without synchronising.                       */
+int patfft_nedner_execute_device(patfft_nedner_plan* plan, const float* samples_dev,
+                                 float* image_dev, void* stream);
+
+/* Frames sharing one sensor layout (config 5): samples F x M x N_t float32,
+ * images F x out-volume float32, both device-resident.                    */
+int patfft_nedner_execute_frames_device(patfft_nedner_plan* plan, int n_frames,
+                                        const float* samples_dev, float* images_dev, void* stream);
+
+void patfft_nedner_plan_destroy(patfft_nedner_plan* plan);
+
+/* Per-stage device timing (CUDA events on the plan's stream).  When enabled
+ * every execute records one event per stage boundary; patfft_nedner_stage_times
+ * returns the accumulated milliseconds per stage and the launch count per
+ * stage since the last reset, and the stage names via patfft_nedner_stage_name. */
+enum { PATFFT_STAGE_SPREAD = 0, PATFFT_STAGE_LATERAL_FFT = 1, PATFFT_STAGE_CROP = 2,
+       PATFFT_STAGE_NER = 3, PATFFT_STAGE_INVERSE_FFT = 4, PATFFT_N_STAGES = 5 };
+int patfft_nedner_set_profiling(patfft_nedner_plan* plan, int enabled);
+int patfft_nedner_stage_times(patfft_nedner_plan* plan, double* ms, int64_t* launches, int n);
+const char* patfft_nedner_stage_name(int stage);
+/* Algorithmic bytes per launch of each stage (roofline table). */
+int patfft_nedner_stage_bytes(const patfft_nedner_plan* plan, double* bytes, int n);
+/* Number of kernels (own + cuFFT) one execute_device launches. */
+int patfft_nedner_launches_per_execute(const patfft_nedner_plan* plan, int* own, int* library);
+
+/* ---- small runtime helpers used by the Python shim and bench.py ---------- */
+const char* patfft_last_error(void);
+const char* patfft_version(void);
+int patfft_device_count(int* count);
+int patfft_device_alloc(int device, size_t bytes, void** ptr);
+int patfft_device_free(void* ptr);
+int patfft_host_alloc(size_t bytes, void** ptr);          /* pinned */
+int patfft_host_free(void* ptr);
+int patfft_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+int patfft_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
+int patfft_stream_sync(void* stream);
+int patfft_plan_stream(const patfft_nedner_plan* plan, void** stream);
+/* f64 <-> f32 conversion on device (for the host-buffer path). */
+int patfft_convert_f64_to_f32(const double* src, float* dst, size_t n, void* stream);
+int patfft_convert_f32_to_f64(const float* src, double* dst, size_t n, void* stream);
+/* Write `bytes` of a scratch buffer larger than L2 (cache flush between
+ * timed iterations). */
+int patfft_l2_flush(void* scratch, size_t bytes, void* stream);
+/* CUDA-event timing on a stream: record/elapsed.  Events are opaque. */
+int patfft_event_create(void** ev);
+int patfft_event_record(void* ev, void* stream);
+int patfft_event_elapsed_ms(void* start, void* stop, float* ms);
+int patfft_event_destroy(void* ev);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PATFFT_B200_H */

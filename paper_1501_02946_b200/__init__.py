@@ -1,0 +1,35 @@
+"""B200-native NEDNER-NUFFT planar photoacoustic reconstruction.
+
+Drop-in for ``patfft.recon.reconstruct_nedner`` of the reference
+(arXiv 1501.02946, /root/reference/pkg/src/patfft/recon.py:358-379): same
+Python signature and types, executed by hand-written sm_100a CUDA kernels
+behind the C ABI in ``include/patfft_b200.h``.
+"""
+
+from .errors import DataValidationError, DeviceError, NumericalError, ParameterError
+from .recon import (
+    NedNerPlan,
+    ScalarField,
+    SensorRecord,
+    amplitude_factor,
+    kappa,
+    reconstruct_nedner,
+)
+from .window import WindowSpec
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DataValidationError",
+    "DeviceError",
+    "NumericalError",
+    "ParameterError",
+    "NedNerPlan",
+    "ScalarField",
+    "SensorRecord",
+    "WindowSpec",
+    "amplitude_factor",
+    "kappa",
+    "reconstruct_nedner",
+    "__version__",
+]

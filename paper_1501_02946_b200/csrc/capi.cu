@@ -1,0 +1,634 @@
+// C ABI (include/patfft_b200.h): plan construction, execution, helpers.
+//
+// Plan construction restates, on the host in float64, what the reference
+// builds per call: NedPlan (nufft.py:352-398: per-axis oversampled sizes,
+// resolved windows, deapodisation, spreading taps) and NerPlan
+// (nufft.py:273-285: oversampled length, pre-window, tap norm), plus the
+// lateral frequency tables of recon.py:200-215/282.  The spreading taps are
+// reorganised for the GPU: per oversampled grid row, the contributing
+// (sensor, row weight, column window) entries sorted by column, split into
+// column segments for load balance.
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "patfft_internal.h"
+
+namespace patfft {
+void spread_config(int K2, int T, int* bdim, int* tpt, int* tchunks);
+int ner_threads(int n_over);
+}  // namespace patfft
+
+using namespace patfft;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess)                                                                     \
+      return fail(PATFFT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));       \
+  } while (0)
+
+#define CUFFT_TRY(expr)                                                                        \
+  do {                                                                                         \
+    cufftResult _r = (expr);                                                                   \
+    if (_r != CUFFT_SUCCESS)                                                                   \
+      return fail(PATFFT_ERR_CUDA, std::string(#expr) + ": cufft error " + std::to_string(_r)); \
+  } while (0)
+
+int64_t pmod(int64_t a, int64_t m) { return ((a % m) + m) % m; }
+int64_t floordiv(int64_t a, int64_t b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+int64_t ceildiv(int64_t a, int64_t b) { return -floordiv(-a, b); }
+
+bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+int ilog2(int64_t n) {
+  int l = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  return l;
+}
+
+template <typename T>
+int upload(T** dptr, const std::vector<T>& h) {
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dptr), std::max<size_t>(1, h.size()) * sizeof(T)));
+  if (!h.empty()) CUDA_TRY(cudaMemcpy(*dptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return PATFFT_OK;
+}
+
+template <typename T>
+int dalloc(T** dptr, size_t count) {
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dptr), std::max<size_t>(1, count) * sizeof(T)));
+  return PATFFT_OK;
+}
+
+// Per-sensor taps along one lateral axis (nufft.py:373-378): centred window
+// start (k0 - K + 1 + n_over/2) and 2K weights psi_hat(x - bin/c)/psi_hat(0).
+void axis_taps(double x, const Window& w, int n_over, int* start, double* wt) {
+  const int K2 = 2 * w.K;
+  const double k0 = std::floor(w.c_eff * x);
+  const double norm = 1.0 / kb_psihat(w, 0.0);
+  for (int a = 0; a < K2; ++a) {
+    const double bin = k0 + double(a - w.K + 1);
+    wt[a] = kb_psihat(w, x - bin / w.c_eff) * norm;
+  }
+  *start = static_cast<int>(k0) - w.K + 1 + n_over / 2;
+}
+
+// fftfreq(n)[k]*n*ratio squared, with numpy's rounding (recon.py:211)
+double jterm(int kw, int n, double ratio) {
+  const int ks = (kw < (n + 1) / 2) ? kw : kw - n;  // fftfreq integer for wrapped index
+  const double v = (double(ks) * (1.0 / double(n))) * double(n) * ratio;
+  return v * v;
+}
+
+void free_dev(void* p) {
+  if (p) cudaFree(p);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* patfft_last_error(void) { return g_err.c_str(); }
+const char* patfft_version(void) { return "patfft-b200 0.1.0 (sm_100a)"; }
+
+int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, const double* sscale, int device,
+                              patfft_nedner_plan** out) {
+  if (!d || !gpos || !sscale || !out) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  *out = nullptr;
+  if (d->n_lat != 1 && d->n_lat != 2) return fail(PATFFT_ERR_PARAMETER, "NED transforms support 1 or 2 position axes");
+  for (int a = 0; a < d->n_lat; ++a)
+    if (d->out_dims[a] < 2 || d->out_dims[a] % 2)
+      return fail(PATFFT_ERR_PARAMETER, "centered grid lengths must be even and >= 2");
+  if (d->n_time < 2 || d->n_time % 2) return fail(PATFFT_ERR_DATA, "samples must be (M, N_t) with even N_t");
+  if (d->upsample < 1) return fail(PATFFT_ERR_PARAMETER, "upsample must be an integer >= 1");
+  if (d->n_sensors < 1) return fail(PATFFT_ERR_DATA, "record has no sensors");
+  if (!(std::isfinite(d->spec_c) && d->spec_c > 1.0))
+    return fail(PATFFT_ERR_PARAMETER, "oversampling factor must exceed 1");
+  if (d->spec_K < 1) return fail(PATFFT_ERR_PARAMETER, "interpolation half-width K must be an integer >= 1");
+  if (d->spec_K > kMaxTaps / 2)
+    return fail(PATFFT_ERR_UNSUPPORTED, "GPU path supports interpolation half-width K <= 8");
+
+  std::unique_ptr<patfft_nedner_plan, void (*)(patfft_nedner_plan*)> P(new patfft_nedner_plan(),
+                                                                     &patfft_nedner_plan_destroy);
+  P->device = device;
+  CUDA_TRY(cudaSetDevice(device));
+  P->n_lat = d->n_lat;
+  P->N0 = d->n_lat == 2 ? d->out_dims[0] : 1;
+  P->N1 = d->out_dims[d->n_lat - 1];
+  P->T = d->n_time;
+  P->up = d->upsample;
+  P->M = d->n_sensors;
+  P->K2 = 2 * d->spec_K;
+  P->N1h = P->N1 / 2 + 1;
+  P->N0u = d->n_lat == 2 ? P->N0 * P->up : 1;
+  P->N1u = P->N1 * P->up;
+  P->N1uh = P->N1u / 2 + 1;
+  P->Tu = P->T * P->up;
+  const int K = d->spec_K;
+  const double c = d->spec_c;
+
+  // ---- lateral oversampled sizes and windows (nufft.py:360-363) ----------
+  int n_over_lat[2] = {1, 1};
+  double ceff_min = 1e300;
+  for (int a = 0; a < d->n_lat; ++a) {
+    const int N = d->out_dims[a];
+    int n = even_fast_len(c * N);
+    if (a == d->n_lat - 1)  // column axis: the spread ring works in groups of 4
+      while (n % 4) n = even_fast_len(n + 1);
+    n_over_lat[a] = n;
+    ceff_min = std::min(ceff_min, double(n) / N);
+  }
+  std::string err;
+  Window wmin;
+  if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, ceff_min, &wmin, &err))
+    return fail(PATFFT_ERR_PARAMETER, err);
+  for (int a = 0; a < d->n_lat; ++a) {
+    if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_lat[a]) / d->out_dims[a], &P->win_lat[a],
+                        &err))
+      return fail(PATFFT_ERR_PARAMETER, err);
+  }
+  P->nrows = d->n_lat == 2 ? n_over_lat[0] : 1;
+  P->ncols = n_over_lat[d->n_lat - 1];
+  const Window& wrow = P->win_lat[0];
+  const Window& wcol = P->win_lat[d->n_lat - 1];
+
+  // ---- NER window (nufft.py:273-285), power-of-two oversampled length ----
+  const int n_ext = 2 * P->T;
+  int64_t n_over_t = 1;
+  while (n_over_t < (int64_t)std::ceil(c * n_ext)) n_over_t <<= 1;
+  if (n_over_t > 16384)
+    return fail(PATFFT_ERR_UNSUPPORTED, "GPU NER supports oversampled depth lengths up to 16384 (N_t <= 4096 at c=2)");
+  P->n_over_t = (int)n_over_t;
+  if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_t) / n_ext, &P->win_t, &err))
+    return fail(PATFFT_ERR_PARAMETER, err);
+  P->fused_ifft = is_pow2(P->Tu) && P->Tu <= 16384;
+  {
+    const int nth = ner_threads(P->n_over_t);
+    if (P->T > 8 * nth) return fail(PATFFT_ERR_UNSUPPORTED, "depth too long for the NER CTA layout");
+  }
+
+  // ---- spreading entries --------------------------------------------------
+  const int M = P->M, K2 = P->K2, nrows = P->nrows, ncols = P->ncols, T = P->T;
+  std::vector<int> ucol(M), urow(M);
+  std::vector<double> wcolv((size_t)M * K2), wrowv((size_t)M * K2);
+  std::vector<float> colw((size_t)M * K2);
+  for (int m = 0; m < M; ++m) {
+    const double xc = gpos[(size_t)m * d->n_lat + (d->n_lat - 1)];
+    if (!std::isfinite(xc)) return fail(PATFFT_ERR_DATA, "sensor positions must be finite");
+    axis_taps(xc, wcol, ncols, &ucol[m], &wcolv[(size_t)m * K2]);
+    for (int a = 0; a < K2; ++a) colw[(size_t)m * K2 + a] = (float)wcolv[(size_t)m * K2 + a];
+    if (d->n_lat == 2) {
+      const double xr = gpos[(size_t)m * 2];
+      if (!std::isfinite(xr)) return fail(PATFFT_ERR_DATA, "sensor positions must be finite");
+      axis_taps(xr, wrow, nrows, &urow[m], &wrowv[(size_t)m * K2]);
+    }
+  }
+  struct E {
+    int row, ws, m;
+    float w;
+  };
+  std::vector<E> es;
+  es.reserve((size_t)M * (d->n_lat == 2 ? K2 : 1) + 64);
+  const int ntap_rows = d->n_lat == 2 ? K2 : 1;
+  for (int m = 0; m < M; ++m) {
+    const double sc = sscale[m];
+    for (int a = 0; a < ntap_rows; ++a) {
+      const int row = d->n_lat == 2 ? (int)pmod(urow[m] + a, nrows) : 0;
+      const double wr = (d->n_lat == 2 ? wrowv[(size_t)m * K2 + a] : 1.0) * sc;
+      const int64_t ws0 = ucol[m];
+      const int64_t smin = ceildiv(-(K2 - 1) - ws0, ncols), smax = floordiv(ncols - 1 - ws0, ncols);
+      for (int64_t s = smin; s <= smax; ++s) es.push_back({row, (int)(ws0 + s * ncols), m, (float)wr});
+    }
+  }
+  std::stable_sort(es.begin(), es.end(), [](const E& x, const E& y) {
+    return x.row != y.row ? x.row < y.row : x.ws < y.ws;
+  });
+  P->n_entries = (int64_t)es.size();
+  std::vector<int4> ent(es.size());
+  for (size_t i = 0; i < es.size(); ++i) {
+    int wbits;
+    std::memcpy(&wbits, &es[i].w, 4);
+    ent[i] = make_int4(es[i].m, es[i].ws, wbits, 0);
+  }
+  std::vector<int64_t> row_start(nrows + 1, 0);
+  for (const E& e : es) row_start[e.row + 1]++;
+  for (int r = 0; r < nrows; ++r) row_start[r + 1] += row_start[r];
+
+  int bdim, tpt, tch;
+  spread_config(K2, T, &bdim, &tpt, &tch);
+  {
+    const int64_t target = 148LL * 16;
+    int64_t nseg = ceildiv(target, (int64_t)nrows * tch);
+    nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, std::max(1, ncols / 32)));
+    int segw = (int)ceildiv(ncols, nseg);
+    segw = (segw + 3) / 4 * 4;
+    P->segw = segw;
+    P->nseg = (int)ceildiv(ncols, segw);
+  }
+  std::vector<int2> segr((size_t)nrows * P->nseg);
+  for (int r = 0; r < nrows; ++r) {
+    auto b = es.begin() + row_start[r], e = es.begin() + row_start[r + 1];
+    for (int s = 0; s < P->nseg; ++s) {
+      const int c0 = s * P->segw, c1 = std::min(ncols, c0 + P->segw);
+      auto lo = std::lower_bound(b, e, c0 - K2 + 1, [](const E& x, int v) { return x.ws < v; });
+      auto hi = std::lower_bound(b, e, c1, [](const E& x, int v) { return x.ws < v; });
+      segr[(size_t)r * P->nseg + s] = make_int2((int)(lo - es.begin()), (int)(hi - es.begin()));
+    }
+  }
+
+  // ---- deapodisation (nufft.py:367-371), normalised by psi_hat(0) --------
+  std::vector<float> dp0(P->N0, 1.0f), dp1(P->N1);
+  auto deapod = [](const Window& w, int N, std::vector<float>& dp) {
+    const double s0 = kb_psihat(w, 0.0);
+    for (int jw = 0; jw < N; ++jw) {
+      const int j = jw < N / 2 ? jw : jw - N;
+      dp[jw] = (float)(s0 / (2.0 * M_PI * w.c_eff * kb_psi(w, 2.0 * M_PI * j / N)));
+    }
+  };
+  if (d->n_lat == 2) deapod(wrow, P->N0, dp0);
+  deapod(wcol, P->N1, dp1);
+
+  // ---- lateral frequency tables (recon.py:200-215) ------------------------
+  std::vector<double> jt0(P->N0, 0.0), jt1(P->N1h);
+  if (d->n_lat == 2)
+    for (int k = 0; k < P->N0; ++k) jt0[k] = jterm(k, P->N0, d->lat_ratio[0]);
+  for (int k = 0; k < P->N1h; ++k) jt1[k] = jterm(k, P->N1, d->lat_ratio[d->n_lat - 1]);
+
+  // ---- NER tables ---------------------------------------------------------
+  const Window& wt = P->win_t;
+  const double norm_t = 1.0 / (2.0 * M_PI * wt.c_eff);  // nufft.py:284
+  const double psh0 = kb_psihat(wt, 0.0);
+  std::vector<float> iw(n_ext);
+  for (int i = 0; i < n_ext; ++i) {
+    const double th = 2.0 * M_PI * i / n_ext - M_PI;  // nufft.py:281
+    iw[i] = (float)(psh0 * norm_t / kb_psi(wt, th));
+  }
+  std::vector<float2> twf(P->n_over_t), twi(P->fused_ifft ? P->Tu : 1);
+  for (int k = 0; k < P->n_over_t; ++k) {
+    const double a = -2.0 * M_PI * k / P->n_over_t;
+    twf[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  if (P->fused_ifft)
+    for (int k = 0; k < P->Tu; ++k) {
+      const double a = 2.0 * M_PI * k / P->Tu;
+      twi[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+
+  // ---- device buffers -----------------------------------------------------
+  int rc;
+  if ((rc = upload(&P->d_entries, ent))) return rc;
+  if ((rc = upload(&P->d_colw, colw))) return rc;
+  if ((rc = upload(&P->d_segr, segr))) return rc;
+  if ((rc = upload(&P->d_dp0, dp0))) return rc;
+  if ((rc = upload(&P->d_dp1, dp1))) return rc;
+  if ((rc = upload(&P->d_jt0, jt0))) return rc;
+  if ((rc = upload(&P->d_jt1, jt1))) return rc;
+  if ((rc = upload(&P->d_iw, iw))) return rc;
+  if ((rc = upload(&P->d_twf, twf))) return rc;
+  if ((rc = upload(&P->d_twi, twi))) return rc;
+  const size_t ncols_h = (size_t)ncols / 2 + 1;
+  if ((rc = dalloc(&P->d_grid, (size_t)nrows * ncols * T))) return rc;
+  if ((rc = dalloc(&P->d_X, (size_t)nrows * ncols_h * T))) return rc;
+  if ((rc = dalloc(&P->d_gh, (size_t)P->N0 * P->N1h * T))) return rc;
+  if ((rc = dalloc(&P->d_z, (size_t)P->N0u * P->N1uh * P->Tu))) return rc;
+
+  CUDA_TRY(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  for (auto& e : P->ev) CUDA_TRY(cudaEventCreate(&e));
+
+  // ---- cuFFT plans --------------------------------------------------------
+  {
+    int n[2], inem[2], onem[2];
+    const int rank = d->n_lat;
+    if (rank == 2) {
+      n[0] = nrows; n[1] = ncols;
+      inem[0] = nrows; inem[1] = ncols;
+      onem[0] = nrows; onem[1] = (int)ncols_h;
+    } else {
+      n[0] = ncols; inem[0] = ncols; onem[0] = (int)ncols_h;
+    }
+    CUFFT_TRY(cufftPlanMany(&P->fft_r2c, rank, n, inem, T, 1, onem, T, 1, CUFFT_R2C, T));
+    P->have_r2c = true;
+    CUFFT_TRY(cufftSetStream(P->fft_r2c, P->stream));
+    if (rank == 2) {
+      n[0] = P->N0u; n[1] = P->N1u;
+      inem[0] = P->N0u; inem[1] = P->N1uh;
+      onem[0] = P->N0u; onem[1] = P->N1u;
+    } else {
+      n[0] = P->N1u; inem[0] = P->N1uh; onem[0] = P->N1u;
+    }
+    CUFFT_TRY(cufftPlanMany(&P->fft_c2r, rank, n, inem, P->Tu, 1, onem, P->Tu, 1, CUFFT_C2R, P->Tu));
+    P->have_c2r = true;
+    CUFFT_TRY(cufftSetStream(P->fft_c2r, P->stream));
+    if (!P->fused_ifft) {
+      int nl[1] = {P->Tu};
+      CUFFT_TRY(cufftPlanMany(&P->fft_l, 1, nl, nl, 1, P->Tu, nl, 1, P->Tu, CUFFT_C2C, P->N0u * P->N1uh));
+      P->have_l = true;
+      CUFFT_TRY(cufftSetStream(P->fft_l, P->stream));
+    }
+  }
+
+  // ---- NER parameter block -----------------------------------------------
+  NerParams& q = P->ner;
+  q.gh = P->d_gh;
+  q.z = P->d_z;
+  q.iw = P->d_iw;
+  q.twf = P->d_twf;
+  q.twi = P->d_twi;
+  q.jt0 = P->d_jt0;
+  q.jt1 = P->d_jt1;
+  q.T = T;
+  q.n_over = P->n_over_t;
+  q.log_n_over = ilog2(P->n_over_t);
+  q.Tu = P->Tu;
+  q.log_tu = P->fused_ifft ? ilog2(P->Tu) : 0;
+  q.N0 = P->N0;
+  q.N1 = P->N1;
+  q.N1h = P->N1h;
+  q.N0u = P->N0u;
+  q.N1uh = P->N1uh;
+  q.up = P->up;
+  q.n_lat = P->n_lat;
+  q.fused_ifft = P->fused_ifft ? 1 : 0;
+  q.c_eff = wt.c_eff;
+  q.inv_c = (float)(1.0 / wt.c_eff);
+  q.alpha = (float)wt.alpha;
+  q.beta = (float)wt.beta;
+  const double s0 = wt.alpha * wt.beta;
+  q.s0 = (float)s0;
+  q.s0_over_sinh_s0 = (float)(s0 / std::sinh(s0));
+  q.inv_one_minus_e2s0 = (float)(1.0 / (1.0 - std::exp(-2.0 * s0)));
+  q.scale = (float)(1.0 / (double(P->N0) * double(P->N1) * double(T)));
+  for (int j = 0; j < kMaxTaps; ++j) {
+    const double a = M_PI * double(j - K + 1) / wt.c_eff;
+    q.tap_phase[j] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+
+  *out = P.release();
+  return PATFFT_OK;
+}
+
+int patfft_nedner_output_shape(const patfft_nedner_plan* P, int64_t shape[3]) {
+  if (!P || !shape) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  if (P->n_lat == 2) {
+    shape[0] = P->N0u;
+    shape[1] = P->N1u;
+    shape[2] = P->Tu;
+    return 3;
+  }
+  shape[0] = P->N1u;
+  shape[1] = P->Tu;
+  return 2;
+}
+
+static int execute_device_locked(patfft_nedner_plan* P, const float* samples, float* image, cudaStream_t st) {
+  const bool prof = P->profiling;
+  if (prof) CUDA_TRY(cudaEventRecord(P->ev[0], st));
+  SpreadParams sp;
+  sp.samples = samples;
+  sp.entries = P->d_entries;
+  sp.colw = P->d_colw;
+  sp.seg_range = P->d_segr;
+  sp.grid = P->d_grid;
+  sp.T = P->T;
+  sp.ncols = P->ncols;
+  sp.nseg = P->nseg;
+  sp.segw = P->segw;
+  CUDA_TRY(launch_spread(sp, P->K2, P->nrows, st));
+  if (prof) CUDA_TRY(cudaEventRecord(P->ev[1], st));
+  CUFFT_TRY(cufftSetStream(P->fft_r2c, st));
+  CUFFT_TRY(cufftExecR2C(P->fft_r2c, P->d_grid, reinterpret_cast<cufftComplex*>(P->d_X)));
+  if (prof) CUDA_TRY(cudaEventRecord(P->ev[2], st));
+  CropParams cp;
+  cp.X = P->d_X;
+  cp.gh = P->d_gh;
+  cp.dp0 = P->d_dp0;
+  cp.dp1 = P->d_dp1;
+  cp.T = P->T;
+  cp.N0 = P->N0;
+  cp.N1 = P->N1;
+  cp.N1h = P->N1h;
+  cp.nrows = P->nrows;
+  cp.ncols_h = P->ncols / 2 + 1;
+  CUDA_TRY(launch_crop(cp, st));
+  if (prof) CUDA_TRY(cudaEventRecord(P->ev[3], st));
+  if (P->up > 1 || !P->fused_ifft)
+    CUDA_TRY(cudaMemsetAsync(P->d_z, 0, sizeof(float2) * (size_t)P->N0u * P->N1uh * P->Tu, st));
+  CUDA_TRY(launch_ner(P->ner, P->K2, st));
+  if (!P->fused_ifft) {
+    CUFFT_TRY(cufftSetStream(P->fft_l, st));
+    CUFFT_TRY(cufftExecC2C(P->fft_l, reinterpret_cast<cufftComplex*>(P->d_z),
+                           reinterpret_cast<cufftComplex*>(P->d_z), CUFFT_INVERSE));
+  }
+  if (prof) CUDA_TRY(cudaEventRecord(P->ev[4], st));
+  CUFFT_TRY(cufftSetStream(P->fft_c2r, st));
+  CUFFT_TRY(cufftExecC2R(P->fft_c2r, reinterpret_cast<cufftComplex*>(P->d_z), image));
+  if (prof) {
+    CUDA_TRY(cudaEventRecord(P->ev[5], st));
+    CUDA_TRY(cudaEventSynchronize(P->ev[5]));
+    for (int s = 0; s < PATFFT_N_STAGES; ++s) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, P->ev[s], P->ev[s + 1]));
+      P->stage_ms[s] += ms;
+      P->stage_launches[s] += 1;
+    }
+  }
+  return PATFFT_OK;
+}
+
+int patfft_nedner_execute_device(patfft_nedner_plan* P, const float* samples, float* image, void* stream) {
+  if (!P || !samples || !image) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+  return execute_device_locked(P, samples, image, st);
+}
+
+int patfft_nedner_execute_frames_device(patfft_nedner_plan* P, int n_frames, const float* samples, float* images,
+                                        void* stream) {
+  if (!P || !samples || !images || n_frames < 0) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+  const size_t in_sz = (size_t)P->M * P->T, out_sz = (size_t)P->N0u * P->N1u * P->Tu;
+  for (int f = 0; f < n_frames; ++f) {
+    int rc = execute_device_locked(P, samples + f * in_sz, images + f * out_sz, st);
+    if (rc) return rc;
+  }
+  return PATFFT_OK;
+}
+
+int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* image, double* imag_residual) {
+  if (!P || !samples || !image) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  const size_t in_n = (size_t)P->M * P->T, out_n = (size_t)P->N0u * P->N1u * P->Tu;
+  int rc;
+  if (!P->d_samples && (rc = dalloc(&P->d_samples, in_n))) return rc;
+  if (!P->d_samples64 && (rc = dalloc(&P->d_samples64, in_n))) return rc;
+  if (!P->d_out && (rc = dalloc(&P->d_out, out_n))) return rc;
+  if (!P->d_out64 && (rc = dalloc(&P->d_out64, out_n))) return rc;
+  cudaStream_t st = P->stream;
+  CUDA_TRY(cudaMemcpyAsync(P->d_samples64, samples, in_n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_f64_to_f32(P->d_samples64, P->d_samples, in_n, st));
+  if ((rc = execute_device_locked(P, P->d_samples, P->d_out, st))) return rc;
+  CUDA_TRY(launch_f32_to_f64(P->d_out, P->d_out64, out_n, st));
+  CUDA_TRY(cudaMemcpyAsync(image, P->d_out64, out_n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (imag_residual) *imag_residual = 0.0;
+  return PATFFT_OK;
+}
+
+void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  if (P->stream) cudaStreamSynchronize(P->stream);
+  if (P->have_r2c) cufftDestroy(P->fft_r2c);
+  if (P->have_c2r) cufftDestroy(P->fft_c2r);
+  if (P->have_l) cufftDestroy(P->fft_l);
+  for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_X, (void*)P->d_gh,
+                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_entries, (void*)P->d_colw,
+                  (void*)P->d_segr, (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_twf,
+                  (void*)P->d_twi, (void*)P->d_jt0, (void*)P->d_jt1})
+    free_dev(p);
+  for (auto& e : P->ev)
+    if (e) cudaEventDestroy(e);
+  if (P->stream) cudaStreamDestroy(P->stream);
+  delete P;
+}
+
+int patfft_nedner_set_profiling(patfft_nedner_plan* P, int enabled) {
+  if (!P) return fail(PATFFT_ERR_PARAMETER, "null plan");
+  std::lock_guard<std::mutex> lk(P->mu);
+  P->profiling = enabled != 0;
+  for (int s = 0; s < PATFFT_N_STAGES; ++s) {
+    P->stage_ms[s] = 0.0;
+    P->stage_launches[s] = 0;
+  }
+  return PATFFT_OK;
+}
+
+int patfft_nedner_stage_times(patfft_nedner_plan* P, double* ms, int64_t* launches, int n) {
+  if (!P) return fail(PATFFT_ERR_PARAMETER, "null plan");
+  std::lock_guard<std::mutex> lk(P->mu);
+  for (int s = 0; s < n && s < PATFFT_N_STAGES; ++s) {
+    if (ms) ms[s] = P->stage_ms[s];
+    if (launches) launches[s] = P->stage_launches[s];
+  }
+  return PATFFT_OK;
+}
+
+const char* patfft_nedner_stage_name(int s) {
+  static const char* names[PATFFT_N_STAGES] = {"spread", "lateral_fft", "crop", "ner", "inverse_fft"};
+  return (s >= 0 && s < PATFFT_N_STAGES) ? names[s] : "";
+}
+
+int patfft_nedner_stage_bytes(const patfft_nedner_plan* P, double* bytes, int n) {
+  if (!P || !bytes) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  const double T = P->T, Tu = P->Tu;
+  const double grid = (double)P->nrows * P->ncols;
+  const double gh_rows = (double)P->N0 * P->N1h;
+  const double v[PATFFT_N_STAGES] = {
+      4.0 * T * ((double)P->M + grid),                                  // spread: samples in + real grid out
+      (4.0 + 8.0 * (P->ncols / 2 + 1) / (double)P->ncols) * grid * T,   // R2C: real in + half complex out
+      8.0 * gh_rows * T * 2.0,                                          // crop: read + write needed half rows
+      8.0 * gh_rows * T + 8.0 * (double)P->N0u * P->N1uh * Tu,          // NER: gh rows in, z rows out
+      8.0 * (double)P->N0u * P->N1uh * Tu + 4.0 * (double)P->N0u * P->N1u * Tu};  // C2R
+  for (int s = 0; s < n && s < PATFFT_N_STAGES; ++s) bytes[s] = v[s];
+  return PATFFT_OK;
+}
+
+int patfft_nedner_launches_per_execute(const patfft_nedner_plan* P, int* own, int* library) {
+  if (!P) return fail(PATFFT_ERR_PARAMETER, "null plan");
+  if (own) *own = 3;  // spread, crop, ner
+  if (library) *library = -1;  // cuFFT kernels: counted by the caller from the launch list
+  return PATFFT_OK;
+}
+
+// ---- helpers ---------------------------------------------------------------
+int patfft_device_count(int* count) {
+  CUDA_TRY(cudaGetDeviceCount(count));
+  return PATFFT_OK;
+}
+int patfft_device_alloc(int device, size_t bytes, void** ptr) {
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaMalloc(ptr, bytes));
+  return PATFFT_OK;
+}
+int patfft_device_free(void* ptr) {
+  CUDA_TRY(cudaFree(ptr));
+  return PATFFT_OK;
+}
+int patfft_host_alloc(size_t bytes, void** ptr) {
+  CUDA_TRY(cudaHostAlloc(ptr, bytes, cudaHostAllocDefault));
+  return PATFFT_OK;
+}
+int patfft_host_free(void* ptr) {
+  CUDA_TRY(cudaFreeHost(ptr));
+  return PATFFT_OK;
+}
+int patfft_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
+  return PATFFT_OK;
+}
+int patfft_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+  return PATFFT_OK;
+}
+int patfft_stream_sync(void* stream) {
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return PATFFT_OK;
+}
+int patfft_plan_stream(const patfft_nedner_plan* P, void** stream) {
+  if (!P || !stream) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  *stream = P->stream;
+  return PATFFT_OK;
+}
+int patfft_convert_f64_to_f32(const double* src, float* dst, size_t n, void* stream) {
+  CUDA_TRY(launch_f64_to_f32(src, dst, n, static_cast<cudaStream_t>(stream)));
+  return PATFFT_OK;
+}
+int patfft_convert_f32_to_f64(const float* src, double* dst, size_t n, void* stream) {
+  CUDA_TRY(launch_f32_to_f64(src, dst, n, static_cast<cudaStream_t>(stream)));
+  return PATFFT_OK;
+}
+int patfft_l2_flush(void* scratch, size_t bytes, void* stream) {
+  CUDA_TRY(launch_fill(static_cast<float*>(scratch), bytes / sizeof(float), 0.f, static_cast<cudaStream_t>(stream)));
+  return PATFFT_OK;
+}
+int patfft_event_create(void** ev) {
+  cudaEvent_t e;
+  CUDA_TRY(cudaEventCreate(&e));
+  *ev = e;
+  return PATFFT_OK;
+}
+int patfft_event_record(void* ev, void* stream) {
+  CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream)));
+  return PATFFT_OK;
+}
+int patfft_event_elapsed_ms(void* a, void* b, float* ms) {
+  CUDA_TRY(cudaEventSynchronize(static_cast<cudaEvent_t>(b)));
+  CUDA_TRY(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(a), static_cast<cudaEvent_t>(b)));
+  return PATFFT_OK;
+}
+int patfft_event_destroy(void* ev) {
+  CUDA_TRY(cudaEventDestroy(static_cast<cudaEvent_t>(ev)));
+  return PATFFT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,135 @@
+// Internal declarations shared by the host plan builder, the kernels and
+// the C ABI.  Not part of the public interface (include/patfft_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/patfft_b200.h"
+
+namespace patfft {
+
+// ---------------------------------------------------------------------------
+// Window pair (reference nufft.py:92-187), evaluated in float64 on the host.
+// ---------------------------------------------------------------------------
+struct Window {
+  double c_eff = 2.0;  // effective oversampling the window is resolved for
+  int K = 6;           // half-width; 2K taps
+  double alpha = 0.0;  // support half-width
+  double beta = 0.0;   // shape
+};
+
+// WindowSpec.resolved(c_eff) (nufft.py:133-149).  Returns false + message
+// when the support is inadmissible (reference raises ParameterError).
+bool resolve_window(double c, int K, double alpha_or_nan, double beta_or_nan, double c_eff, Window* out,
+                    std::string* err);
+double bessel_i0(double x);                 // scipy.special.i0 equivalent
+double kb_psi(const Window& w, double th);  // window_eval (nufft.py:159-165)
+double kb_psihat(const Window& w, double x);  // window_ft_eval (nufft.py:168-187)
+int even_fast_len(double target);           // next_even_fast_len (nufft.py:83-89)
+
+// ---------------------------------------------------------------------------
+// Device-side parameter blocks
+// ---------------------------------------------------------------------------
+constexpr int kMaxTaps = 16;  // 2K <= 16 (K <= 8)
+
+struct SpreadParams {
+  const float* samples;   // [M][T] float32, already in device memory
+  const int4* entries;    // sorted by (row, ws): {m, ws, float_bits(w_row*scale), 0}
+  const float* colw;      // [M][K2] normalised column weights
+  const int2* seg_range;  // per (row, seg): [lo, hi) into entries
+  float* grid;            // [nrows][ncols][T] centred oversampled grid
+  int T, ncols, nseg, segw;
+};
+
+struct CropParams {
+  const float2* X;   // [nrows][ncols/2+1][T] R2C output of the centred grid
+  float2* gh;        // [N0][N1h][T] symmetrised lateral spectrum (wrapped j0, half j1)
+  const float* dp0;  // [N0] deapodisation (wrapped index), {1} when n_lat == 1
+  const float* dp1;  // [N1]
+  int T, N0, N1, N1h, nrows, ncols_h;
+};
+
+struct NerParams {
+  const float2* gh;    // [N0][N1h][T]
+  float2* z;           // [N0u][N1uh][Tu]
+  const float* iw;     // [2T] psihat(0)*norm/psi(theta_n) (nufft.py:281-284)
+  const float2* twf;   // [n_over] exp(-2 pi i k / n_over)
+  const float2* twi;   // [Tu]    exp(+2 pi i k / Tu)
+  const double* jt0;   // [N0] (j0*ratio0)^2 on the wrapped grid (recon.py:211)
+  const double* jt1;   // [N1h]
+  int T, n_over, log_n_over, Tu, log_tu;
+  int N0, N1, N1h, N0u, N1uh, up, n_lat;
+  int fused_ifft;      // 1: inverse l-FFT in shared memory, 0: write spectrum
+  double c_eff;        // n_over / (2T)
+  float inv_c, alpha, beta, s0, s0_over_sinh_s0, inv_one_minus_e2s0;
+  float scale;         // 1/(N0*N1*T): scipy ifftn normalisation * up^d
+  float2 tap_phase[kMaxTaps];  // exp(+i pi dk / c_eff), dk = -K+1..K
+};
+
+// Kernel launchers (kernels.cu)
+cudaError_t launch_spread(const SpreadParams& p, int K2, int nrows, cudaStream_t s);
+cudaError_t launch_crop(const CropParams& p, cudaStream_t s);
+cudaError_t launch_ner(const NerParams& p, int K2, cudaStream_t s);
+size_t ner_smem_bytes(int n_over, int Tu);
+cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);
+cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s);
+cudaError_t launch_fill(float* dst, size_t n, float v, cudaStream_t s);
+
+}  // namespace patfft
+
+// ---------------------------------------------------------------------------
+// The plan (opaque to C callers)
+// ---------------------------------------------------------------------------
+struct patfft_nedner_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+
+  // sizes
+  int n_lat = 2, N0 = 1, N1 = 0, T = 0, up = 1, M = 0;
+  int nrows = 1, ncols = 0, N1h = 0;
+  int N0u = 1, N1u = 0, N1uh = 0, Tu = 0;
+  int n_over_t = 0, K2 = 12;
+  int nseg = 1, segw = 0;
+  int64_t n_entries = 0;
+  bool fused_ifft = true;
+
+  patfft::Window win_lat[2], win_t;
+
+  // device buffers
+  float* d_samples = nullptr;   // [M][T] f32 (host path staging)
+  double* d_samples64 = nullptr;
+  float* d_grid = nullptr;      // [nrows][ncols][T]
+  float2* d_X = nullptr;        // [nrows][ncols/2+1][T]
+  float2* d_gh = nullptr;       // [N0][N1h][T]
+  float2* d_z = nullptr;        // [N0u][N1uh][Tu]
+  float* d_out = nullptr;       // [N0u][N1u][Tu] f32 (host path staging)
+  double* d_out64 = nullptr;
+  int4* d_entries = nullptr;
+  float* d_colw = nullptr;
+  int2* d_segr = nullptr;
+  float* d_dp0 = nullptr;
+  float* d_dp1 = nullptr;
+  float* d_iw = nullptr;
+  float2* d_twf = nullptr;
+  float2* d_twi = nullptr;
+  double* d_jt0 = nullptr;
+  double* d_jt1 = nullptr;
+
+  cufftHandle fft_r2c = 0, fft_c2r = 0, fft_l = 0;
+  bool have_r2c = false, have_c2r = false, have_l = false;
+
+  patfft::NerParams ner{};
+
+  // profiling
+  bool profiling = false;
+  cudaEvent_t ev[PATFFT_N_STAGES + 1] = {};
+  double stage_ms[PATFFT_N_STAGES] = {};
+  int64_t stage_launches[PATFFT_N_STAGES] = {};
+};

@@ -1,0 +1,65 @@
+"""The CPU oracle pinned against the reference's own outputs (golden vectors).
+
+The goldens were produced by tests/golden/make_golden.py, which runs the
+reference implementation itself.  These tests need no GPU.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_recon_files, golden_spec, rel_l2
+from oracle import nedner_oracle as O
+
+
+@pytest.mark.parametrize("path", golden_recon_files(), ids=os.path.basename)
+def test_oracle_matches_reference_reconstruction(path):
+    g = np.load(path)
+    img, resid = O.reconstruct_nedner(g["positions"], g["weights"], g["samples"], float(g["dt"]),
+                                      float(g["sound_speed"]), float(g["dx"]), tuple(g["n_lateral"]),
+                                      out_dims=tuple(g["out_dims"]), upsample=int(g["upsample"]),
+                                      spec=golden_spec(g))
+    assert img.shape == g["values"].shape
+    assert rel_l2(img, g["values"]) <= 1e-12
+    assert resid <= 1e-9  # recon.py:256-257 meta
+
+
+def test_oracle_ner_matches_reference_and_direct_sum():
+    g = np.load(os.path.join(GOLDEN, "ner_rows.npz"))
+    plan = O.NerOracle(g["u"].shape[-1])
+    out = plan.rows(g["u"], g["kappas"])
+    assert rel_l2(out, g["out"]) <= 1e-13
+    assert rel_l2(out, g["direct"]) <= 1e-9          # SPEC.md:79-84 (<= 1e-6 required)
+    assert rel_l2(O.ner_direct(g["u"], g["kappas"]), g["direct"]) <= 1e-13
+    assert rel_l2(plan.shared(g["u"], g["kappas_shared"]), g["out_shared"]) <= 1e-13
+
+
+def test_oracle_ned_matches_reference_and_direct_sum():
+    g = np.load(os.path.join(GOLDEN, "ned_axes.npz"))
+    out1 = O.NedOracle((32,)).execute(g["pos1"], g["v1"], wrapped=False)
+    assert rel_l2(out1, g["out1"]) <= 1e-13
+    assert rel_l2(out1, g["direct1"]) <= 1e-9
+    assert rel_l2(O.ned_direct(g["pos1"], g["v1"], (32,)), g["direct1"]) <= 1e-12
+    out2 = O.NedOracle((16, 24)).execute(g["pos2"], g["v2"], wrapped=True)
+    assert rel_l2(out2, g["out2_wrapped"]) <= 1e-13
+
+
+def test_window_pair_and_warp_known_answers():
+    g = np.load(os.path.join(GOLDEN, "window_pair.npz"))
+    win = O.resolve_window(2.0, 6, None, None, 2.0)
+    assert win[2] == pytest.approx(float(g["alpha"]), rel=1e-15)
+    assert win[3] == pytest.approx(float(g["beta"]), rel=1e-15)
+    assert win[2] == pytest.approx(9.41535318280861, rel=1e-13)
+    assert win[3] == pytest.approx(2.9813866459901393, rel=1e-13)
+    assert rel_l2(O.kb_window_ft(win, g["x"]), g["ft"]) <= 1e-14
+    assert rel_l2(O.kb_window(win, g["theta"]), g["psi"]) <= 1e-14
+    assert O.even_fast_len(2 * 226) == int(g["n_over_226"]) == 462
+    assert float(g["kappa_345"]) == 5.0 and float(g["amp_345"]) == pytest.approx(1.6)
+
+
+def test_oracle_zero_data_gives_zero_image():
+    g = np.load(golden_recon_files()[0])
+    img, _ = O.reconstruct_nedner(g["positions"], g["weights"], np.zeros_like(g["samples"]), float(g["dt"]),
+                                  float(g["sound_speed"]), float(g["dx"]), tuple(g["n_lateral"]))
+    assert not np.any(img)
