@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark: reconstructed voxels/s of the NEDNER-NUFFT path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl reference]
+
+A "step" is one full reconstruction (NED spread -> lateral FFT -> crop ->
+fused NER -> inverse FFT) of one synthetic record.  ``value`` is measured
+device-resident (float32 samples already in HBM); ``e2e`` goes through the
+C ABI's host entry point (float64 host samples in pinned memory, H2D + D2H
+inside the timed region).  ``--impl reference`` times the CPU oracle (the
+restated reference algorithm, float64 numpy/scipy) on a bounded sample of
+the same workload.
+
+For N > 1 (torchrun) every rank reconstructs its own record (independent
+volumes, "replicas"; no collective on the data path) and ``value`` is the
+total voxels of all ranks over the max per-rank device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "reconstructed voxels/sec (3D NEDNER-NUFFT)"
+UNIT = "voxels/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = f"/tmp/patfft_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(name, rank=0):
+    from paper_1501_02946_b200 import synth
+
+    if name == "cfg5":
+        frames = list(synth.make_frames(seed=5 + 1000 * rank, frames=8))
+        return frames
+    seed = {"cfg1": 1, "cfg2": 2, "cfg3": 3, "cfg4": 4}[name] + 1000 * rank
+    return [synth.CONFIGS[name](seed)]
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle = restated reference), bounded sample + extrapolation
+# ---------------------------------------------------------------------------
+
+def cpu_sample_seconds(rec, frac):
+    """Time the reference algorithm on ``frac`` of the work and extrapolate.
+
+    NED: the full plan (spread operator) + SpMM/FFT/crop on frac of the time
+    samples (the operator is identical for every time sample).  NER: frac of
+    the lateral rows.  Inverse FFT: frac of the depth planes (lateral 2-D
+    IFFTs) and frac of the rows (depth IFFTs) -- the separable parts of the
+    reference's ifftn.  Returns (extrapolated full seconds, measured seconds).
+    """
+    import scipy.fft as sfft
+
+    from oracle import nedner_oracle as O
+
+    pos, w, smp = rec.positions, rec.weights, rec.samples
+    nl = tuple(rec.n_lateral)
+    nt = smp.shape[1]
+    dd = len(nl)
+    thr = int(os.environ.get("PAT_THREADS", "1"))
+    t0 = time.perf_counter()
+    scaled = smp * (w / rec.dx ** dd)[:, None]
+    ned = O.NedOracle(nl)
+    gp = pos / rec.dx
+    op = ned.spread_operator(gp)
+    t_plan = time.perf_counter() - t0
+    tf = max(1, int(round(nt * frac)))
+    t1 = time.perf_counter()
+    vb = scaled[:, :tf].astype(np.complex128)
+    grid = (op @ vb).reshape(ned.n_over + (tf,))
+    spec = sfft.fftn(grid, axes=tuple(range(dd)), workers=thr)
+    sel = [np.arange(-n // 2, n // 2) % m for n, m in zip(nl, ned.n_over)]
+    gh_part = spec[np.ix_(*sel)]
+    for ax, dp in enumerate(ned.deapod):
+        shape = [1] * gh_part.ndim
+        shape[ax] = dp.size
+        gh_part = gh_part * dp.reshape(shape)
+    gh_part = np.fft.ifftshift(gh_part, axes=tuple(range(dd)))
+    t_ned = time.perf_counter() - t1
+    # NER on frac of the lateral rows (cost is data-independent; rows carry noise)
+    rows = int(np.prod(nl))
+    rsub = max(1, int(round(rows * frac)))
+    ratios = O.lateral_ratios(nt, rec.dt, rec.sound_speed, rec.dx, nl)
+    j2 = O.lateral_freq_sq(nl, ratios).reshape(rows)[:rsub]
+    rng = np.random.default_rng(0)
+    gh_rows = rng.standard_normal((rsub, nt)) + 1j * rng.standard_normal((rsub, nt))
+    t2 = time.perf_counter()
+    fh = O.fhat_rows(gh_rows, j2, nt, (2.0, 6, None, None))
+    t_ner = time.perf_counter() - t2
+    # inverse (recon.py:249-260) on frac of the volume: Hermitian part and
+    # lateral IFFTs on frac of the depth planes, depth IFFTs on frac of rows
+    planes = max(1, int(round(nt * frac)))
+    slab = rng.standard_normal(nl + (planes,)) + 0j
+    t3 = time.perf_counter()
+    O.hermitian_part(slab)
+    lat = sfft.ifftn(slab, axes=tuple(range(dd)))
+    np.fft.fftshift(lat.real, axes=tuple(range(dd)))
+    sfft.ifft(fh, axis=-1)
+    t_inv = time.perf_counter() - t3
+    measured = t_plan + t_ned + t_ner + t_inv
+    full = t_plan + (t_ned + t_ner + t_inv) / frac
+    return full, measured
+
+
+def run_reference_arm(args):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return 0
+    os.environ.setdefault("PAT_THREADS", str(os.cpu_count() or 1))
+    recs = make_workload(args.config)
+    rec = recs[0]
+    vox = _voxels(rec)
+    frac = args.cpu_frac
+    vals = []
+    for i in range(args.warmup + args.steps):
+        full, meas = cpu_sample_seconds(rec, frac)
+        if i >= args.warmup:
+            vals.append(vox / full)
+    value = statistics.median(vals)
+    cores = int(os.environ["PAT_THREADS"])
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * vox / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": _config_json(args, rec),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": _sample_desc(args.config, frac)},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def _sample_desc(cfg, frac):
+    return (f"{cfg}, oracle (restated reference, float64 numpy/scipy, PAT_THREADS=all cores for FFTs): "
+            f"full NED plan + NED on {frac:g} of the time samples + NER on {frac:g} of the lateral rows + "
+            f"inverse FFT on {frac:g} of planes/rows, extrapolated linearly to the full step")
+
+
+def _voxels(rec):
+    return int(np.prod(rec.n_lateral)) * rec.samples.shape[1]
+
+
+def _config_json(args, rec):
+    from paper_1501_02946_b200 import synth
+
+    return {"workload": f"{args.config}: {synth.DESCRIPTIONS[args.config]}",
+            "sensors": int(rec.positions.shape[0]), "n_time": int(rec.samples.shape[1]),
+            "out_shape": list(rec.n_lateral) + [int(rec.samples.shape[1])],
+            "window": "Kaiser-Bessel c=2 K=6 (reference default)",
+            "l2": "inputs (>=268 MB at cfg4) exceed L2 and a 512 MB scratch write flushes L2 between steps",
+            "parallelism": "replicas" if args.gpus > 1 else "single-gpu"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu_arm(args):
+    rank, world, local = _env_rank()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    device = local
+    from paper_1501_02946_b200 import NedNerPlan, _lib
+
+    lib = _lib.load()
+    recs = make_workload(args.config, rank)
+    rec = recs[0]
+    plan = NedNerPlan(rec.positions, rec.weights, rec.samples.shape[1], rec.dt, rec.sound_speed, rec.dx,
+                      rec.n_lateral, device=device)
+    stream = ctypes.c_void_p(plan.stream())
+    nsamp = rec.samples.size
+    nout = int(np.prod(plan.out_shape))
+    nframes = len(recs)
+
+    def dalloc(nbytes):
+        p = ctypes.c_void_p()
+        _lib.check(lib.patfft_device_alloc(device, nbytes, ctypes.byref(p)))
+        return p
+
+    d_in = dalloc(4 * nsamp * nframes)
+    d_out = dalloc(4 * nout * nframes)
+    host32 = np.ascontiguousarray(np.stack([r.samples for r in recs]).astype(np.float32))
+    _lib.check(lib.patfft_memcpy_h2d(d_in, _lib.ptr(host32), host32.nbytes, stream))
+    _lib.check(lib.patfft_stream_sync(stream))
+    flush_bytes = 512 << 20
+    d_flush = dalloc(flush_bytes)
+    ev = []
+    for _ in range(2 * args.steps + 2):
+        e = ctypes.c_void_p()
+        _lib.check(lib.patfft_event_create(ctypes.byref(e)))
+        ev.append(e)
+
+    def step():
+        if nframes == 1:
+            plan.execute_device(d_in.value, d_out.value, stream.value)
+        else:
+            plan.execute_frames_device(nframes, d_in.value, d_out.value, stream.value)
+
+    for _ in range(args.warmup):
+        step()
+    _lib.check(lib.patfft_stream_sync(stream))
+
+    plan.set_profiling(True)
+    clocks = Clocks(device)
+    if dist is not None:
+        dist.barrier()
+    _lib.check(lib.patfft_stream_sync(stream))
+    clocks.start()
+    times = []
+    for i in range(args.steps):
+        _lib.check(lib.patfft_l2_flush(d_flush, flush_bytes, stream))
+        _lib.check(lib.patfft_event_record(ev[2 * i], stream))
+        step()
+        _lib.check(lib.patfft_event_record(ev[2 * i + 1], stream))
+        ms = ctypes.c_float()
+        _lib.check(lib.patfft_event_elapsed_ms(ev[2 * i], ev[2 * i + 1], ctypes.byref(ms)))
+        times.append(ms.value)
+    _lib.check(lib.patfft_stream_sync(stream))
+    clk = clocks.stop()
+    if dist is not None:
+        dist.barrier()
+    stages = plan.stage_times()
+    plan.set_profiling(False)
+    ms_step = float(np.mean(times))
+    if dist is not None:
+        import torch
+
+        t = torch.tensor([ms_step], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    vox = _voxels(rec) * nframes
+    value = vox * world / (ms_step / 1e3)
+
+    # ---- end-to-end through the host entry point (pinned f64 buffers) ----
+    e2e = None
+    if nframes == 1:
+        hin, hout = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(lib.patfft_host_alloc(8 * nsamp, ctypes.byref(hin)))
+        _lib.check(lib.patfft_host_alloc(8 * nout, ctypes.byref(hout)))
+        hin_np = np.ctypeslib.as_array(ctypes.cast(hin, ctypes.POINTER(ctypes.c_double)), shape=(nsamp,))
+        hin_np[:] = rec.samples.ravel()
+        resid = ctypes.c_double()
+        for _ in range(max(1, args.warmup)):
+            _lib.check(lib.patfft_nedner_execute(plan.handle, hin, hout, ctypes.byref(resid)))
+        if dist is not None:
+            dist.barrier()
+        et = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            _lib.check(lib.patfft_nedner_execute(plan.handle, hin, hout, ctypes.byref(resid)))
+            et.append(time.perf_counter() - t0)
+        e2e_s = float(np.mean(et))
+        if dist is not None:
+            import torch
+
+            t = torch.tensor([e2e_s], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": vox * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * nsamp,
+               "d2h_bytes_per_step": 8 * nout, "ms_per_step": 1e3 * e2e_s,
+               "path": "patfft_nedner_execute (C ABI): pinned f64 host -> device -> pinned f64 host"}
+        lib.patfft_host_free(hin)
+        lib.patfft_host_free(hout)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant own kernel ----
+    peak, peak_kind = _peaks()
+    sbytes = plan.stage_bytes()
+    own = ["spread", "crop", "ner"]
+    per = {k: (stages[k][0] / max(1, stages[k][1])) for k in stages}
+    dom = max(own, key=lambda k: per[k])
+    ach = sbytes[dom] / (per[dom] / 1e3) / 1e9
+    traffic = _traffic_from_profiles(args.config, dom)
+    roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "peak_source": peak_kind, "traffic": traffic, "algorithmic_bytes": sbytes[dom],
+            "launch_ms": per[dom]}
+    stage_report = {k: {"ms": per[k], "share": per[k] / sum(per.values()),
+                        "GBps": sbytes[k] / (per[k] / 1e3) / 1e9 if per[k] > 0 else None} for k in per}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        os.environ.setdefault("PAT_THREADS", str(os.cpu_count() or 1))
+        full, meas = cpu_sample_seconds(rec, args.cpu_frac)
+        cpu = {"value": _voxels(rec) / full, "unit": UNIT, "cores": int(os.environ["PAT_THREADS"]),
+               "kind": "port", "sample": _sample_desc(args.config, args.cpu_frac), "measured_s": meas}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32/c64", "data": "synthetic (seeded, BASELINE config shapes)",
+        "config": _config_json(args, rec), "clocks": clk, "roofline": roof, "stages": stage_report,
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 3 * args.steps * nframes,
+        "gpu_launches_note": "own kernels (spread, crop, ner) per step; cuFFT R2C/C2R launches not counted",
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def _traffic_from_profiles(cfg, kernel):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(cfg, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-frac", type=float, default=1.0 / 16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

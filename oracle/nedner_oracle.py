@@ -275,10 +275,14 @@ def even_extension(gh):
     return np.concatenate([gh, pad, gh[..., :0:-1]], axis=-1)
 
 
-def ner_targets(n_lateral, nt, ratios):
-    """kappa_e = 2*kappa on the band, 0 off it; also amp*band (recon.py:282-293)."""
+def ner_targets(j2, nt):
+    """kappa_e = 2*kappa on the band, 0 off it; and amp*band (recon.py:282-293).
+
+    ``j2`` holds the squared lateral frequency of each row (any shape); the
+    returned arrays have shape ``j2.shape + (nt,)``.
+    """
     lv = wrapped_freqs(nt)
-    j2 = lateral_freq_sq(n_lateral, ratios)[..., None]
+    j2 = np.asarray(j2)[..., None]
     kap = np.sign(lv) * np.sqrt(j2 + lv ** 2)
     band = (j2 + lv ** 2) <= (nt / 2.0) ** 2
     amp = np.zeros(kap.shape)
@@ -286,22 +290,23 @@ def ner_targets(n_lateral, nt, ratios):
     return np.where(band, 2.0 * kap, 0.0), amp * band
 
 
-def assemble_fhat(gh, nt, spec, ratios, rows=None):
-    """Warped time-axis NER + amplitude + band (recon.py:274-308, 'nufft' branch).
+def fhat_rows(gh_rows, j2_rows, nt, spec):
+    """Steps 2-3 for a set of lateral rows (recon.py:282-308, 'nufft' branch).
 
-    ``rows`` optionally restricts the NER to a subset of flattened lateral
-    rows (used only for the bounded CPU-baseline sample); the others stay 0.
+    gh_rows: (R, nt) lateral spectra; j2_rows: (R,) squared lateral frequency.
     """
+    kap_e, scale = ner_targets(j2_rows, nt)
+    ext = even_extension(gh_rows)
+    phi = NerOracle(2 * nt, *spec).rows(ext, kap_e)
+    return 0.5 * phi * scale
+
+
+def assemble_fhat(gh, nt, spec, ratios):
+    """Warped time-axis NER + amplitude + band over the whole lateral grid (recon.py:274-308)."""
     n_lateral = gh.shape[:-1]
-    kap_e, scale = ner_targets(n_lateral, nt, ratios)
     nrows = int(np.prod(n_lateral)) if n_lateral else 1
-    ext = even_extension(gh).reshape(nrows, 2 * nt)
-    plan = NerOracle(2 * nt, *spec)
-    ke = kap_e.reshape(nrows, nt)
-    phi = np.zeros((nrows, nt), dtype=np.complex128)
-    sel = slice(None) if rows is None else rows
-    phi[sel] = plan.rows(ext[sel], ke[sel])
-    return 0.5 * phi.reshape(kap_e.shape) * scale
+    j2 = lateral_freq_sq(n_lateral, ratios).reshape(nrows)
+    return fhat_rows(gh.reshape(nrows, nt), j2, nt, spec).reshape(gh.shape)
 
 
 def hermitian_part(a):
