@@ -101,14 +101,19 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* plan);
  * every execute records one event per stage boundary; patfft_nedner_stage_times
  * returns the accumulated milliseconds per stage and the launch count per
  * stage since the last reset, and the stage names via patfft_nedner_stage_name. */
-enum { PATFFT_STAGE_SPREAD = 0, PATFFT_STAGE_LATERAL_FFT = 1, PATFFT_STAGE_CROP = 2,
-       PATFFT_STAGE_NER = 3, PATFFT_STAGE_INVERSE_FFT = 4, PATFFT_N_STAGES = 5 };
+enum { PATFFT_STAGE_SPREAD = 0,       /* NED gridding onto the oversampled plane      */
+       PATFFT_STAGE_LATERAL_COL = 1,  /* real FFT along grid columns (half kept)      */
+       PATFFT_STAGE_LATERAL_ROW = 2,  /* FFT along rows + crop + deapodise + Nyquist  */
+       PATFFT_STAGE_NER = 3,          /* fused NER + epilogue + depth inverse FFT     */
+       PATFFT_STAGE_INVERSE = 4,      /* lateral inverse FFT (C2R) to the image       */
+       PATFFT_N_STAGES = 5 };
 int patfft_nedner_set_profiling(patfft_nedner_plan* plan, int enabled);
 int patfft_nedner_stage_times(patfft_nedner_plan* plan, double* ms, int64_t* launches, int n);
 const char* patfft_nedner_stage_name(int stage);
 /* Algorithmic bytes per launch of each stage (roofline table). */
 int patfft_nedner_stage_bytes(const patfft_nedner_plan* plan, double* bytes, int n);
-/* Number of kernels (own + cuFFT) one execute_device launches. */
+/* Number of kernels one execute_device launches: own sm_100a kernels and
+ * library (cuFFT) kernels (the latter only on fallback sizes). */
 int patfft_nedner_launches_per_execute(const patfft_nedner_plan* plan, int* own, int* library);
 
 /* ---- small runtime helpers used by the Python shim and bench.py ---------- */

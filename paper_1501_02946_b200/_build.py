@@ -13,8 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpatfft_b200.so")
-SOURCES = ["capi.cu", "kernels.cu", "window.cpp"]
-HEADERS = ["patfft_internal.h"]
+SOURCES = ["capi.cu", "spread.cu", "lateral.cu", "ner.cu", "util.cu", "window.cpp"]
+HEADERS = ["patfft_internal.h", "fft_smem.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",

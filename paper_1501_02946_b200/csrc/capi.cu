@@ -5,9 +5,9 @@
 // resolved windows, deapodisation, spreading taps) and NerPlan
 // (nufft.py:273-285: oversampled length, pre-window, tap norm), plus the
 // lateral frequency tables of recon.py:200-215/282.  The spreading taps are
-// reorganised for the GPU: per oversampled grid row, the contributing
-// (sensor, row weight, column window) entries sorted by column, split into
-// column segments for load balance.
+// reorganised for the GPU: per group of R oversampled grid rows, one record
+// per contributing sensor (R row weights, 2K column weights, column window),
+// sorted by column window and split into column segments for load balance.
 #include <cuda_runtime.h>
 #include <cufft.h>
 
@@ -16,16 +16,10 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
-#include <numeric>
 #include <string>
 #include <vector>
 
 #include "patfft_internal.h"
-
-namespace patfft {
-void spread_config(int K2, int T, int* bdim, int* tpt, int* tchunks);
-int ner_threads(int n_over);
-}  // namespace patfft
 
 using namespace patfft;
 
@@ -38,29 +32,33 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
-#define CUDA_TRY(expr)                                                                         \
-  do {                                                                                         \
-    cudaError_t _e = (expr);                                                                   \
-    if (_e != cudaSuccess)                                                                     \
-      return fail(PATFFT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));       \
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(PATFFT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
-#define CUFFT_TRY(expr)                                                                        \
-  do {                                                                                         \
-    cufftResult _r = (expr);                                                                   \
-    if (_r != CUFFT_SUCCESS)                                                                   \
+#define CUFFT_TRY(expr)                                                                          \
+  do {                                                                                           \
+    cufftResult _r = (expr);                                                                     \
+    if (_r != CUFFT_SUCCESS)                                                                     \
       return fail(PATFFT_ERR_CUDA, std::string(#expr) + ": cufft error " + std::to_string(_r)); \
   } while (0)
 
 int64_t pmod(int64_t a, int64_t m) { return ((a % m) + m) % m; }
 int64_t floordiv(int64_t a, int64_t b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
 int64_t ceildiv(int64_t a, int64_t b) { return -floordiv(-a, b); }
-
 bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 int ilog2(int64_t n) {
   int l = 0;
   while ((int64_t(1) << l) < n) ++l;
   return l;
+}
+int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
 }
 
 template <typename T>
@@ -91,9 +89,70 @@ void axis_taps(double x, const Window& w, int n_over, int* start, double* wt) {
 
 // fftfreq(n)[k]*n*ratio squared, with numpy's rounding (recon.py:211)
 double jterm(int kw, int n, double ratio) {
-  const int ks = (kw < (n + 1) / 2) ? kw : kw - n;  // fftfreq integer for wrapped index
+  const int ks = (kw < (n + 1) / 2) ? kw : kw - n;
   const double v = (double(ks) * (1.0 / double(n))) * double(n) * ratio;
   return v * v;
+}
+
+// Interpolating polynomial of degree D through Chebyshev nodes on
+// [-1/2, 1/2] (monomial coefficients in z), fp64 Gaussian elimination.
+template <class F>
+std::vector<double> cheb_fit(F f, int D) {
+  const int n = D + 1;
+  std::vector<double> A((size_t)n * n), b(n);
+  for (int i = 0; i < n; ++i) {
+    const double z = 0.5 * std::cos(M_PI * (i + 0.5) / n);
+    double zp = 1.0;
+    for (int j = 0; j < n; ++j) {
+      A[(size_t)i * n + j] = zp;
+      zp *= z;
+    }
+    b[i] = f(z);
+  }
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs(A[(size_t)r * n + c]) > std::fabs(A[(size_t)piv * n + c])) piv = r;
+    for (int j = 0; j < n; ++j) std::swap(A[(size_t)c * n + j], A[(size_t)piv * n + j]);
+    std::swap(b[c], b[piv]);
+    for (int r = c + 1; r < n; ++r) {
+      const double fct = A[(size_t)r * n + c] / A[(size_t)c * n + c];
+      for (int j = c; j < n; ++j) A[(size_t)r * n + j] -= fct * A[(size_t)c * n + j];
+      b[r] -= fct * b[c];
+    }
+  }
+  std::vector<double> x(n);
+  for (int r = n - 1; r >= 0; --r) {
+    double acc = b[r];
+    for (int j = r + 1; j < n; ++j) acc -= A[(size_t)r * n + j] * x[j];
+    x[r] = acc / A[(size_t)r * n + r];
+  }
+  return x;
+}
+
+// NER tap polynomials: P_j(z) = psihat((z + K - 1/2 - j)/c)/psihat(0), z = f - 1/2.
+// Returns the max abs error on a fine grid.
+double fit_ner_poly(const Window& w, int D, NerParams* q) {
+  const double norm = 1.0 / kb_psihat(w, 0.0);
+  double worst = 0.0;
+  for (int j = 0; j < kMaxTaps / 2; ++j)
+    for (int d = 0; d <= kMaxPolyDegree; ++d) q->poly[j][d] = 0.f;
+  for (int j = 0; j < w.K; ++j) {
+    const double a = w.K - 0.5 - j;
+    auto f = [&](double z) { return kb_psihat(w, (z + a) / w.c_eff) * norm; };
+    const std::vector<double> c = cheb_fit(f, D);
+    for (int d = 0; d <= D; ++d) q->poly[j][d] = (float)c[d];
+    for (int i = 0; i <= 400; ++i) {
+      const double z = -0.5 + i / 400.0;
+      for (double zz : {z, -z}) {
+        double v = 0.0;
+        for (int d = D; d >= 0; --d) v = v * zz + (double)q->poly[j][d];
+        const double ex = kb_psihat(w, (zz + a) / w.c_eff) * norm;
+        worst = std::max(worst, std::fabs(v - ex));
+      }
+    }
+  }
+  return worst;
 }
 
 void free_dev(void* p) {
@@ -105,7 +164,7 @@ void free_dev(void* p) {
 extern "C" {
 
 const char* patfft_last_error(void) { return g_err.c_str(); }
-const char* patfft_version(void) { return "patfft-b200 0.1.0 (sm_100a)"; }
+const char* patfft_version(void) { return "patfft-b200 0.2.0 (sm_100a)"; }
 
 int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, const double* sscale, int device,
                               patfft_nedner_plan** out) {
@@ -142,25 +201,28 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
   P->Tu = P->T * P->up;
   const int K = d->spec_K;
   const double c = d->spec_c;
+  std::string err;
 
   // ---- lateral oversampled sizes and windows (nufft.py:360-363) ----------
-  int n_over_lat[2] = {1, 1};
-  double ceff_min = 1e300;
-  for (int a = 0; a < d->n_lat; ++a) {
-    const int N = d->out_dims[a];
-    int n = even_fast_len(c * N);
-    if (a == d->n_lat - 1)  // column axis: the spread ring works in groups of 4
-      while (n % 4) n = even_fast_len(n + 1);
-    n_over_lat[a] = n;
-    ceff_min = std::min(ceff_min, double(n) / N);
+  // The reference rounds c*N up to an even 11-smooth length; the GPU rounds
+  // up to a power of two (shared-memory radix-16 FFTs) and resolves the
+  // window for that effective oversampling exactly as the reference does for
+  // its own length.  The two coincide for power-of-two grids.
+  {
+    double ceff_ref_min = 1e300;
+    for (int a = 0; a < d->n_lat; ++a)
+      ceff_ref_min = std::min(ceff_ref_min, double(even_fast_len(c * d->out_dims[a])) / d->out_dims[a]);
+    Window tmp;
+    if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, ceff_ref_min, &tmp, &err))  // nufft.py:362
+      return fail(PATFFT_ERR_PARAMETER, err);
   }
-  std::string err;
-  Window wmin;
-  if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, ceff_min, &wmin, &err))
-    return fail(PATFFT_ERR_PARAMETER, err);
+  int n_over_lat[2] = {1, 1};
   for (int a = 0; a < d->n_lat; ++a) {
-    if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_lat[a]) / d->out_dims[a], &P->win_lat[a],
-                        &err))
+    int64_t n = next_pow2((int64_t)std::ceil(c * d->out_dims[a]));
+    if (n < 4) n = 4;
+    if (n > 16384) return fail(PATFFT_ERR_UNSUPPORTED, "GPU path supports oversampled lateral grids up to 16384");
+    n_over_lat[a] = (int)n;
+    if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n) / d->out_dims[a], &P->win_lat[a], &err))
       return fail(PATFFT_ERR_PARAMETER, err);
   }
   P->nrows = d->n_lat == 2 ? n_over_lat[0] : 1;
@@ -170,85 +232,107 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
 
   // ---- NER window (nufft.py:273-285), power-of-two oversampled length ----
   const int n_ext = 2 * P->T;
-  int64_t n_over_t = 1;
-  while (n_over_t < (int64_t)std::ceil(c * n_ext)) n_over_t <<= 1;
+  const int64_t n_over_t = next_pow2((int64_t)std::ceil(c * n_ext));
   if (n_over_t > 16384)
     return fail(PATFFT_ERR_UNSUPPORTED, "GPU NER supports oversampled depth lengths up to 16384 (N_t <= 4096 at c=2)");
   P->n_over_t = (int)n_over_t;
   if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_t) / n_ext, &P->win_t, &err))
     return fail(PATFFT_ERR_PARAMETER, err);
   P->fused_ifft = is_pow2(P->Tu) && P->Tu <= 16384;
-  {
-    const int nth = ner_threads(P->n_over_t);
-    if (P->T > 8 * nth) return fail(PATFFT_ERR_UNSUPPORTED, "depth too long for the NER CTA layout");
-  }
+  if (P->T > 8 * ner_threads(P->n_over_t))
+    return fail(PATFFT_ERR_UNSUPPORTED, "depth too long for the NER CTA layout");
+  P->custom_inverse = is_pow2(P->N0u) && is_pow2(P->N1u) && P->N0u <= 16384 && P->N1u <= 16384 && P->N1u >= 2;
 
-  // ---- spreading entries --------------------------------------------------
+  // ---- spreading records --------------------------------------------------
   const int M = P->M, K2 = P->K2, nrows = P->nrows, ncols = P->ncols, T = P->T;
+  const int R = spread_rows_per_group(d->n_lat, K2);
+  const int RECW = spread_record_words(K2);
+  P->R = R;
+  P->ngroups = (nrows + R - 1) / R;
   std::vector<int> ucol(M), urow(M);
   std::vector<double> wcolv((size_t)M * K2), wrowv((size_t)M * K2);
-  std::vector<float> colw((size_t)M * K2);
   for (int m = 0; m < M; ++m) {
     const double xc = gpos[(size_t)m * d->n_lat + (d->n_lat - 1)];
     if (!std::isfinite(xc)) return fail(PATFFT_ERR_DATA, "sensor positions must be finite");
     axis_taps(xc, wcol, ncols, &ucol[m], &wcolv[(size_t)m * K2]);
-    for (int a = 0; a < K2; ++a) colw[(size_t)m * K2 + a] = (float)wcolv[(size_t)m * K2 + a];
     if (d->n_lat == 2) {
       const double xr = gpos[(size_t)m * 2];
       if (!std::isfinite(xr)) return fail(PATFFT_ERR_DATA, "sensor positions must be finite");
       axis_taps(xr, wrow, nrows, &urow[m], &wrowv[(size_t)m * K2]);
     }
   }
-  struct E {
-    int row, ws, m;
-    float w;
+  struct Rec {
+    int grp, ws, m;
+    float wr[4];
   };
-  std::vector<E> es;
-  es.reserve((size_t)M * (d->n_lat == 2 ? K2 : 1) + 64);
-  const int ntap_rows = d->n_lat == 2 ? K2 : 1;
-  for (int m = 0; m < M; ++m) {
-    const double sc = sscale[m];
-    for (int a = 0; a < ntap_rows; ++a) {
-      const int row = d->n_lat == 2 ? (int)pmod(urow[m] + a, nrows) : 0;
-      const double wr = (d->n_lat == 2 ? wrowv[(size_t)m * K2 + a] : 1.0) * sc;
+  std::vector<Rec> recs;
+  recs.reserve((size_t)M * ((d->n_lat == 2 ? (K2 + R - 1) / R + 1 : 1)) + 64);
+  {
+    std::vector<float> wr_acc;
+    std::vector<int> grp_seen;
+    for (int m = 0; m < M; ++m) {
+      const double sc = sscale[m];
+      // row weights of this sensor, accumulated per row group (a row can be
+      // hit twice when nrows < 2K and the taps wrap)
+      std::vector<std::pair<int, std::array<double, 4>>> groups;
+      const int ntaps = d->n_lat == 2 ? K2 : 1;
+      for (int a = 0; a < ntaps; ++a) {
+        const int row = d->n_lat == 2 ? (int)pmod(urow[m] + a, nrows) : 0;
+        const double w = (d->n_lat == 2 ? wrowv[(size_t)m * K2 + a] : 1.0) * sc;
+        const int g = row / R, r = row - g * R;
+        auto it = std::find_if(groups.begin(), groups.end(), [&](const auto& x) { return x.first == g; });
+        if (it == groups.end()) {
+          groups.push_back({g, {0.0, 0.0, 0.0, 0.0}});
+          it = groups.end() - 1;
+        }
+        it->second[r] += w;
+      }
       const int64_t ws0 = ucol[m];
       const int64_t smin = ceildiv(-(K2 - 1) - ws0, ncols), smax = floordiv(ncols - 1 - ws0, ncols);
-      for (int64_t s = smin; s <= smax; ++s) es.push_back({row, (int)(ws0 + s * ncols), m, (float)wr});
+      for (const auto& g : groups)
+        for (int64_t s = smin; s <= smax; ++s) {
+          Rec rc;
+          rc.grp = g.first;
+          rc.ws = (int)(ws0 + s * ncols);
+          rc.m = m;
+          for (int r = 0; r < 4; ++r) rc.wr[r] = (float)g.second[r];
+          recs.push_back(rc);
+        }
     }
   }
-  std::stable_sort(es.begin(), es.end(), [](const E& x, const E& y) {
-    return x.row != y.row ? x.row < y.row : x.ws < y.ws;
+  std::stable_sort(recs.begin(), recs.end(), [](const Rec& x, const Rec& y) {
+    return x.grp != y.grp ? x.grp < y.grp : x.ws < y.ws;
   });
-  P->n_entries = (int64_t)es.size();
-  std::vector<int4> ent(es.size());
-  for (size_t i = 0; i < es.size(); ++i) {
-    int wbits;
-    std::memcpy(&wbits, &es[i].w, 4);
-    ent[i] = make_int4(es[i].m, es[i].ws, wbits, 0);
+  P->n_records = (int64_t)recs.size();
+  std::vector<float> recbuf(recs.size() * (size_t)RECW, 0.f);
+  for (size_t i = 0; i < recs.size(); ++i) {
+    float* o = &recbuf[i * RECW];
+    std::memcpy(&o[0], &recs[i].ws, 4);
+    std::memcpy(&o[1], &recs[i].m, 4);
+    for (int r = 0; r < 4; ++r) o[4 + r] = recs[i].wr[r];
+    for (int j = 0; j < K2; ++j) o[8 + j] = (float)wcolv[(size_t)recs[i].m * K2 + j];
   }
-  std::vector<int64_t> row_start(nrows + 1, 0);
-  for (const E& e : es) row_start[e.row + 1]++;
-  for (int r = 0; r < nrows; ++r) row_start[r + 1] += row_start[r];
-
-  int bdim, tpt, tch;
-  spread_config(K2, T, &bdim, &tpt, &tch);
+  std::vector<int64_t> gstart(P->ngroups + 1, 0);
+  for (const Rec& r : recs) gstart[r.grp + 1]++;
+  for (int g = 0; g < P->ngroups; ++g) gstart[g + 1] += gstart[g];
   {
-    const int64_t target = 148LL * 16;
-    int64_t nseg = ceildiv(target, (int64_t)nrows * tch);
-    nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, std::max(1, ncols / 32)));
+    const int64_t tch = spread_time_chunks(T);
+    const int64_t target = 148LL * 12;
+    int64_t nseg = ceildiv(target, (int64_t)P->ngroups * tch);
+    nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, std::max(1, ncols / 64)));
     int segw = (int)ceildiv(ncols, nseg);
     segw = (segw + 3) / 4 * 4;
     P->segw = segw;
     P->nseg = (int)ceildiv(ncols, segw);
   }
-  std::vector<int2> segr((size_t)nrows * P->nseg);
-  for (int r = 0; r < nrows; ++r) {
-    auto b = es.begin() + row_start[r], e = es.begin() + row_start[r + 1];
+  std::vector<int2> segr((size_t)P->ngroups * P->nseg);
+  for (int g = 0; g < P->ngroups; ++g) {
+    auto b = recs.begin() + gstart[g], e = recs.begin() + gstart[g + 1];
     for (int s = 0; s < P->nseg; ++s) {
       const int c0 = s * P->segw, c1 = std::min(ncols, c0 + P->segw);
-      auto lo = std::lower_bound(b, e, c0 - K2 + 1, [](const E& x, int v) { return x.ws < v; });
-      auto hi = std::lower_bound(b, e, c1, [](const E& x, int v) { return x.ws < v; });
-      segr[(size_t)r * P->nseg + s] = make_int2((int)(lo - es.begin()), (int)(hi - es.begin()));
+      auto lo = std::lower_bound(b, e, c0 - K2 + 1, [](const Rec& x, int v) { return x.ws < v; });
+      auto hi = std::lower_bound(b, e, c1, [](const Rec& x, int v) { return x.ws < v; });
+      segr[(size_t)g * P->nseg + s] = make_int2((int)(lo - recs.begin()), (int)(hi - recs.begin()));
     }
   }
 
@@ -279,52 +363,41 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
     const double th = 2.0 * M_PI * i / n_ext - M_PI;  // nufft.py:281
     iw[i] = (float)(psh0 * norm_t / kb_psi(wt, th));
   }
-  std::vector<float2> twf(P->n_over_t), twi(P->fused_ifft ? P->Tu : 1);
-  for (int k = 0; k < P->n_over_t; ++k) {
-    const double a = -2.0 * M_PI * k / P->n_over_t;
-    twf[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+  std::vector<float2> tw(1 << 14);
+  for (int k = 0; k < (1 << 14); ++k) {
+    const double a = -2.0 * M_PI * k / (1 << 14);
+    tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
   }
-  if (P->fused_ifft)
-    for (int k = 0; k < P->Tu; ++k) {
-      const double a = 2.0 * M_PI * k / P->Tu;
-      twi[k] = make_float2((float)std::cos(a), (float)std::sin(a));
-    }
+  NerParams& q = P->ner;
+  P->poly_degree = 8;
+  if (fit_ner_poly(wt, 8, &q) > 2e-8) {
+    P->poly_degree = 12;
+    if (fit_ner_poly(wt, 12, &q) > 1e-6)
+      return fail(PATFFT_ERR_UNSUPPORTED, "window transform not representable by the tap polynomials");
+  }
 
   // ---- device buffers -----------------------------------------------------
   int rc;
-  if ((rc = upload(&P->d_entries, ent))) return rc;
-  if ((rc = upload(&P->d_colw, colw))) return rc;
+  if ((rc = upload(&P->d_recs, recbuf))) return rc;
   if ((rc = upload(&P->d_segr, segr))) return rc;
   if ((rc = upload(&P->d_dp0, dp0))) return rc;
   if ((rc = upload(&P->d_dp1, dp1))) return rc;
   if ((rc = upload(&P->d_jt0, jt0))) return rc;
   if ((rc = upload(&P->d_jt1, jt1))) return rc;
   if ((rc = upload(&P->d_iw, iw))) return rc;
-  if ((rc = upload(&P->d_twf, twf))) return rc;
-  if ((rc = upload(&P->d_twi, twi))) return rc;
-  const size_t ncols_h = (size_t)ncols / 2 + 1;
+  if ((rc = upload(&P->d_tw, tw))) return rc;
   if ((rc = dalloc(&P->d_grid, (size_t)nrows * ncols * T))) return rc;
-  if ((rc = dalloc(&P->d_X, (size_t)nrows * ncols_h * T))) return rc;
+  if ((rc = dalloc(&P->d_Y, (size_t)nrows * P->N1h * T))) return rc;
   if ((rc = dalloc(&P->d_gh, (size_t)P->N0 * P->N1h * T))) return rc;
   if ((rc = dalloc(&P->d_z, (size_t)P->N0u * P->N1uh * P->Tu))) return rc;
 
   CUDA_TRY(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
   for (auto& e : P->ev) CUDA_TRY(cudaEventCreate(&e));
 
-  // ---- cuFFT plans --------------------------------------------------------
-  {
+  // ---- cuFFT only for sizes the shared-memory kernels do not cover --------
+  if (!P->custom_inverse) {
     int n[2], inem[2], onem[2];
     const int rank = d->n_lat;
-    if (rank == 2) {
-      n[0] = nrows; n[1] = ncols;
-      inem[0] = nrows; inem[1] = ncols;
-      onem[0] = nrows; onem[1] = (int)ncols_h;
-    } else {
-      n[0] = ncols; inem[0] = ncols; onem[0] = (int)ncols_h;
-    }
-    CUFFT_TRY(cufftPlanMany(&P->fft_r2c, rank, n, inem, T, 1, onem, T, 1, CUFFT_R2C, T));
-    P->have_r2c = true;
-    CUFFT_TRY(cufftSetStream(P->fft_r2c, P->stream));
     if (rank == 2) {
       n[0] = P->N0u; n[1] = P->N1u;
       inem[0] = P->N0u; inem[1] = P->N1uh;
@@ -334,22 +407,18 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
     }
     CUFFT_TRY(cufftPlanMany(&P->fft_c2r, rank, n, inem, P->Tu, 1, onem, P->Tu, 1, CUFFT_C2R, P->Tu));
     P->have_c2r = true;
-    CUFFT_TRY(cufftSetStream(P->fft_c2r, P->stream));
-    if (!P->fused_ifft) {
-      int nl[1] = {P->Tu};
-      CUFFT_TRY(cufftPlanMany(&P->fft_l, 1, nl, nl, 1, P->Tu, nl, 1, P->Tu, CUFFT_C2C, P->N0u * P->N1uh));
-      P->have_l = true;
-      CUFFT_TRY(cufftSetStream(P->fft_l, P->stream));
-    }
+  }
+  if (!P->fused_ifft) {
+    int nl[1] = {P->Tu};
+    CUFFT_TRY(cufftPlanMany(&P->fft_l, 1, nl, nl, 1, P->Tu, nl, 1, P->Tu, CUFFT_C2C, P->N0u * P->N1uh));
+    P->have_l = true;
   }
 
-  // ---- NER parameter block -----------------------------------------------
-  NerParams& q = P->ner;
+  // ---- kernel parameter blocks --------------------------------------------
   q.gh = P->d_gh;
   q.z = P->d_z;
   q.iw = P->d_iw;
-  q.twf = P->d_twf;
-  q.twi = P->d_twi;
+  q.tw = P->d_tw;
   q.jt0 = P->d_jt0;
   q.jt1 = P->d_jt1;
   q.T = T;
@@ -366,18 +435,31 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
   q.n_lat = P->n_lat;
   q.fused_ifft = P->fused_ifft ? 1 : 0;
   q.c_eff = wt.c_eff;
-  q.inv_c = (float)(1.0 / wt.c_eff);
-  q.alpha = (float)wt.alpha;
-  q.beta = (float)wt.beta;
-  const double s0 = wt.alpha * wt.beta;
-  q.s0 = (float)s0;
-  q.s0_over_sinh_s0 = (float)(s0 / std::sinh(s0));
-  q.inv_one_minus_e2s0 = (float)(1.0 / (1.0 - std::exp(-2.0 * s0)));
   q.scale = (float)(1.0 / (double(P->N0) * double(P->N1) * double(T)));
-  for (int j = 0; j < kMaxTaps; ++j) {
-    const double a = M_PI * double(j - K + 1) / wt.c_eff;
-    q.tap_phase[j] = make_float2((float)std::cos(a), (float)std::sin(a));
-  }
+
+  LateralParams& L = P->lat;
+  L.grid = P->d_grid;
+  L.Y = P->d_Y;
+  L.gh = P->d_gh;
+  L.tw = P->d_tw;
+  L.dp0 = P->d_dp0;
+  L.dp1 = P->d_dp1;
+  L.T = T;
+  L.nrows = nrows;
+  L.lrows = ilog2(nrows);
+  L.ncols = ncols;
+  L.lcols = ilog2(ncols);
+  L.ny = P->N1h;
+  L.N0 = P->N0;
+  L.N1 = P->N1;
+  L.z = P->d_z;
+  L.out = nullptr;
+  L.Tu = P->Tu;
+  L.N0u = P->N0u;
+  L.N1u = P->N1u;
+  L.N1uh = P->N1uh;
+  L.l0u = ilog2(P->N0u);
+  L.l1u = ilog2(P->N1u);
 
   *out = P.release();
   return PATFFT_OK;
@@ -401,43 +483,37 @@ static int execute_device_locked(patfft_nedner_plan* P, const float* samples, fl
   if (prof) CUDA_TRY(cudaEventRecord(P->ev[0], st));
   SpreadParams sp;
   sp.samples = samples;
-  sp.entries = P->d_entries;
-  sp.colw = P->d_colw;
+  sp.recs = P->d_recs;
   sp.seg_range = P->d_segr;
   sp.grid = P->d_grid;
   sp.T = P->T;
   sp.ncols = P->ncols;
+  sp.nrows = P->nrows;
   sp.nseg = P->nseg;
   sp.segw = P->segw;
-  CUDA_TRY(launch_spread(sp, P->K2, P->nrows, st));
+  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->ngroups, st));
   if (prof) CUDA_TRY(cudaEventRecord(P->ev[1], st));
-  CUFFT_TRY(cufftSetStream(P->fft_r2c, st));
-  CUFFT_TRY(cufftExecR2C(P->fft_r2c, P->d_grid, reinterpret_cast<cufftComplex*>(P->d_X)));
+  LateralParams L = P->lat;
+  L.out = image;
+  CUDA_TRY(launch_lateral_col(L, st));
   if (prof) CUDA_TRY(cudaEventRecord(P->ev[2], st));
-  CropParams cp;
-  cp.X = P->d_X;
-  cp.gh = P->d_gh;
-  cp.dp0 = P->d_dp0;
-  cp.dp1 = P->d_dp1;
-  cp.T = P->T;
-  cp.N0 = P->N0;
-  cp.N1 = P->N1;
-  cp.N1h = P->N1h;
-  cp.nrows = P->nrows;
-  cp.ncols_h = P->ncols / 2 + 1;
-  CUDA_TRY(launch_crop(cp, st));
+  CUDA_TRY(launch_lateral_row(L, st));
   if (prof) CUDA_TRY(cudaEventRecord(P->ev[3], st));
   if (P->up > 1 || !P->fused_ifft)
     CUDA_TRY(cudaMemsetAsync(P->d_z, 0, sizeof(float2) * (size_t)P->N0u * P->N1uh * P->Tu, st));
-  CUDA_TRY(launch_ner(P->ner, P->K2, st));
+  CUDA_TRY(launch_ner(P->ner, P->K2, P->poly_degree, st));
   if (!P->fused_ifft) {
     CUFFT_TRY(cufftSetStream(P->fft_l, st));
     CUFFT_TRY(cufftExecC2C(P->fft_l, reinterpret_cast<cufftComplex*>(P->d_z),
                            reinterpret_cast<cufftComplex*>(P->d_z), CUFFT_INVERSE));
   }
   if (prof) CUDA_TRY(cudaEventRecord(P->ev[4], st));
-  CUFFT_TRY(cufftSetStream(P->fft_c2r, st));
-  CUFFT_TRY(cufftExecC2R(P->fft_c2r, reinterpret_cast<cufftComplex*>(P->d_z), image));
+  if (P->custom_inverse) {
+    CUDA_TRY(launch_lateral_inverse(L, st));
+  } else {
+    CUFFT_TRY(cufftSetStream(P->fft_c2r, st));
+    CUFFT_TRY(cufftExecC2R(P->fft_c2r, reinterpret_cast<cufftComplex*>(P->d_z), image));
+  }
   if (prof) {
     CUDA_TRY(cudaEventRecord(P->ev[5], st));
     CUDA_TRY(cudaEventSynchronize(P->ev[5]));
@@ -498,13 +574,12 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
   if (P->stream) cudaStreamSynchronize(P->stream);
-  if (P->have_r2c) cufftDestroy(P->fft_r2c);
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
-  for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_X, (void*)P->d_gh,
-                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_entries, (void*)P->d_colw,
-                  (void*)P->d_segr, (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_twf,
-                  (void*)P->d_twi, (void*)P->d_jt0, (void*)P->d_jt1})
+  for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_gh,
+                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_segr,
+                  (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_tw, (void*)P->d_jt0,
+                  (void*)P->d_jt1})
     free_dev(p);
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
@@ -534,29 +609,39 @@ int patfft_nedner_stage_times(patfft_nedner_plan* P, double* ms, int64_t* launch
 }
 
 const char* patfft_nedner_stage_name(int s) {
-  static const char* names[PATFFT_N_STAGES] = {"spread", "lateral_fft", "crop", "ner", "inverse_fft"};
+  static const char* names[PATFFT_N_STAGES] = {"spread", "lateral_col", "lateral_row", "ner", "inverse"};
   return (s >= 0 && s < PATFFT_N_STAGES) ? names[s] : "";
 }
 
 int patfft_nedner_stage_bytes(const patfft_nedner_plan* P, double* bytes, int n) {
   if (!P || !bytes) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  // Algorithmic bytes: each stage reads its input once and writes its output
+  // once (DESIGN.md roofline table).
   const double T = P->T, Tu = P->Tu;
   const double grid = (double)P->nrows * P->ncols;
-  const double gh_rows = (double)P->N0 * P->N1h;
+  const double y = (double)P->nrows * P->N1h;    // column-transformed half rows
+  const double gh = (double)P->N0 * P->N1h;      // NER rows
+  const double zr = (double)P->N0u * P->N1uh;    // half-spectrum rows after NER
+  const double img = (double)P->N0u * P->N1u;
   const double v[PATFFT_N_STAGES] = {
-      4.0 * T * ((double)P->M + grid),                                  // spread: samples in + real grid out
-      (4.0 + 8.0 * (P->ncols / 2 + 1) / (double)P->ncols) * grid * T,   // R2C: real in + half complex out
-      8.0 * gh_rows * T * 2.0,                                          // crop: read + write needed half rows
-      8.0 * gh_rows * T + 8.0 * (double)P->N0u * P->N1uh * Tu,          // NER: gh rows in, z rows out
-      8.0 * (double)P->N0u * P->N1uh * Tu + 4.0 * (double)P->N0u * P->N1u * Tu};  // C2R
+      4.0 * T * ((double)P->M + grid),                      // spread: f32 samples in + f32 grid out
+      4.0 * T * grid + 8.0 * T * y,                         // colfft: grid in, half spectrum out
+      8.0 * T * y + 8.0 * T * gh,                           // rowfft: half spectrum in, gh out
+      8.0 * T * gh + 8.0 * Tu * zr,                         // ner: gh rows in, z rows out
+      (P->N0u > 1 ? 16.0 * Tu * zr : 0.0) + 8.0 * Tu * zr + 4.0 * Tu * img};  // inverse
   for (int s = 0; s < n && s < PATFFT_N_STAGES; ++s) bytes[s] = v[s];
   return PATFFT_OK;
 }
 
 int patfft_nedner_launches_per_execute(const patfft_nedner_plan* P, int* own, int* library) {
   if (!P) return fail(PATFFT_ERR_PARAMETER, "null plan");
-  if (own) *own = 3;  // spread, crop, ner
-  if (library) *library = -1;  // cuFFT kernels: counted by the caller from the launch list
+  int o = 4;  // spread, colfft, rowfft, ner
+  int lib = 0;
+  if (P->custom_inverse) o += (P->N0u > 1 ? 2 : 1);
+  else lib += 1;  // cuFFT C2R (may be several kernels)
+  if (!P->fused_ifft) lib += 1;
+  if (own) *own = o;
+  if (library) *library = lib;
   return PATFFT_OK;
 }
 

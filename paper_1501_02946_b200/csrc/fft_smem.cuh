@@ -1,0 +1,108 @@
+// Shared-memory power-of-two FFTs used by the lateral, NER and inverse
+// kernels.  In-place radix-2^R decimation in time: the caller stores the
+// input in bit-reversed order, every thread then owns 2^R points of one
+// transform per pass and does R radix-2 stages in registers.
+//
+// Layout is abstracted by an address functor so the same passes run on
+//  * a single long transform with bank-conflict padding (NER rows), and
+//  * P interleaved transforms of a [len][P] tile whose fast axis is the
+//    batch (lateral FFTs over a chunk of consecutive time samples), which
+//    is conflict-free because neighbouring threads own neighbouring batches.
+//
+// Twiddles come from one table tw[k] = exp(-2 pi i k / 2^LMAX); a length-2^L
+// transform reads it with stride 2^(LMAX-L).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace patfft {
+namespace fft {
+
+constexpr int kLogTwiddles = 14;  // table length 16384
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+
+// exp(-+2 pi i j / 16)
+template <bool INV>
+__device__ __forceinline__ float2 w16(int j) {
+  const float c[16] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                       0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                       -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
+                       0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+  const float s = c[(j + 12) & 15];
+  return make_float2(c[j & 15], INV ? s : -s);
+}
+
+struct PadAddr {  // single transform, 1 pad word per 16 (bank-conflict free radix-16 passes)
+  __device__ __forceinline__ int operator()(int i, int) const { return i + (i >> 4); }
+};
+struct TileAddr {  // [len][P] tile, batch fastest
+  int plog;
+  __device__ __forceinline__ int operator()(int i, int p) const { return (i << plog) + p; }
+};
+
+// One pass: stages logh+1 .. logh+R of P transforms of length 2^L.
+template <int R, bool INV, class Addr>
+__device__ __forceinline__ void dit_pass(float2* __restrict__ buf, int L, int plog, int logh,
+                                         const float2* __restrict__ tw, int tid, int nth, Addr addr) {
+  constexpr int PR = 1 << R;
+  const int h = 1 << logh;
+  const int items = 1 << (L - R + plog);
+  const int pmask = (1 << plog) - 1;
+  for (int it = tid; it < items; it += nth) {
+    const int p = it & pmask;
+    const int q = it >> plog;
+    const int k = q & (h - 1);
+    const int base = ((q >> logh) << (logh + R)) + k;
+    float2 e[PR];
+#pragma unroll
+    for (int m = 0; m < PR; ++m) e[m] = buf[addr(base + m * h, p)];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      float2 wi = __ldg(&tw[k << (kLogTwiddles - logh - i - 1)]);  // W_{h 2^{i+1}}^k
+      if (INV) wi.y = -wi.y;
+#pragma unroll
+      for (int r = 0; r < (1 << i); ++r) {
+        const float2 t = (r == 0) ? wi : cmul(wi, w16<INV>(r << (3 - i)));
+#pragma unroll
+        for (int m0 = 0; m0 < PR; m0 += (2 << i)) {
+          const int m = m0 + r;
+          const float2 x = cmul(e[m + (1 << i)], t);
+          e[m + (1 << i)] = csub(e[m], x);
+          e[m] = cadd(e[m], x);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < PR; ++m) buf[addr(base + m * h, p)] = e[m];
+  }
+}
+
+// Full transform (input already bit-reversed); ends with __syncthreads.
+template <bool INV, class Addr>
+__device__ __forceinline__ void fft_inplace(float2* __restrict__ buf, int L, int plog, const float2* __restrict__ tw,
+                                            int tid, int nth, Addr addr) {
+  int logh = 0;
+  while (logh < L) {
+    const int R = min(4, L - logh);
+    switch (R) {
+      case 4: dit_pass<4, INV>(buf, L, plog, logh, tw, tid, nth, addr); break;
+      case 3: dit_pass<3, INV>(buf, L, plog, logh, tw, tid, nth, addr); break;
+      case 2: dit_pass<2, INV>(buf, L, plog, logh, tw, tid, nth, addr); break;
+      default: dit_pass<1, INV>(buf, L, plog, logh, tw, tid, nth, addr); break;
+    }
+    logh += R;
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ int brev(int i, int L) { return L ? (int)(__brev((unsigned)i) >> (32 - L)) : 0; }
+
+}  // namespace fft
+}  // namespace patfft

@@ -1,0 +1,219 @@
+// Lateral (sensor-plane) FFTs of the NEDNER pipeline, as tiled shared-memory
+// transforms over chunks of consecutive time samples.  The time axis is the
+// fastest in every array, so each tile row is one coalesced 128-256 B
+// segment and the P transforms of a tile are interleaved (conflict-free).
+//
+// Forward (replaces nufft.py:406-415 -- oversampled FFT, centred crop,
+// deapodisation -- plus the Nyquist-plane Hermitian part of recon.py:218-222):
+//   colfft : real FFT along grid columns, two time samples packed per complex
+//            transform, only the j1 in [0, N1/2] half that is needed is kept;
+//   rowfft : complex FFT along grid rows, crop j0 in [-N0/2, N0/2], deapodise,
+//            symmetrise the Nyquist planes -> gh (half spectrum in j1).
+// Inverse (replaces the lateral part of recon.py:255 ifftn + fftshift + real):
+//   inv_col: complex inverse FFT along j0 (in place);
+//   inv_c2r: Hermitian-completed inverse FFT along j1, two time samples packed
+//            per transform -> real image rows.
+#include <cuda_runtime.h>
+
+#include "fft_smem.cuh"
+#include "patfft_internal.h"
+
+namespace patfft {
+namespace {
+
+using fft::TileAddr;
+
+template <int PLOG>
+__global__ void __launch_bounds__(512) colfft_kernel(const LateralParams p) {
+  extern __shared__ float2 sm[];
+  constexpr int P = 1 << PLOG;
+  const int u0 = blockIdx.x;
+  const int t0 = blockIdx.y * 2 * P;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int T = p.T, n = p.ncols;
+  const TileAddr ad{PLOG};
+  const float* __restrict__ src = p.grid + (size_t)u0 * n * T;
+  for (int i = tid; i < n * P; i += nth) {
+    const int row = i >> PLOG, q = i & (P - 1);
+    const int t = t0 + 2 * q;
+    float2 v = make_float2(0.f, 0.f);
+    if (t < T) v = __ldcs(reinterpret_cast<const float2*>(src + (size_t)row * T + t));
+    sm[ad(fft::brev(row, p.lcols), q)] = v;
+  }
+  __syncthreads();
+  fft::fft_inplace<false>(sm, p.lcols, PLOG, p.tw, tid, nth, ad);
+  float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * T;
+  for (int i = tid; i < p.ny * P; i += nth) {
+    const int k = i >> PLOG, q = i & (P - 1);
+    const int t = t0 + 2 * q;
+    if (t >= T) continue;
+    const float2 zk = sm[ad(k, q)];
+    const float2 zm = fft::conjf2(sm[ad((n - k) & (n - 1), q)]);
+    const float2 d = fft::csub(zk, zm);
+    const float4 o = make_float4(0.5f * (zk.x + zm.x), 0.5f * (zk.y + zm.y), 0.5f * d.y, -0.5f * d.x);
+    *reinterpret_cast<float4*>(dst + (size_t)k * T + t) = o;
+  }
+}
+
+template <int PLOG>
+__global__ void __launch_bounds__(512) rowfft_kernel(const LateralParams p) {
+  extern __shared__ float2 sm[];
+  constexpr int P = 1 << PLOG;
+  const int j1 = blockIdx.x;
+  const int t0 = blockIdx.y * P;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int T = p.T, nr = p.nrows;
+  const TileAddr ad{PLOG};
+  for (int i = tid; i < nr * P; i += nth) {
+    const int row = i >> PLOG, q = i & (P - 1);
+    const int t = t0 + q;
+    sm[ad(fft::brev(row, p.lrows), q)] =
+        (t < T) ? __ldcs(p.Y + ((size_t)row * p.ny + j1) * T + t) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  fft::fft_inplace<false>(sm, p.lrows, PLOG, p.tw, tid, nth, ad);
+  const bool nyq1 = (j1 == p.N1 / 2);
+  const int N0 = p.N0, mask = nr - 1;
+  const float dp1 = p.dp1[j1];
+  for (int i = tid; i < N0 * P; i += nth) {
+    const int j0w = i >> PLOG, q = i & (P - 1);
+    const int t = t0 + q;
+    if (t >= T) continue;
+    const int a = (N0 > 1) ? (j0w < N0 / 2 ? j0w : j0w - N0) : 0;
+    const bool nyq0 = (N0 > 1) && (a == -(N0 / 2));
+    float2 v;
+    if (nyq1) {  // stored j1 = N1/2 is signed -N1/2: X(a,-N1/2) = conj X(-a,+N1/2)
+      const float2 v1 = fft::conjf2(sm[ad((-a) & mask, q)]);
+      const float2 v2 = sm[ad((nyq0 ? -a : a) & mask, q)];
+      v = fft::cscale(fft::cadd(v1, v2), 0.5f);
+    } else if (nyq0) {
+      v = fft::cscale(fft::cadd(sm[ad(a & mask, q)], sm[ad((-a) & mask, q)]), 0.5f);
+    } else {
+      v = sm[ad(a & mask, q)];
+    }
+    p.gh[((size_t)j0w * p.ny + j1) * T + t] = fft::cscale(v, p.dp0[j0w] * dp1);
+  }
+}
+
+template <int PLOG>
+__global__ void __launch_bounds__(512) inv_col_kernel(const LateralParams p) {
+  extern __shared__ float2 sm[];
+  constexpr int P = 1 << PLOG;
+  const int j1 = blockIdx.x;
+  const int t0 = blockIdx.y * P;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int T = p.Tu, n = p.N0u;
+  const TileAddr ad{PLOG};
+  float2* __restrict__ z = p.z;
+  for (int i = tid; i < n * P; i += nth) {
+    const int row = i >> PLOG, q = i & (P - 1);
+    const int t = t0 + q;
+    sm[ad(fft::brev(row, p.l0u), q)] =
+        (t < T) ? z[((size_t)row * p.N1uh + j1) * T + t] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  fft::fft_inplace<true>(sm, p.l0u, PLOG, p.tw, tid, nth, ad);
+  for (int i = tid; i < n * P; i += nth) {
+    const int row = i >> PLOG, q = i & (P - 1);
+    const int t = t0 + q;
+    if (t < T) z[((size_t)row * p.N1uh + j1) * T + t] = sm[ad(row, q)];
+  }
+}
+
+template <int PLOG>
+__global__ void __launch_bounds__(512) inv_c2r_kernel(const LateralParams p) {
+  extern __shared__ float2 sm[];
+  constexpr int P = 1 << PLOG;
+  const int n0 = blockIdx.x;
+  const int t0 = blockIdx.y * 2 * P;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int T = p.Tu, n = p.N1u, half = n / 2;
+  const TileAddr ad{PLOG};
+  const float2* __restrict__ z = p.z + (size_t)n0 * p.N1uh * T;
+  for (int i = tid; i < (half + 1) * P; i += nth) {
+    const int k = i >> PLOG, q = i & (P - 1);
+    const int t = t0 + 2 * q;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < T) v = __ldcs(reinterpret_cast<const float4*>(z + (size_t)k * T + t));
+    if (k == 0 || k == half) {  // C2R semantics: self-conjugate bins are real
+      v.y = 0.f;
+      v.w = 0.f;
+    }
+    // Z = Xa + i Xb ; Z[n-k] = conj(Xa) + i conj(Xb)
+    sm[ad(fft::brev(k, p.l1u), q)] = make_float2(v.x - v.w, v.y + v.z);
+    if (k != 0 && k != half) sm[ad(fft::brev(n - k, p.l1u), q)] = make_float2(v.x + v.w, v.z - v.y);
+  }
+  __syncthreads();
+  fft::fft_inplace<true>(sm, p.l1u, PLOG, p.tw, tid, nth, ad);
+  float* __restrict__ out = p.out + (size_t)n0 * n * T;
+  for (int i = tid; i < n * P; i += nth) {
+    const int row = i >> PLOG, q = i & (P - 1);
+    const int t = t0 + 2 * q;
+    if (t < T) *reinterpret_cast<float2*>(out + (size_t)row * T + t) = sm[ad(row, q)];
+  }
+}
+
+int plog_for(int len) {
+  // P transforms per tile, tile <= 64 KB of float2
+  int plog = 4;
+  while (plog > 0 && ((size_t)len << plog) * sizeof(float2) > 65536) --plog;
+  return plog;
+}
+
+int threads_for(int len, int plog) {
+  int items = (len >> 4 ? len >> 4 : 1) << plog;  // radix-16 passes
+  if (items < 64) items = 64;
+  if (items > 512) items = 512;
+  return items;
+}
+
+#define PATFFT_DEF_LAUNCH(NAME)                                                                        \
+  cudaError_t launch_##NAME(const LateralParams& p, int len, dim3 grid_xy, int tpack, cudaStream_t s) { \
+    const int plog = plog_for(len);                                                                    \
+    const size_t smem = ((size_t)len << plog) * sizeof(float2);                                        \
+    const int thr = threads_for(len, plog);                                                            \
+    dim3 grid(grid_xy.x, (unsigned)((grid_xy.y + (tpack << plog) - 1) / (tpack << plog)));              \
+    cudaError_t err = cudaSuccess;                                                                     \
+    auto run = [&](auto k) {                                                                           \
+      err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
+      if (err == cudaSuccess) {                                                                        \
+        k<<<grid, thr, smem, s>>>(p);                                                                  \
+        err = cudaGetLastError();                                                                      \
+      }                                                                                                \
+    };                                                                                                 \
+    switch (plog) {                                                                                    \
+      case 4: run(NAME##_kernel<4>); break;                                                            \
+      case 3: run(NAME##_kernel<3>); break;                                                            \
+      case 2: run(NAME##_kernel<2>); break;                                                            \
+      case 1: run(NAME##_kernel<1>); break;                                                            \
+      default: run(NAME##_kernel<0>); break;                                                           \
+    }                                                                                                  \
+    return err;                                                                                        \
+  }
+
+}  // namespace
+
+namespace {
+PATFFT_DEF_LAUNCH(colfft)
+PATFFT_DEF_LAUNCH(rowfft)
+PATFFT_DEF_LAUNCH(inv_col)
+PATFFT_DEF_LAUNCH(inv_c2r)
+}  // namespace
+
+cudaError_t launch_lateral_col(const LateralParams& p, cudaStream_t s) {
+  return launch_colfft(p, p.ncols, dim3((unsigned)p.nrows, (unsigned)p.T), 2, s);
+}
+
+cudaError_t launch_lateral_row(const LateralParams& p, cudaStream_t s) {
+  return launch_rowfft(p, p.nrows, dim3((unsigned)p.ny, (unsigned)p.T), 1, s);
+}
+
+cudaError_t launch_lateral_inverse(const LateralParams& p, cudaStream_t s) {
+  if (p.N0u > 1) {
+    cudaError_t e = launch_inv_col(p, p.N0u, dim3((unsigned)p.N1uh, (unsigned)p.Tu), 1, s);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_inv_c2r(p, p.N1u, dim3((unsigned)p.N0u, (unsigned)p.Tu), 2, s);
+}
+
+}  // namespace patfft

@@ -1,0 +1,250 @@
+// NER stage: one CTA per lateral frequency row j = (j0, j1) of the half
+// spectrum.  Everything between reading gh[j, :] and writing the depth-
+// inverted row z[j, :] stays in shared memory:
+//
+//  1. even time extension [g0..g_{T-1}, 0, g_{T-1}..g1] (recon.py:263-271)
+//     times the pre-window 1/psi(2 pi n/2T - pi) (nufft.py:281-282, 325),
+//     zero padded to n_over and stored rotated by -T (so the FFT output is
+//     already multiplied by exp(i pi k / c), which removes the per-tap phase
+//     of nufft.py:292) and bit-reversed;
+//  2. radix-16 FFT of length n_over;
+//  3. for every depth frequency l: kappa_e = 2 sign(l) sqrt(j2 + l^2) on the
+//     band (recon.py:282-293), 2K-tap Kaiser-Bessel interpolation
+//     (nufft.py:287-293, 329-331) with the tap weights evaluated as even/odd
+//     split polynomials (no transcendental per tap), one phase
+//     exp(-i pi kappa_e) per target, amplitude 2l/kappa, 0.5 and the
+//     inverse-FFT normalisation (recon.py:308, 255);
+//  4. zero padding / Nyquist split for upsampling (recon.py:225-246) and the
+//     inverse FFT along depth (recon.py:255), written out as one z row (or
+//     two rows for the lateral Nyquist split).
+#include <cuda_runtime.h>
+
+#include "fft_smem.cuh"
+#include "patfft_internal.h"
+
+namespace patfft {
+namespace {
+
+using fft::PadAddr;
+
+constexpr int kMaxTargetsPerThread = 8;
+
+// (cos(pi r), sin(pi r)) for |r| <= 1, ~1e-8 absolute
+__device__ __forceinline__ float2 cospi_sinpi(float r) {
+  const float q = rintf(2.f * r);
+  const float x = 3.14159265358979f * fmaf(-0.5f, q, r);  // |x| <= pi/4
+  const float x2 = x * x;
+  const float s = x * fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, 2.7557319e-6f, -1.98412698e-4f), 8.33333333e-3f),
+                                    -0.166666667f), 1.f);
+  const float c = fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, -2.7557319e-7f, 2.48015873e-5f), -1.38888889e-3f),
+                                          4.16666667e-2f), -0.5f), 1.f);
+  const int qi = ((int)q) & 3;
+  switch (qi) {
+    case 0: return make_float2(c, s);
+    case 1: return make_float2(-s, c);
+    case 2: return make_float2(-c, -s);
+    default: return make_float2(s, -c);
+  }
+}
+
+template <int K2, int D>
+__global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
+  extern __shared__ float2 sbuf[];
+  constexpr int K = K2 / 2;
+  const int r = blockIdx.x;  // gh row: j0w * N1h + j1
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int T = p.T, n = p.n_over, L = p.log_n_over;
+  const PadAddr ad;
+  const float2* __restrict__ g = p.gh + (size_t)r * T;
+
+  // 1. rotated, windowed even extension -> bit-reversed smem
+  for (int m = tid; m < n; m += nth) {
+    const int i = (m + T) & (n - 1);  // sequence index stored at slot m
+    float2 v = make_float2(0.f, 0.f);
+    if (i < 2 * T && i != T) {
+      const float2 gv = __ldcs(&g[i < T ? i : 2 * T - i]);
+      v = fft::cscale(gv, __ldg(&p.iw[i]));
+    }
+    sbuf[ad(fft::brev(m, L), 0)] = v;
+  }
+  __syncthreads();
+  fft::fft_inplace<false>(sbuf, L, 0, p.tw, tid, nth, ad);
+
+  // 2. targets
+  const int j0w = r / p.N1h;
+  const int j1 = r - j0w * p.N1h;
+  const double j2 = p.jt0[j0w] + p.jt1[j1];  // recon.py:210-214 summation order
+  const double halfT = (double)T / 2.0;
+  const double band_r2 = halfT * halfT;
+  float2 vals[kMaxTargetsPerThread];
+#pragma unroll
+  for (int it = 0; it < kMaxTargetsPerThread; ++it) {
+    const int l = tid + it * nth;
+    float2 out = make_float2(0.f, 0.f);
+    if (l < T) {
+      const int ls = (l < T / 2) ? l : l - T;
+      const double lv = __dmul_rn(__dmul_rn((double)ls, 1.0 / (double)T), (double)T);  // fftfreq(T)*T
+      const double r2 = __dadd_rn(j2, __dmul_rn(lv, lv));
+      if (ls != 0 && r2 <= band_r2) {
+        double kap = sqrt(r2);
+        if (ls < 0) kap = -kap;
+        const double ke = 2.0 * kap;
+        const double xi = __dmul_rn(p.c_eff, ke);
+        const double k0d = floor(xi);
+        const int k0 = (int)k0d;
+        const float z = (float)(xi - k0d) - 0.5f;
+        const float z2 = z * z;
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          // tap j (dk = j-K+1) and its mirror K2-1-j share one polynomial:
+          // w_j = E(z^2) + z O(z^2), w_mirror = E(z^2) - z O(z^2)
+          float e = p.poly[j][D], o = p.poly[j][D - 1];
+          if (D % 2) {
+            e = p.poly[j][D - 1];
+            o = p.poly[j][D];
+          }
+#pragma unroll
+          for (int d = (D % 2 ? D - 3 : D - 2); d >= 0; d -= 2) e = fmaf(e, z2, p.poly[j][d]);
+#pragma unroll
+          for (int d = (D % 2 ? D - 2 : D - 3); d >= 1; d -= 2) o = fmaf(o, z2, p.poly[j][d]);
+          const float wa = fmaf(z, o, e);
+          const float wb = fmaf(-z, o, e);
+          const float2 Fa = sbuf[ad((k0 + j - K + 1) & (n - 1), 0)];
+          const float2 Fb = sbuf[ad((k0 + K - j) & (n - 1), 0)];
+          acc.x = fmaf(wa, Fa.x, fmaf(wb, Fb.x, acc.x));
+          acc.y = fmaf(wa, Fa.y, fmaf(wb, Fb.y, acc.y));
+        }
+        // exp(-i pi kappa_e), kappa_e reduced mod 2 in float64
+        const double red = ke - 2.0 * floor(0.5 * ke + 0.5);
+        const float2 cs = cospi_sinpi((float)red);
+        const float amp = __fdividef(2.f * (float)lv, (float)kap);
+        const float a = 0.5f * amp * p.scale;
+        out = make_float2(a * (acc.x * cs.x + acc.y * cs.y), a * (acc.y * cs.x - acc.x * cs.y));
+      }
+    }
+    vals[it] = out;
+  }
+
+  // destination rows in the (possibly upsampled) half spectrum z
+  int drow0 = 0, drow1 = -1;
+  float dfac = 1.f;
+  {
+    int j0u = 0, j0u2 = -1;
+    float f0 = 1.f;
+    if (p.n_lat == 2) {
+      const int a = j0w < p.N0 / 2 ? j0w : j0w - p.N0;
+      if (p.up == 1) {
+        j0u = j0w;
+      } else if (a == -(p.N0 / 2)) {  // Nyquist split (recon.py:239-245)
+        j0u = p.N0 / 2;
+        j0u2 = p.N0u - p.N0 / 2;
+        f0 = 0.5f;
+      } else {
+        j0u = a >= 0 ? a : p.N0u + a;
+      }
+    }
+    const float f1 = (p.up > 1 && j1 == p.N1 / 2) ? 0.5f : 1.f;
+    drow0 = j0u * p.N1uh + j1;
+    if (j0u2 >= 0) drow1 = j0u2 * p.N1uh + j1;
+    dfac = f0 * f1;
+  }
+
+  const int Tu = p.Tu;
+  __syncthreads();  // forward spectrum fully consumed
+  if (p.fused_ifft) {
+    const int Lu = p.log_tu;
+    if (p.up > 1) {
+      for (int i = tid; i < Tu; i += nth) sbuf[ad(i, 0)] = make_float2(0.f, 0.f);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int it = 0; it < kMaxTargetsPerThread; ++it) {
+      const int l = tid + it * nth;
+      if (l >= T) break;
+      const int ls = (l < T / 2) ? l : l - T;
+      const float2 v = fft::cscale(vals[it], dfac);
+      if (ls == -(T / 2) && p.up > 1) {
+        const float2 hv = fft::cscale(v, 0.5f);
+        sbuf[ad(fft::brev(T / 2, Lu), 0)] = hv;
+        sbuf[ad(fft::brev(Tu - T / 2, Lu), 0)] = hv;
+      } else {
+        sbuf[ad(fft::brev(ls >= 0 ? ls : Tu + ls, Lu), 0)] = v;
+      }
+    }
+    __syncthreads();
+    fft::fft_inplace<true>(sbuf, Lu, 0, p.tw, tid, nth, ad);
+    float2* __restrict__ z0 = p.z + (size_t)drow0 * Tu;
+    float2* __restrict__ z1 = p.z + (size_t)(drow1 >= 0 ? drow1 : drow0) * Tu;
+    for (int i = tid; i < Tu; i += nth) {
+      const float2 v = sbuf[ad(i, 0)];
+      z0[i] = v;
+      if (drow1 >= 0) z1[i] = v;
+    }
+  } else {
+    // spectrum only; z was zero-filled and a batched cuFFT does the depth IFFT
+#pragma unroll
+    for (int it = 0; it < kMaxTargetsPerThread; ++it) {
+      const int l = tid + it * nth;
+      if (l >= T) break;
+      const int ls = (l < T / 2) ? l : l - T;
+      const float2 v = fft::cscale(vals[it], dfac);
+      for (int d = 0; d < (drow1 >= 0 ? 2 : 1); ++d) {
+        float2* __restrict__ zr = p.z + (size_t)(d ? drow1 : drow0) * Tu;
+        if (ls == -(T / 2) && p.up > 1) {
+          zr[T / 2] = fft::cscale(v, 0.5f);
+          zr[Tu - T / 2] = fft::cscale(v, 0.5f);
+        } else {
+          zr[ls >= 0 ? ls : Tu + ls] = v;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+size_t ner_smem_bytes(int n_over, int Tu) {
+  const int m = n_over > Tu ? n_over : Tu;
+  return (size_t)(m + m / 16 + 1) * sizeof(float2);
+}
+
+int ner_threads(int n_over) {
+  int t = n_over / 16;
+  if (t < 64) t = 64;
+  if (t > 512) t = 512;
+  return t;
+}
+
+cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
+  const int threads = ner_threads(p.n_over);
+  const size_t smem = ner_smem_bytes(p.n_over, p.fused_ifft ? p.Tu : 0);
+  const unsigned rows = (unsigned)(p.N0 * p.N1h);
+  cudaError_t err = cudaSuccess;
+  auto go = [&](auto kern) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return;
+    kern<<<rows, threads, smem, s>>>(p);
+    err = cudaGetLastError();
+  };
+#define PATFFT_NER_CASE(k2)                          \
+  case k2:                                           \
+    if (degree == 8) go(ner_kernel<k2, 8>);          \
+    else go(ner_kernel<k2, 12>);                     \
+    break;
+  switch (K2) {
+    PATFFT_NER_CASE(2)
+    PATFFT_NER_CASE(4)
+    PATFFT_NER_CASE(6)
+    PATFFT_NER_CASE(8)
+    PATFFT_NER_CASE(10)
+    PATFFT_NER_CASE(12)
+    PATFFT_NER_CASE(14)
+    PATFFT_NER_CASE(16)
+    default: return cudaErrorInvalidValue;
+  }
+#undef PATFFT_NER_CASE
+  return err;
+}
+
+}  // namespace patfft

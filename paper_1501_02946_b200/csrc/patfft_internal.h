@@ -6,6 +6,7 @@
 #include <cufft.h>
 
 #include <cstdint>
+#include <array>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -28,55 +29,66 @@ struct Window {
 // when the support is inadmissible (reference raises ParameterError).
 bool resolve_window(double c, int K, double alpha_or_nan, double beta_or_nan, double c_eff, Window* out,
                     std::string* err);
-double bessel_i0(double x);                 // scipy.special.i0 equivalent
-double kb_psi(const Window& w, double th);  // window_eval (nufft.py:159-165)
+double bessel_i0(double x);                   // scipy.special.i0 equivalent
+double kb_psi(const Window& w, double th);    // window_eval (nufft.py:159-165)
 double kb_psihat(const Window& w, double x);  // window_ft_eval (nufft.py:168-187)
-int even_fast_len(double target);           // next_even_fast_len (nufft.py:83-89)
+int even_fast_len(double target);             // next_even_fast_len (nufft.py:83-89)
 
 // ---------------------------------------------------------------------------
 // Device-side parameter blocks
 // ---------------------------------------------------------------------------
 constexpr int kMaxTaps = 16;  // 2K <= 16 (K <= 8)
+constexpr int kMaxPolyDegree = 12;
 
 struct SpreadParams {
-  const float* samples;   // [M][T] float32, already in device memory
-  const int4* entries;    // sorted by (row, ws): {m, ws, float_bits(w_row*scale), 0}
-  const float* colw;      // [M][K2] normalised column weights
-  const int2* seg_range;  // per (row, seg): [lo, hi) into entries
+  const float* samples;   // [M][T] float32, device
+  const float* recs;      // per (row group) column-sorted records, see spread.cu
+  const int2* seg_range;  // per (row group, column segment): [lo, hi) into recs
   float* grid;            // [nrows][ncols][T] centred oversampled grid
-  int T, ncols, nseg, segw;
+  int T, ncols, nrows, nseg, segw;
 };
 
-struct CropParams {
-  const float2* X;   // [nrows][ncols/2+1][T] R2C output of the centred grid
-  float2* gh;        // [N0][N1h][T] symmetrised lateral spectrum (wrapped j0, half j1)
-  const float* dp0;  // [N0] deapodisation (wrapped index), {1} when n_lat == 1
-  const float* dp1;  // [N1]
-  int T, N0, N1, N1h, nrows, ncols_h;
+struct LateralParams {
+  // forward
+  const float* grid;   // [nrows][ncols][T]
+  float2* Y;           // [nrows][ny][T]  column-transformed half spectrum
+  float2* gh;          // [N0][ny][T]     symmetrised, deapodised lateral spectrum
+  const float2* tw;    // exp(-2 pi i k / 2^14)
+  const float* dp0;    // [N0] deapodisation (wrapped index)
+  const float* dp1;    // [N1]
+  int T, nrows, lrows, ncols, lcols, ny, N0, N1;
+  // inverse
+  float2* z;           // [N0u][N1uh][Tu]
+  float* out;          // [N0u][N1u][Tu]
+  int Tu, N0u, N1u, N1uh, l0u, l1u;
 };
 
 struct NerParams {
   const float2* gh;    // [N0][N1h][T]
   float2* z;           // [N0u][N1uh][Tu]
   const float* iw;     // [2T] psihat(0)*norm/psi(theta_n) (nufft.py:281-284)
-  const float2* twf;   // [n_over] exp(-2 pi i k / n_over)
-  const float2* twi;   // [Tu]    exp(+2 pi i k / Tu)
+  const float2* tw;    // exp(-2 pi i k / 2^14)
   const double* jt0;   // [N0] (j0*ratio0)^2 on the wrapped grid (recon.py:211)
   const double* jt1;   // [N1h]
   int T, n_over, log_n_over, Tu, log_tu;
   int N0, N1, N1h, N0u, N1uh, up, n_lat;
-  int fused_ifft;      // 1: inverse l-FFT in shared memory, 0: write spectrum
+  int fused_ifft;      // 1: inverse depth FFT in shared memory, 0: write spectrum
   double c_eff;        // n_over / (2T)
-  float inv_c, alpha, beta, s0, s0_over_sinh_s0, inv_one_minus_e2s0;
   float scale;         // 1/(N0*N1*T): scipy ifftn normalisation * up^d
-  float2 tap_phase[kMaxTaps];  // exp(+i pi dk / c_eff), dk = -K+1..K
+  float poly[kMaxTaps / 2][kMaxPolyDegree + 1];  // psihat((z + K-1/2-j)/c)/psihat(0), z in [-1/2,1/2]
 };
 
-// Kernel launchers (kernels.cu)
-cudaError_t launch_spread(const SpreadParams& p, int K2, int nrows, cudaStream_t s);
-cudaError_t launch_crop(const CropParams& p, cudaStream_t s);
-cudaError_t launch_ner(const NerParams& p, int K2, cudaStream_t s);
+// Kernel launchers
+cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int ngroups, cudaStream_t s);
+int spread_rows_per_group(int n_lat, int K2);
+int spread_record_words(int K2);
+int spread_time_chunks(int T);
+cudaError_t launch_lateral_col(const LateralParams& p, cudaStream_t s);
+cudaError_t launch_lateral_row(const LateralParams& p, cudaStream_t s);
+cudaError_t launch_lateral_inverse(const LateralParams& p, cudaStream_t s);
+cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s);
 size_t ner_smem_bytes(int n_over, int Tu);
+int ner_threads(int n_over);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);
 cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s);
 cudaError_t launch_fill(float* dst, size_t n, float v, cudaStream_t s);
@@ -95,10 +107,11 @@ struct patfft_nedner_plan {
   int n_lat = 2, N0 = 1, N1 = 0, T = 0, up = 1, M = 0;
   int nrows = 1, ncols = 0, N1h = 0;
   int N0u = 1, N1u = 0, N1uh = 0, Tu = 0;
-  int n_over_t = 0, K2 = 12;
-  int nseg = 1, segw = 0;
-  int64_t n_entries = 0;
+  int n_over_t = 0, K2 = 12, poly_degree = 8;
+  int R = 4, ngroups = 0, nseg = 1, segw = 0;
+  int64_t n_records = 0;
   bool fused_ifft = true;
+  bool custom_inverse = true;
 
   patfft::Window win_lat[2], win_t;
 
@@ -106,26 +119,25 @@ struct patfft_nedner_plan {
   float* d_samples = nullptr;   // [M][T] f32 (host path staging)
   double* d_samples64 = nullptr;
   float* d_grid = nullptr;      // [nrows][ncols][T]
-  float2* d_X = nullptr;        // [nrows][ncols/2+1][T]
+  float2* d_Y = nullptr;        // [nrows][N1h][T]
   float2* d_gh = nullptr;       // [N0][N1h][T]
   float2* d_z = nullptr;        // [N0u][N1uh][Tu]
   float* d_out = nullptr;       // [N0u][N1u][Tu] f32 (host path staging)
   double* d_out64 = nullptr;
-  int4* d_entries = nullptr;
-  float* d_colw = nullptr;
+  float* d_recs = nullptr;
   int2* d_segr = nullptr;
   float* d_dp0 = nullptr;
   float* d_dp1 = nullptr;
   float* d_iw = nullptr;
-  float2* d_twf = nullptr;
-  float2* d_twi = nullptr;
+  float2* d_tw = nullptr;
   double* d_jt0 = nullptr;
   double* d_jt1 = nullptr;
 
-  cufftHandle fft_r2c = 0, fft_c2r = 0, fft_l = 0;
-  bool have_r2c = false, have_c2r = false, have_l = false;
+  cufftHandle fft_c2r = 0, fft_l = 0;
+  bool have_c2r = false, have_l = false;
 
   patfft::NerParams ner{};
+  patfft::LateralParams lat{};
 
   // profiling
   bool profiling = false;

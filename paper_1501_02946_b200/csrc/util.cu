@@ -1,0 +1,41 @@
+// Small elementwise kernels: float64 <-> float32 conversion for the host
+// path, and a fill used to flush L2 between timed iterations.
+#include <cuda_runtime.h>
+
+#include "patfft_internal.h"
+
+namespace patfft {
+namespace {
+__global__ void f64_to_f32_kernel(const double* __restrict__ s, float* __restrict__ d, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    d[i] = (float)s[i];
+}
+__global__ void f32_to_f64_kernel(const float* __restrict__ s, double* __restrict__ d, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    d[i] = (double)s[i];
+}
+__global__ void fill_kernel(float* __restrict__ d, size_t n, float v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    d[i] = v;
+}
+unsigned grid_for(size_t n) {
+  const size_t b = (n + 255) / 256;
+  const size_t cap = 148 * 32;
+  return (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+}  // namespace
+
+cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s) {
+  f64_to_f32_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s) {
+  f32_to_f64_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_fill(float* dst, size_t n, float v, cudaStream_t s) {
+  fill_kernel<<<grid_for(n), 256, 0, s>>>(dst, n, v);
+  return cudaGetLastError();
+}
+
+}  // namespace patfft

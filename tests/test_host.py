@@ -30,7 +30,7 @@ def test_library_metadata_calls():
     lib = _lib_or_skip()
     assert b"sm_100a" in lib.patfft_version()
     assert lib.patfft_nedner_stage_name(0) == b"spread"
-    assert lib.patfft_nedner_stage_name(4) == b"inverse_fft"
+    assert lib.patfft_nedner_stage_name(4) == b"inverse"
 
 
 def test_window_spec_mirrors_reference_validation():
