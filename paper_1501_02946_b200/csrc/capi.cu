@@ -310,7 +310,8 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
     std::memcpy(&o[0], &recs[i].ws, 4);
     std::memcpy(&o[1], &recs[i].m, 4);
     for (int r = 0; r < 4; ++r) o[4 + r] = recs[i].wr[r];
-    for (int j = 0; j < K2; ++j) o[8 + j] = (float)wcolv[(size_t)recs[i].m * K2 + j];
+    const int ring = RECW - 8;
+    for (int j = 0; j < K2; ++j) o[8 + (int)pmod(recs[i].ws + j, ring)] = (float)wcolv[(size_t)recs[i].m * K2 + j];
   }
   std::vector<int64_t> gstart(P->ngroups + 1, 0);
   for (const Rec& r : recs) gstart[r.grp + 1]++;

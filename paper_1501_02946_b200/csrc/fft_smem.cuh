@@ -104,5 +104,24 @@ __device__ __forceinline__ void fft_inplace(float2* __restrict__ buf, int L, int
 
 __device__ __forceinline__ int brev(int i, int L) { return L ? (int)(__brev((unsigned)i) >> (32 - L)) : 0; }
 
+// Global -> shared staging with up to B independent loads in flight per
+// thread (all loads of a batch are issued before the first store).
+template <int B, class V, class Load, class Store>
+__device__ __forceinline__ void staged_copy(int total, int tid, int nth, Load load, Store store) {
+  for (int i0 = 0; i0 < total; i0 += B * nth) {
+    V v[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int i = i0 + tid + k * nth;
+      if (i < total) v[k] = load(i);
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int i = i0 + tid + k * nth;
+      if (i < total) store(i, v[k]);
+    }
+  }
+}
+
 }  // namespace fft
 }  // namespace patfft

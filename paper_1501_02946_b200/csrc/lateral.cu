@@ -33,13 +33,13 @@ __global__ void __launch_bounds__(512) colfft_kernel(const LateralParams p) {
   const int T = p.T, n = p.ncols;
   const TileAddr ad{PLOG};
   const float* __restrict__ src = p.grid + (size_t)u0 * n * T;
-  for (int i = tid; i < n * P; i += nth) {
-    const int row = i >> PLOG, q = i & (P - 1);
-    const int t = t0 + 2 * q;
-    float2 v = make_float2(0.f, 0.f);
-    if (t < T) v = __ldcs(reinterpret_cast<const float2*>(src + (size_t)row * T + t));
-    sm[ad(fft::brev(row, p.lcols), q)] = v;
-  }
+  fft::staged_copy<8, float2>(
+      n * P, tid, nth,
+      [&](int i) {
+        const int row = i >> PLOG, t = t0 + 2 * (i & (P - 1));
+        return (t < T) ? __ldcs(reinterpret_cast<const float2*>(src + (size_t)row * T + t)) : make_float2(0.f, 0.f);
+      },
+      [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lcols), i & (P - 1))] = v; });
   __syncthreads();
   fft::fft_inplace<false>(sm, p.lcols, PLOG, p.tw, tid, nth, ad);
   float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * T;
@@ -64,12 +64,13 @@ __global__ void __launch_bounds__(512) rowfft_kernel(const LateralParams p) {
   const int tid = threadIdx.x, nth = blockDim.x;
   const int T = p.T, nr = p.nrows;
   const TileAddr ad{PLOG};
-  for (int i = tid; i < nr * P; i += nth) {
-    const int row = i >> PLOG, q = i & (P - 1);
-    const int t = t0 + q;
-    sm[ad(fft::brev(row, p.lrows), q)] =
-        (t < T) ? __ldcs(p.Y + ((size_t)row * p.ny + j1) * T + t) : make_float2(0.f, 0.f);
-  }
+  fft::staged_copy<8, float2>(
+      nr * P, tid, nth,
+      [&](int i) {
+        const int row = i >> PLOG, t = t0 + (i & (P - 1));
+        return (t < T) ? __ldcs(p.Y + ((size_t)row * p.ny + j1) * T + t) : make_float2(0.f, 0.f);
+      },
+      [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lrows), i & (P - 1))] = v; });
   __syncthreads();
   fft::fft_inplace<false>(sm, p.lrows, PLOG, p.tw, tid, nth, ad);
   const bool nyq1 = (j1 == p.N1 / 2);
@@ -105,12 +106,13 @@ __global__ void __launch_bounds__(512) inv_col_kernel(const LateralParams p) {
   const int T = p.Tu, n = p.N0u;
   const TileAddr ad{PLOG};
   float2* __restrict__ z = p.z;
-  for (int i = tid; i < n * P; i += nth) {
-    const int row = i >> PLOG, q = i & (P - 1);
-    const int t = t0 + q;
-    sm[ad(fft::brev(row, p.l0u), q)] =
-        (t < T) ? z[((size_t)row * p.N1uh + j1) * T + t] : make_float2(0.f, 0.f);
-  }
+  fft::staged_copy<8, float2>(
+      n * P, tid, nth,
+      [&](int i) {
+        const int row = i >> PLOG, t = t0 + (i & (P - 1));
+        return (t < T) ? z[((size_t)row * p.N1uh + j1) * T + t] : make_float2(0.f, 0.f);
+      },
+      [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.l0u), i & (P - 1))] = v; });
   __syncthreads();
   fft::fft_inplace<true>(sm, p.l0u, PLOG, p.tw, tid, nth, ad);
   for (int i = tid; i < n * P; i += nth) {
@@ -130,19 +132,23 @@ __global__ void __launch_bounds__(512) inv_c2r_kernel(const LateralParams p) {
   const int T = p.Tu, n = p.N1u, half = n / 2;
   const TileAddr ad{PLOG};
   const float2* __restrict__ z = p.z + (size_t)n0 * p.N1uh * T;
-  for (int i = tid; i < (half + 1) * P; i += nth) {
-    const int k = i >> PLOG, q = i & (P - 1);
-    const int t = t0 + 2 * q;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (t < T) v = __ldcs(reinterpret_cast<const float4*>(z + (size_t)k * T + t));
-    if (k == 0 || k == half) {  // C2R semantics: self-conjugate bins are real
-      v.y = 0.f;
-      v.w = 0.f;
-    }
-    // Z = Xa + i Xb ; Z[n-k] = conj(Xa) + i conj(Xb)
-    sm[ad(fft::brev(k, p.l1u), q)] = make_float2(v.x - v.w, v.y + v.z);
-    if (k != 0 && k != half) sm[ad(fft::brev(n - k, p.l1u), q)] = make_float2(v.x + v.w, v.z - v.y);
-  }
+  fft::staged_copy<8, float4>(
+      (half + 1) * P, tid, nth,
+      [&](int i) {
+        const int k = i >> PLOG, t = t0 + 2 * (i & (P - 1));
+        return (t < T) ? __ldcs(reinterpret_cast<const float4*>(z + (size_t)k * T + t))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      },
+      [&](int i, float4 v) {
+        const int k = i >> PLOG, q = i & (P - 1);
+        if (k == 0 || k == half) {  // C2R semantics: self-conjugate bins are real
+          v.y = 0.f;
+          v.w = 0.f;
+        }
+        // Z = Xa + i Xb ; Z[n-k] = conj(Xa) + i conj(Xb)
+        sm[ad(fft::brev(k, p.l1u), q)] = make_float2(v.x - v.w, v.y + v.z);
+        if (k != 0 && k != half) sm[ad(fft::brev(n - k, p.l1u), q)] = make_float2(v.x + v.w, v.z - v.y);
+      });
   __syncthreads();
   fft::fft_inplace<true>(sm, p.l1u, PLOG, p.tw, tid, nth, ad);
   float* __restrict__ out = p.out + (size_t)n0 * n * T;

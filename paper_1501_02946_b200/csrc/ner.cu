@@ -58,15 +58,15 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
   const float2* __restrict__ g = p.gh + (size_t)r * T;
 
   // 1. rotated, windowed even extension -> bit-reversed smem
-  for (int m = tid; m < n; m += nth) {
-    const int i = (m + T) & (n - 1);  // sequence index stored at slot m
-    float2 v = make_float2(0.f, 0.f);
-    if (i < 2 * T && i != T) {
-      const float2 gv = __ldcs(&g[i < T ? i : 2 * T - i]);
-      v = fft::cscale(gv, __ldg(&p.iw[i]));
-    }
-    sbuf[ad(fft::brev(m, L), 0)] = v;
-  }
+  fft::staged_copy<8, float2>(
+      n, tid, nth,
+      [&](int m) {
+        const int i = (m + T) & (n - 1);  // sequence index stored at slot m
+        float2 v = make_float2(0.f, 0.f);
+        if (i < 2 * T && i != T) v = fft::cscale(__ldcs(&g[i < T ? i : 2 * T - i]), __ldg(&p.iw[i]));
+        return v;
+      },
+      [&](int m, float2 v) { sbuf[ad(fft::brev(m, L), 0)] = v; });
   __syncthreads();
   fft::fft_inplace<false>(sbuf, L, 0, p.tw, tid, nth, ad);
 

@@ -36,39 +36,6 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int ROT, int K2, int R, int RING>
-__device__ __forceinline__ void ring_apply(float (&acc)[R][RING], const float (&w)[K2], const float (&sv)[R]) {
-#pragma unroll
-  for (int j = 0; j < K2; ++j)
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r][(ROT + j) % RING] = fmaf(w[j], sv[r], acc[r][(ROT + j) % RING]);
-}
-
-template <int K2, int R, int RING>
-__device__ __forceinline__ void ring_dispatch(int rot, float (&acc)[R][RING], const float (&w)[K2],
-                                              const float (&sv)[R]) {
-  switch (rot) {
-#define PATFFT_ROT(r) \
-  case r:             \
-    ring_apply<(r % RING), K2, R, RING>(acc, w, sv); \
-    break;
-    PATFFT_ROT(0) PATFFT_ROT(1) PATFFT_ROT(2) PATFFT_ROT(3) PATFFT_ROT(4) PATFFT_ROT(5) PATFFT_ROT(6)
-    PATFFT_ROT(7) PATFFT_ROT(8) PATFFT_ROT(9) PATFFT_ROT(10) PATFFT_ROT(11) PATFFT_ROT(12) PATFFT_ROT(13)
-    PATFFT_ROT(14) PATFFT_ROT(15)
-    default:
-      if constexpr (RING > 16) {
-        switch (rot) {
-          PATFFT_ROT(16) PATFFT_ROT(17) PATFFT_ROT(18) PATFFT_ROT(19) PATFFT_ROT(20) PATFFT_ROT(21)
-          PATFFT_ROT(22) PATFFT_ROT(23) PATFFT_ROT(24) PATFFT_ROT(25) PATFFT_ROT(26) PATFFT_ROT(27)
-          PATFFT_ROT(28) PATFFT_ROT(29) PATFFT_ROT(30) PATFFT_ROT(31)
-          default: break;
-        }
-      }
-      break;
-#undef PATFFT_ROT
-  }
-}
-
 template <int Q, int R, int RING>
 __device__ __forceinline__ void flush_q(float (&acc)[R][RING], float* __restrict__ colp, size_t row_stride,
                                         int T, int rows_valid, bool store) {
@@ -99,12 +66,14 @@ __device__ __forceinline__ void flush_group(float (&acc)[R][RING], int g, float*
 }
 
 // Record layout (float words): [0] ws (int bits), [1] sensor m (int bits),
-// [2..3] pad, [4..7] row weights (R <= 4), [8..8+KP) column weights.
+// [2..3] pad, [4..7] row weights (R <= 4), [8..8+RING) column weights
+// rotated into ring order: slot (ws + j) mod RING holds tap j, the other
+// RING - 2K slots are zero.  Every record then updates the whole ring with
+// compile-time register indices (no per-record branch on the rotation).
 template <int K2, int R, int RING, bool VEC16>
 __global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams p) {
   static_assert(K2 + 3 <= RING, "ring too small for the window");
-  constexpr int KP = (K2 + 3) & ~3;
-  constexpr int RECW = 8 + KP;
+  constexpr int RECW = 8 + RING;
   constexpr int NG = RING / 4;
   constexpr int PIECE = VEC16 ? 4 : 2;                 // floats per cp.async
   constexpr int PIECES = kThreads / PIECE;             // per record
@@ -207,16 +176,18 @@ __global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams 
       float sv[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) sv[r] = s * wrv[r];
-      float w[K2];
+      const float4* wq = reinterpret_cast<const float4*>(rec + 8);
 #pragma unroll
-      for (int j = 0; j < KP / 4; ++j) {
-        const float4 q = *reinterpret_cast<const float4*>(rec + 8 + 4 * j);
-        if (4 * j + 0 < K2) w[(4 * j + 0) % K2] = q.x;
-        if (4 * j + 1 < K2) w[(4 * j + 1) % K2] = q.y;
-        if (4 * j + 2 < K2) w[(4 * j + 2) % K2] = q.z;
-        if (4 * j + 3 < K2) w[(4 * j + 3) % K2] = q.w;
+      for (int j = 0; j < RING / 4; ++j) {
+        const float4 q = wq[j];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          acc[r][4 * j + 0] = fmaf(q.x, sv[r], acc[r][4 * j + 0]);
+          acc[r][4 * j + 1] = fmaf(q.y, sv[r], acc[r][4 * j + 1]);
+          acc[r][4 * j + 2] = fmaf(q.z, sv[r], acc[r][4 * j + 2]);
+          acc[r][4 * j + 3] = fmaf(q.w, sv[r], acc[r][4 * j + 3]);
+        }
       }
-      ring_dispatch<K2, R, RING>(ws & (RING - 1), acc, w, sv);
     }
     __syncthreads();
   }
@@ -229,8 +200,7 @@ __global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams 
 
 template <int K2, int R, int RING>
 cudaError_t go(const SpreadParams& p, int ngroups, cudaStream_t s) {
-  constexpr int KP = (K2 + 3) & ~3;
-  constexpr int RECW = 8 + KP;
+  constexpr int RECW = 8 + RING;
   const size_t smem = sizeof(float) * 2 * kChunk * (RECW + kThreads);
   dim3 grid((unsigned)(ngroups * p.nseg), (unsigned)((p.T + kThreads - 1) / kThreads));
   cudaError_t err;
@@ -249,7 +219,8 @@ cudaError_t go(const SpreadParams& p, int ngroups, cudaStream_t s) {
 }  // namespace
 
 int spread_rows_per_group(int n_lat, int K2) { return n_lat == 1 ? 1 : (K2 <= 12 ? 4 : 2); }
-int spread_record_words(int K2) { return 8 + ((K2 + 3) & ~3); }
+int spread_ring(int K2) { return K2 <= 12 ? 16 : 32; }
+int spread_record_words(int K2) { return 8 + spread_ring(K2); }
 int spread_time_chunks(int T) { return (T + kThreads - 1) / kThreads; }
 
 cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int ngroups, cudaStream_t s) {
