@@ -28,19 +28,23 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 
-// exp(-+2 pi i j / 16)
+// exp(-+2 pi i j / 32)
 template <bool INV>
-__device__ __forceinline__ float2 w16(int j) {
-  const float c[16] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
-                       0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
-                       -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
-                       0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
-  const float s = c[(j + 12) & 15];
-  return make_float2(c[j & 15], INV ? s : -s);
+__device__ __forceinline__ float2 w32(int j) {
+  const float c[32] = {1.0f, 0.98078528040323043f, 0.92387953251128674f, 0.83146961230254524f,
+                       0.70710678118654752f, 0.55557023301960218f, 0.38268343236508977f, 0.19509032201612827f,
+                       0.0f, -0.19509032201612827f, -0.38268343236508977f, -0.55557023301960218f,
+                       -0.70710678118654752f, -0.83146961230254524f, -0.92387953251128674f, -0.98078528040323043f,
+                       -1.0f, -0.98078528040323043f, -0.92387953251128674f, -0.83146961230254524f,
+                       -0.70710678118654752f, -0.55557023301960218f, -0.38268343236508977f, -0.19509032201612827f,
+                       0.0f, 0.19509032201612827f, 0.38268343236508977f, 0.55557023301960218f,
+                       0.70710678118654752f, 0.83146961230254524f, 0.92387953251128674f, 0.98078528040323043f};
+  const float s = c[(j + 24) & 31];  // sin(2 pi j/32) = cos(2 pi (j-8)/32)
+  return make_float2(c[j & 31], INV ? s : -s);
 }
 
-struct PadAddr {  // single transform, 1 pad word per 16 (bank-conflict free radix-16 passes)
-  __device__ __forceinline__ int operator()(int i, int) const { return i + (i >> 4); }
+struct PadAddr {  // single transform, 1 pad word per 32 (bank-conflict free radix-32 passes)
+  __device__ __forceinline__ int operator()(int i, int) const { return i + (i >> 5); }
 };
 struct TileAddr {  // [len][P] tile, batch fastest
   int plog;
@@ -69,7 +73,7 @@ __device__ __forceinline__ void dit_pass(float2* __restrict__ buf, int L, int pl
       if (INV) wi.y = -wi.y;
 #pragma unroll
       for (int r = 0; r < (1 << i); ++r) {
-        const float2 t = (r == 0) ? wi : cmul(wi, w16<INV>(r << (3 - i)));
+        const float2 t = (r == 0) ? wi : cmul(wi, w32<INV>(r << (4 - i)));
 #pragma unroll
         for (int m0 = 0; m0 < PR; m0 += (2 << i)) {
           const int m = m0 + r;
@@ -84,14 +88,29 @@ __device__ __forceinline__ void dit_pass(float2* __restrict__ buf, int L, int pl
   }
 }
 
+// Radix of the pass starting at stage logh of a length-2^L transform: as few
+// passes as possible (at most MAXR stages, i.e. 2^MAXR points per thread),
+// split evenly so no pass degenerates to radix 2.
+// EVEN: split the stages evenly over the passes (e.g. 10 = 4+3+3) instead of
+// greedily (10 = 4+4+2); which one is faster depends on the kernel's
+// threads per transform and register budget (measured).
+template <int MAXR, bool EVEN>
+__device__ __forceinline__ int pass_radix(int L, int logh) {
+  const int left = L - logh;
+  if (!EVEN) return left < MAXR ? left : MAXR;
+  const int passes = (left + MAXR - 1) / MAXR;
+  return (left + passes - 1) / passes;
+}
+
 // Full transform (input already bit-reversed); ends with __syncthreads.
-template <bool INV, class Addr>
+template <bool INV, int MAXR, bool EVEN, class Addr>
 __device__ __forceinline__ void fft_inplace(float2* __restrict__ buf, int L, int plog, const float2* __restrict__ tw,
                                             int tid, int nth, Addr addr) {
   int logh = 0;
   while (logh < L) {
-    const int R = min(4, L - logh);
+    const int R = pass_radix<MAXR, EVEN>(L, logh);
     switch (R) {
+      case 5: if constexpr (MAXR >= 5) dit_pass<5, INV>(buf, L, plog, logh, tw, tid, nth, addr); break;
       case 4: dit_pass<4, INV>(buf, L, plog, logh, tw, tid, nth, addr); break;
       case 3: dit_pass<3, INV>(buf, L, plog, logh, tw, tid, nth, addr); break;
       case 2: dit_pass<2, INV>(buf, L, plog, logh, tw, tid, nth, addr); break;

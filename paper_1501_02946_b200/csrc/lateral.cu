@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(512) colfft_kernel(const LateralParams p) {
       },
       [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lcols), i & (P - 1))] = v; });
   __syncthreads();
-  fft::fft_inplace<false>(sm, p.lcols, PLOG, p.tw, tid, nth, ad);
+  fft::fft_inplace<false, 4, false>(sm, p.lcols, PLOG, p.tw, tid, nth, ad);
   float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * T;
   for (int i = tid; i < p.ny * P; i += nth) {
     const int k = i >> PLOG, q = i & (P - 1);
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(512) rowfft_kernel(const LateralParams p) {
       },
       [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lrows), i & (P - 1))] = v; });
   __syncthreads();
-  fft::fft_inplace<false>(sm, p.lrows, PLOG, p.tw, tid, nth, ad);
+  fft::fft_inplace<false, 4, false>(sm, p.lrows, PLOG, p.tw, tid, nth, ad);
   const bool nyq1 = (j1 == p.N1 / 2);
   const int N0 = p.N0, mask = nr - 1;
   const float dp1 = p.dp1[j1];
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(512) inv_col_kernel(const LateralParams p) {
       },
       [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.l0u), i & (P - 1))] = v; });
   __syncthreads();
-  fft::fft_inplace<true>(sm, p.l0u, PLOG, p.tw, tid, nth, ad);
+  fft::fft_inplace<true, 4, false>(sm, p.l0u, PLOG, p.tw, tid, nth, ad);
   for (int i = tid; i < n * P; i += nth) {
     const int row = i >> PLOG, q = i & (P - 1);
     const int t = t0 + q;
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(512) inv_c2r_kernel(const LateralParams p) {
         if (k != 0 && k != half) sm[ad(fft::brev(n - k, p.l1u), q)] = make_float2(v.x + v.w, v.z - v.y);
       });
   __syncthreads();
-  fft::fft_inplace<true>(sm, p.l1u, PLOG, p.tw, tid, nth, ad);
+  fft::fft_inplace<true, 4, false>(sm, p.l1u, PLOG, p.tw, tid, nth, ad);
   float* __restrict__ out = p.out + (size_t)n0 * n * T;
   for (int i = tid; i < n * P; i += nth) {
     const int row = i >> PLOG, q = i & (P - 1);

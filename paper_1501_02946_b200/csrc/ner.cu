@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
       },
       [&](int m, float2 v) { sbuf[ad(fft::brev(m, L), 0)] = v; });
   __syncthreads();
-  fft::fft_inplace<false>(sbuf, L, 0, p.tw, tid, nth, ad);
+  fft::fft_inplace<false, 4, true>(sbuf, L, 0, p.tw, tid, nth, ad);
 
   // 2. targets
   const int j0w = r / p.N1h;
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
       }
     }
     __syncthreads();
-    fft::fft_inplace<true>(sbuf, Lu, 0, p.tw, tid, nth, ad);
+    fft::fft_inplace<true, 4, true>(sbuf, Lu, 0, p.tw, tid, nth, ad);
     float2* __restrict__ z0 = p.z + (size_t)drow0 * Tu;
     float2* __restrict__ z1 = p.z + (size_t)(drow1 >= 0 ? drow1 : drow0) * Tu;
     for (int i = tid; i < Tu; i += nth) {
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
 
 size_t ner_smem_bytes(int n_over, int Tu) {
   const int m = n_over > Tu ? n_over : Tu;
-  return (size_t)(m + m / 16 + 1) * sizeof(float2);
+  return (size_t)(m + m / 32 + 1) * sizeof(float2);  // PadAddr: 1 word per 32
 }
 
 int ner_threads(int n_over) {
