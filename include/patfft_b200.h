@@ -97,6 +97,28 @@ int patfft_nedner_execute_frames_device(patfft_nedner_plan* plan, int n_frames,
 
 void patfft_nedner_plan_destroy(patfft_nedner_plan* plan);
 
+/* ---- multi-GPU (one process per GPU; the caller runs the two exchanges) ----
+ * A sharded plan splits one reconstruction over `world` ranks:
+ *   forward  : NED spread + lateral FFT of the rank's time slice
+ *              samples_slice [M][Tr] (Tr = N_t/world)  ->  gh_send [rows_total][Tr]
+ *   exchange : all-to-all, rank q receives rows [row_start[q], row_start[q+1])
+ *              of every rank's gh_send                 ->  gh_recv [world][rows_mine][Tr]
+ *   ner      : NER + depth inverse FFT of the rank's rows
+ *              gh_recv                                 ->  z_send [world][rows_mine][Tr]
+ *   exchange : all-to-all of the world blocks          ->  z_recv [rows_total][Tr]
+ *   inverse  : lateral inverse FFT of the time slice   ->  image_slice [N0][N1][Tr]
+ * (complex buffers are float32 pairs).  Requires upsample == 1 and a
+ * power-of-two Tr.  All stages enqueue on `stream` and do not synchronise. */
+int patfft_nedner_plan_create_sharded(const patfft_nedner_desc* desc, const double* grid_positions,
+                                      const double* sensor_scale, int device, int rank, int world,
+                                      patfft_nedner_plan** out);
+/* info: rank, world, Tr, rows_total, row_begin, rows_mine, N0u, N1u */
+int patfft_nedner_shard_info(const patfft_nedner_plan* plan, int64_t info[8]);
+int patfft_nedner_shard_rows(const patfft_nedner_plan* plan, int64_t* row_starts, int n);
+int patfft_nedner_shard_forward(patfft_nedner_plan* plan, const float* samples_slice, void* gh_send, void* stream);
+int patfft_nedner_shard_ner(patfft_nedner_plan* plan, const void* gh_recv, void* z_send, void* stream);
+int patfft_nedner_shard_inverse(patfft_nedner_plan* plan, const void* z_recv, float* image_slice, void* stream);
+
 /* Per-stage device timing (CUDA events on the plan's stream).  When enabled
  * every execute records one event per stage boundary; patfft_nedner_stage_times
  * returns the accumulated milliseconds per stage and the launch count per

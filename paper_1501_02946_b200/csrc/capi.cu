@@ -166,9 +166,10 @@ extern "C" {
 const char* patfft_last_error(void) { return g_err.c_str(); }
 const char* patfft_version(void) { return "patfft-b200 0.2.0 (sm_100a)"; }
 
-int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, const double* sscale, int device,
-                              patfft_nedner_plan** out) {
+static int create_plan(const patfft_nedner_desc* d, const double* gpos, const double* sscale, int device, int rank,
+                       int world, patfft_nedner_plan** out) {
   if (!d || !gpos || !sscale || !out) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(PATFFT_ERR_PARAMETER, "invalid rank / world size");
   *out = nullptr;
   if (d->n_lat != 1 && d->n_lat != 2) return fail(PATFFT_ERR_PARAMETER, "NED transforms support 1 or 2 position axes");
   for (int a = 0; a < d->n_lat; ++a)
@@ -231,7 +232,7 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
   const Window& wcol = P->win_lat[d->n_lat - 1];
 
   // ---- NER window (nufft.py:273-285), power-of-two oversampled length ----
-  const int n_ext = 2 * P->T;
+  const int n_ext = 2 * P->T;  // NER always works on the full record length
   const int64_t n_over_t = next_pow2((int64_t)std::ceil(c * n_ext));
   if (n_over_t > 16384)
     return fail(PATFFT_ERR_UNSUPPORTED, "GPU NER supports oversampled depth lengths up to 16384 (N_t <= 4096 at c=2)");
@@ -244,7 +245,26 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
   P->custom_inverse = is_pow2(P->N0u) && is_pow2(P->N1u) && P->N0u <= 16384 && P->N1u <= 16384 && P->N1u >= 2;
 
   // ---- spreading records --------------------------------------------------
-  const int M = P->M, K2 = P->K2, nrows = P->nrows, ncols = P->ncols, T = P->T;
+  // ---- sharding: NED + lateral inverse on a time slice, NER on a row slice
+  P->rank = rank;
+  P->world = world;
+  P->rows_total = P->N0 * P->N1h;
+  P->row_starts.resize(world + 1);
+  for (int q = 0; q <= world; ++q) P->row_starts[q] = (int)((int64_t)q * P->rows_total / world);
+  P->row_begin = P->row_starts[rank];
+  P->rows_mine = P->row_starts[rank + 1] - P->row_begin;
+  P->Tr = P->T / world;
+  if (world > 1) {
+    if (P->up != 1) return fail(PATFFT_ERR_UNSUPPORTED, "sharded reconstruction requires upsample == 1");
+    if (P->T % world || !is_pow2(P->Tr) || P->Tr < 2)
+      return fail(PATFFT_ERR_UNSUPPORTED, "sharded reconstruction requires N_t / world to be a power of two");
+    if (!P->fused_ifft || !P->custom_inverse)
+      return fail(PATFFT_ERR_UNSUPPORTED, "sharded reconstruction requires power-of-two lateral and depth grids");
+    if (P->rows_mine < 1) return fail(PATFFT_ERR_UNSUPPORTED, "more ranks than lateral frequency rows");
+  }
+  // T: depth length of the spread / lateral stages (the local time slice)
+  const int M = P->M, K2 = P->K2, nrows = P->nrows, ncols = P->ncols, T = P->Tr;
+  const int Tfull = P->T;
   const int R = spread_rows_per_group(d->n_lat, K2);
   const int RECW = spread_record_words(K2);
   P->R = R;
@@ -389,8 +409,10 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
   if ((rc = upload(&P->d_tw, tw))) return rc;
   if ((rc = dalloc(&P->d_grid, (size_t)nrows * ncols * T))) return rc;
   if ((rc = dalloc(&P->d_Y, (size_t)nrows * P->N1h * T))) return rc;
-  if ((rc = dalloc(&P->d_gh, (size_t)P->N0 * P->N1h * T))) return rc;
-  if ((rc = dalloc(&P->d_z, (size_t)P->N0u * P->N1uh * P->Tu))) return rc;
+  if (world == 1) {
+    if ((rc = dalloc(&P->d_gh, (size_t)P->N0 * P->N1h * T))) return rc;
+    if ((rc = dalloc(&P->d_z, (size_t)P->N0u * P->N1uh * P->Tu))) return rc;
+  }
 
   CUDA_TRY(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
   for (auto& e : P->ev) CUDA_TRY(cudaEventCreate(&e));
@@ -422,7 +444,7 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
   q.tw = P->d_tw;
   q.jt0 = P->d_jt0;
   q.jt1 = P->d_jt1;
-  q.T = T;
+  q.T = Tfull;
   q.n_over = P->n_over_t;
   q.log_n_over = ilog2(P->n_over_t);
   q.Tu = P->Tu;
@@ -436,7 +458,30 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
   q.n_lat = P->n_lat;
   q.fused_ifft = P->fused_ifft ? 1 : 0;
   q.c_eff = wt.c_eff;
-  q.scale = (float)(1.0 / (double(P->N0) * double(P->N1) * double(T)));
+  q.scale = (float)(1.0 / (double(P->N0) * double(P->N1) * double(Tfull)));
+  if (world == 1) {
+    q.row0 = 0;
+    q.rows_local = P->rows_total;
+    q.in_tchunk = Tfull;
+    q.in_tshift = 31;
+    q.in_tmask = 0x7fffffff;
+    q.out_row0 = 0;
+    q.rows_out = P->N0u * P->N1uh;
+    q.out_tchunk = P->Tu;
+    q.out_tshift = 31;
+    q.out_tmask = 0x7fffffff;
+  } else {  // input [world][rows_mine][Tr], output [world][rows_mine][Tr]
+    q.row0 = P->row_begin;
+    q.rows_local = P->rows_mine;
+    q.in_tchunk = P->Tr;
+    q.in_tshift = ilog2(P->Tr);
+    q.in_tmask = P->Tr - 1;
+    q.out_row0 = P->row_begin;
+    q.rows_out = P->rows_mine;
+    q.out_tchunk = P->Tr;
+    q.out_tshift = ilog2(P->Tr);
+    q.out_tmask = P->Tr - 1;
+  }
 
   LateralParams& L = P->lat;
   L.grid = P->d_grid;
@@ -455,7 +500,7 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
   L.N1 = P->N1;
   L.z = P->d_z;
   L.out = nullptr;
-  L.Tu = P->Tu;
+  L.Tu = world == 1 ? P->Tu : P->Tr;
   L.N0u = P->N0u;
   L.N1u = P->N1u;
   L.N1uh = P->N1uh;
@@ -463,6 +508,82 @@ int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, c
   L.l1u = ilog2(P->N1u);
 
   *out = P.release();
+  return PATFFT_OK;
+}
+
+int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, const double* sscale, int device,
+                              patfft_nedner_plan** out) {
+  return create_plan(d, gpos, sscale, device, 0, 1, out);
+}
+
+int patfft_nedner_plan_create_sharded(const patfft_nedner_desc* d, const double* gpos, const double* sscale,
+                                      int device, int rank, int world, patfft_nedner_plan** out) {
+  return create_plan(d, gpos, sscale, device, rank, world, out);
+}
+
+int patfft_nedner_shard_info(const patfft_nedner_plan* P, int64_t info[8]) {
+  if (!P || !info) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  info[0] = P->rank;
+  info[1] = P->world;
+  info[2] = P->Tr;
+  info[3] = P->rows_total;
+  info[4] = P->row_begin;
+  info[5] = P->rows_mine;
+  info[6] = P->N0u;
+  info[7] = P->N1u;
+  return PATFFT_OK;
+}
+
+int patfft_nedner_shard_rows(const patfft_nedner_plan* P, int64_t* starts, int n) {
+  if (!P || !starts || n < P->world + 1) return fail(PATFFT_ERR_PARAMETER, "need world + 1 entries");
+  for (int q = 0; q <= P->world; ++q) starts[q] = P->row_starts[q];
+  return PATFFT_OK;
+}
+
+int patfft_nedner_shard_forward(patfft_nedner_plan* P, const float* samples_slice, void* gh_send, void* stream) {
+  if (!P || !samples_slice || !gh_send) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+  SpreadParams sp;
+  sp.samples = samples_slice;
+  sp.recs = P->d_recs;
+  sp.seg_range = P->d_segr;
+  sp.grid = P->d_grid;
+  sp.T = P->Tr;
+  sp.ncols = P->ncols;
+  sp.nrows = P->nrows;
+  sp.nseg = P->nseg;
+  sp.segw = P->segw;
+  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->ngroups, st));
+  LateralParams L = P->lat;
+  L.gh = static_cast<float2*>(gh_send);
+  CUDA_TRY(launch_lateral_col(L, st));
+  CUDA_TRY(launch_lateral_row(L, st));
+  return PATFFT_OK;
+}
+
+int patfft_nedner_shard_ner(patfft_nedner_plan* P, const void* gh_recv, void* z_send, void* stream) {
+  if (!P || !gh_recv || !z_send) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+  NerParams q = P->ner;
+  q.gh = static_cast<const float2*>(gh_recv);
+  q.z = static_cast<float2*>(z_send);
+  CUDA_TRY(launch_ner(q, P->K2, P->poly_degree, st));
+  return PATFFT_OK;
+}
+
+int patfft_nedner_shard_inverse(patfft_nedner_plan* P, const void* z_recv, float* image_slice, void* stream) {
+  if (!P || !z_recv || !image_slice) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+  LateralParams L = P->lat;
+  L.z = static_cast<float2*>(const_cast<void*>(z_recv));
+  L.out = image_slice;
+  CUDA_TRY(launch_lateral_inverse(L, st));
   return PATFFT_OK;
 }
 
@@ -480,6 +601,7 @@ int patfft_nedner_output_shape(const patfft_nedner_plan* P, int64_t shape[3]) {
 }
 
 static int execute_device_locked(patfft_nedner_plan* P, const float* samples, float* image, cudaStream_t st) {
+  if (P->world != 1) return fail(PATFFT_ERR_PARAMETER, "sharded plan: use the patfft_nedner_shard_* stages");
   const bool prof = P->profiling;
   if (prof) CUDA_TRY(cudaEventRecord(P->ev[0], st));
   SpreadParams sp;

@@ -51,11 +51,17 @@ template <int K2, int D>
 __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
   extern __shared__ float2 sbuf[];
   constexpr int K = K2 / 2;
-  const int r = blockIdx.x;  // gh row: j0w * N1h + j1
+  const int rl = blockIdx.x;         // local row of the input array
+  const int r = p.row0 + rl;         // global gh row: j0w * N1h + j1
   const int tid = threadIdx.x, nth = blockDim.x;
   const int T = p.T, n = p.n_over, L = p.log_n_over;
   const PadAddr ad;
-  const float2* __restrict__ g = p.gh + (size_t)r * T;
+  // input row rl, time t lives at gh[((t / tci) * rows_local + rl) * tci + t % tci]
+  // (tci = T for a single GPU; the power-of-two time slice per source rank
+  // when sharded; the division is a shift/mask, shift = 31 for one chunk)
+  const int tci = p.in_tchunk;
+  const float2* __restrict__ g = p.gh + (size_t)rl * tci;
+  const size_t gstride = (size_t)p.rows_local * tci;
 
   // 1. rotated, windowed even extension -> bit-reversed smem
   fft::staged_copy<8, float2>(
@@ -63,7 +69,10 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
       [&](int m) {
         const int i = (m + T) & (n - 1);  // sequence index stored at slot m
         float2 v = make_float2(0.f, 0.f);
-        if (i < 2 * T && i != T) v = fft::cscale(__ldcs(&g[i < T ? i : 2 * T - i]), __ldg(&p.iw[i]));
+        if (i < 2 * T && i != T) {
+          const int t = i < T ? i : 2 * T - i;
+          v = fft::cscale(__ldcs(&g[(t >> p.in_tshift) * gstride + (t & p.in_tmask)]), __ldg(&p.iw[i]));
+        }
         return v;
       },
       [&](int m, float2 v) { sbuf[ad(fft::brev(m, L), 0)] = v; });
@@ -174,12 +183,16 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
     }
     __syncthreads();
     fft::fft_inplace<true, 4, true>(sbuf, Lu, 0, p.tw, tid, nth, ad);
-    float2* __restrict__ z0 = p.z + (size_t)drow0 * Tu;
-    float2* __restrict__ z1 = p.z + (size_t)(drow1 >= 0 ? drow1 : drow0) * Tu;
+    // output row d, depth i lives at z[((i / tco) * rows_out + d) * tco + i % tco]
+    const int tco = p.out_tchunk;
+    const size_t zstride = (size_t)p.rows_out * tco;
+    float2* __restrict__ z0 = p.z + (size_t)(drow0 - p.out_row0) * tco;
+    float2* __restrict__ z1 = p.z + (size_t)((drow1 >= 0 ? drow1 : drow0) - p.out_row0) * tco;
     for (int i = tid; i < Tu; i += nth) {
       const float2 v = sbuf[ad(i, 0)];
-      z0[i] = v;
-      if (drow1 >= 0) z1[i] = v;
+      const size_t o = (i >> p.out_tshift) * zstride + (i & p.out_tmask);
+      z0[o] = v;
+      if (drow1 >= 0) z1[o] = v;
     }
   } else {
     // spectrum only; z was zero-filled and a batched cuFFT does the depth IFFT
@@ -219,7 +232,7 @@ int ner_threads(int n_over) {
 cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
   const int threads = ner_threads(p.n_over);
   const size_t smem = ner_smem_bytes(p.n_over, p.fused_ifft ? p.Tu : 0);
-  const unsigned rows = (unsigned)(p.N0 * p.N1h);
+  const unsigned rows = (unsigned)p.rows_local;
   cudaError_t err = cudaSuccess;
   auto go = [&](auto kern) {
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -73,6 +73,10 @@ struct NerParams {
   int T, n_over, log_n_over, Tu, log_tu;
   int N0, N1, N1h, N0u, N1uh, up, n_lat;
   int fused_ifft;      // 1: inverse depth FFT in shared memory, 0: write spectrum
+  // row / time layout (single GPU: row0 = out_row0 = 0, rows_local = N0*N1h,
+  // rows_out = N0u*N1uh, in_tchunk = T, out_tchunk = Tu)
+  int row0, rows_local, in_tchunk, in_tshift, in_tmask;
+  int out_row0, rows_out, out_tchunk, out_tshift, out_tmask;
   double c_eff;        // n_over / (2T)
   float scale;         // 1/(N0*N1*T): scipy ifftn normalisation * up^d
   float poly[kMaxTaps / 2][kMaxPolyDegree + 1];  // psihat((z + K-1/2-j)/c)/psihat(0), z in [-1/2,1/2]
@@ -137,6 +141,10 @@ struct patfft_nedner_plan {
   bool have_c2r = false, have_l = false;
 
   patfft::NerParams ner{};
+  // sharding (time-sliced NED / inverse, row-sliced NER); world = 1 for a single GPU
+  int rank = 0, world = 1, Tr = 0;          // Tr: local time slice length
+  int rows_total = 0, row_begin = 0, rows_mine = 0;
+  std::vector<int> row_starts;              // world + 1 row boundaries
   patfft::LateralParams lat{};
 
   // profiling
