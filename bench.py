@@ -227,8 +227,96 @@ def _config_json(args, rec):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def run_sharded_arm(args):
+    """One cfg reconstruction split over all ranks (strong scaling, NCCL all-to-all x2)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1501_02946_b200.parallel import ShardedNedNer
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    rec = make_workload(args.config, 0)[0]  # every rank: the same record, its own time slice
+    T = rec.samples.shape[1]
+    sh = ShardedNedNer(rec.positions, rec.weights, T, rec.dt, rec.sound_speed, rec.dx, rec.n_lateral,
+                       torch_device=dev)
+    tr = sh.layout.Tr
+    host_slice = np.ascontiguousarray(rec.samples[:, rank * tr:(rank + 1) * tr])
+    d_slice = torch.tensor(host_slice, dtype=torch.float32, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    st = sh.cuda_stream
+    for _ in range(args.warmup):
+        sh.run(d_slice)
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.wait_stream(torch.cuda.current_stream(dev))
+        a.record(st)
+        sh.run(d_slice)
+        b.record(st)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    dist.barrier()
+    t = torch.tensor([float(np.mean(times))], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    vox = _voxels(rec)
+    value = vox / (ms_step / 1e3)
+
+    # e2e: pinned f64 host slice -> device -> f32, sharded run, image slice -> pinned f64 host
+    pin_in = torch.from_numpy(host_slice).pin_memory()
+    pin_out = torch.empty(sh.layout.image_slice_shape(), dtype=torch.float64).pin_memory()
+    et = []
+    for i in range(args.warmup + args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x = pin_in.to(dev, non_blocking=True).float()
+        img = sh.run(x)
+        pin_out.copy_(img.double(), non_blocking=True)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            et.append(time.perf_counter() - t0)
+    t = torch.tensor([float(np.mean(et))], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32/c64", "data": "synthetic (seeded, BASELINE config shapes)",
+            "config": dict(_config_json(args, rec), parallelism=f"sharded x{world}: time-sliced NED, "
+                           "all-to-all, row-sliced NER, all-to-all, time-sliced lateral inverse"),
+            "clocks": clk,
+            "e2e": {"value": vox / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * host_slice.size * world,
+                    "d2h_bytes_per_step": 8 * int(np.prod(pin_out.shape)) * world, "ms_per_step": 1e3 * e2e_s},
+            "gpu_launches": 7 * args.steps, "gpu_launches_note": "per rank per step: spread, colfft, rowfft, ner, "
+            "inv_col, inv_c2r (+1 flush outside the events); 2 NCCL all-to-alls",
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()
+    return 0
+
+
 def run_gpu_arm(args):
     rank, world, local = _env_rank()
+    if args.gpus > 1 or world > 1 or args.sharded:
+        from paper_1501_02946_b200.parallel import ShardLayout
+
+        rec_T = {"cfg1": 512, "cfg2": 256, "cfg3": 512, "cfg4": 1024}.get(args.config)
+        if rec_T and ShardLayout.supported(rec_T, world):
+            return run_sharded_arm(args)
     dist = None
     if world > 1:
         import torch
@@ -398,6 +486,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-frac", type=float, default=1.0 / 16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="use the sharded multi-GPU path even at N=1")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -168,14 +168,28 @@ class ShardedNedNer:
         self.recv1 = [rm * L.Tr * 2] * self.world
         self.send2 = self.recv1
         self.recv2 = self.send1
-
-    def _stream(self):
-        if self.tdev.type == "cuda":
-            return self.torch.cuda.current_stream(self.tdev).cuda_stream
-        return 0
+        # A dedicated (non-default) stream: the C stages treat a NULL stream as
+        # "the plan's own stream", which would not be ordered with torch's
+        # legacy default stream.
+        self.cuda_stream = torch.cuda.Stream(device=torch_device) if torch_device.type == "cuda" else None
 
     def run(self, samples_slice):
-        s = self._stream()
+        """Enqueue one sharded reconstruction; returns this rank's image slice.
+
+        Work is ordered after everything already queued on the caller's current
+        stream and the caller's stream waits for the result.
+        """
+        if self.cuda_stream is None:
+            return self._run(samples_slice, 0)
+        torch = self.torch
+        cur = torch.cuda.current_stream(self.tdev)
+        self.cuda_stream.wait_stream(cur)
+        with torch.cuda.stream(self.cuda_stream):
+            out = self._run(samples_slice, self.cuda_stream.cuda_stream)
+        cur.wait_stream(self.cuda_stream)
+        return out
+
+    def _run(self, samples_slice, s):
         self.stages.forward(samples_slice, self.gh_send, s)
         self.dist.all_to_all_single(self.gh_recv, self.gh_send, output_split_sizes=self.recv1,
                                     input_split_sizes=self.send1, group=self.group)

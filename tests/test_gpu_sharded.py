@@ -22,13 +22,15 @@ def test_sharded_stages_match_single_gpu(world, case):
 
     from paper_1501_02946_b200.parallel import GpuStages, ShardLayout
 
-    rec = synth.make_3d(40 + world, 48, 256, 20e-9, case, 3, sigma=2e-3)
+    rec = synth.make_3d(40 + world, 64, 256, 20e-9, case, 3, sigma=2e-3)
     want = pb.reconstruct_nedner(rec.as_record()).values
     nl = tuple(rec.n_lateral)
     T = rec.samples.shape[1]
     L = ShardLayout(2, nl, T, world)
     dev = torch.device("cuda", 0)
-    s = torch.cuda.current_stream(dev).cuda_stream
+    stream = torch.cuda.Stream(device=dev)  # non-default: NULL would mean "plan stream" to the C stages
+    torch.cuda.set_stream(stream)
+    s = stream.cuda_stream
     stages = [GpuStages(rec.positions, rec.weights, T, rec.dt, rec.sound_speed, rec.dx, nl, nl, pb.WindowSpec(), q,
                         world, 0) for q in range(world)]
     samples = torch.tensor(rec.samples, dtype=torch.float32, device=dev)
@@ -48,6 +50,7 @@ def test_sharded_stages_match_single_gpu(world, case):
         stages[q].inverse(z_recv[q], imgs[q], s)
     torch.cuda.synchronize()
     got = torch.cat(imgs, dim=-1).double().cpu().numpy()
+    torch.cuda.set_stream(torch.cuda.default_stream(dev))
     err = rel_l2(got, want)
     print(f"world {world} {case}: rel-L2 vs single GPU {err:.2e}")
     assert err <= 1e-6
