@@ -336,25 +336,40 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   std::vector<int64_t> gstart(P->ngroups + 1, 0);
   for (const Rec& r : recs) gstart[r.grp + 1]++;
   for (int g = 0; g < P->ngroups; ++g) gstart[g + 1] += gstart[g];
+  // Blocks = (row group, column segment).  Segment boundaries (multiples of
+  // 4 columns) split each group's records into near-equal counts, so dense
+  // groups (clustered layouts) get more, narrower segments and every CTA of
+  // a time chunk does a similar amount of work.
+  std::vector<int4> blk;   // {lo, hi, c0, c1}
+  std::vector<int> blk_grp;
   {
     const int64_t tch = spread_time_chunks(T);
-    const int64_t target = 148LL * 12;
-    int64_t nseg = ceildiv(target, (int64_t)P->ngroups * tch);
-    nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, std::max(1, ncols / 64)));
-    int segw = (int)ceildiv(ncols, nseg);
-    segw = (segw + 3) / 4 * 4;
-    P->segw = segw;
-    P->nseg = (int)ceildiv(ncols, segw);
-  }
-  std::vector<int2> segr((size_t)P->ngroups * P->nseg);
-  for (int g = 0; g < P->ngroups; ++g) {
-    auto b = recs.begin() + gstart[g], e = recs.begin() + gstart[g + 1];
-    for (int s = 0; s < P->nseg; ++s) {
-      const int c0 = s * P->segw, c1 = std::min(ncols, c0 + P->segw);
-      auto lo = std::lower_bound(b, e, c0 - K2 + 1, [](const Rec& x, int v) { return x.ws < v; });
-      auto hi = std::lower_bound(b, e, c1, [](const Rec& x, int v) { return x.ws < v; });
-      segr[(size_t)g * P->nseg + s] = make_int2((int)(lo - recs.begin()), (int)(hi - recs.begin()));
+    const int64_t target_blocks = 148LL * 16;  // ~4 resident CTAs/SM x 4 waves
+    const int64_t per_chunk = std::max<int64_t>(1, ceildiv(target_blocks, tch));
+    const int64_t nrec_all = std::max<int64_t>(1, (int64_t)recs.size());
+    const double rec_per_block = std::max(64.0, (double)nrec_all / (double)per_chunk);
+    for (int g = 0; g < P->ngroups; ++g) {
+      auto b = recs.begin() + gstart[g], e = recs.begin() + gstart[g + 1];
+      const int64_t ng = e - b;
+      int nseg = (int)std::max<int64_t>(1, std::llround(ng / rec_per_block));
+      nseg = std::min(nseg, std::max(1, ncols / 16));
+      std::vector<int> cuts{0};
+      for (int s = 1; s < nseg; ++s) {
+        const int64_t idx = ng * s / nseg;
+        int col = (b + idx)->ws + K2 / 2;  // centre of that record's window
+        col = std::max(0, std::min(ncols, (col + 2) / 4 * 4));
+        if (col > cuts.back() && col < ncols) cuts.push_back(col);
+      }
+      cuts.push_back(ncols);
+      for (size_t s = 0; s + 1 < cuts.size(); ++s) {
+        const int c0 = cuts[s], c1 = cuts[s + 1];
+        auto lo = std::lower_bound(b, e, c0 - K2 + 1, [](const Rec& x, int v) { return x.ws < v; });
+        auto hi = std::lower_bound(b, e, c1, [](const Rec& x, int v) { return x.ws < v; });
+        blk.push_back(make_int4((int)(lo - recs.begin()), (int)(hi - recs.begin()), c0, c1));
+        blk_grp.push_back(g);
+      }
     }
+    P->nblk = (int)blk.size();
   }
 
   // ---- deapodisation (nufft.py:367-371), normalised by psi_hat(0) --------
@@ -400,7 +415,8 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // ---- device buffers -----------------------------------------------------
   int rc;
   if ((rc = upload(&P->d_recs, recbuf))) return rc;
-  if ((rc = upload(&P->d_segr, segr))) return rc;
+  if ((rc = upload(&P->d_blk, blk))) return rc;
+  if ((rc = upload(&P->d_blkgrp, blk_grp))) return rc;
   if ((rc = upload(&P->d_dp0, dp0))) return rc;
   if ((rc = upload(&P->d_dp1, dp1))) return rc;
   if ((rc = upload(&P->d_jt0, jt0))) return rc;
@@ -548,14 +564,13 @@ int patfft_nedner_shard_forward(patfft_nedner_plan* P, const float* samples_slic
   SpreadParams sp;
   sp.samples = samples_slice;
   sp.recs = P->d_recs;
-  sp.seg_range = P->d_segr;
+  sp.blk = P->d_blk;
+  sp.blk_grp = P->d_blkgrp;
   sp.grid = P->d_grid;
   sp.T = P->Tr;
   sp.ncols = P->ncols;
   sp.nrows = P->nrows;
-  sp.nseg = P->nseg;
-  sp.segw = P->segw;
-  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->ngroups, st));
+  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
   LateralParams L = P->lat;
   L.gh = static_cast<float2*>(gh_send);
   CUDA_TRY(launch_lateral_col(L, st));
@@ -607,14 +622,13 @@ static int execute_device_locked(patfft_nedner_plan* P, const float* samples, fl
   SpreadParams sp;
   sp.samples = samples;
   sp.recs = P->d_recs;
-  sp.seg_range = P->d_segr;
+  sp.blk = P->d_blk;
+  sp.blk_grp = P->d_blkgrp;
   sp.grid = P->d_grid;
   sp.T = P->T;
   sp.ncols = P->ncols;
   sp.nrows = P->nrows;
-  sp.nseg = P->nseg;
-  sp.segw = P->segw;
-  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->ngroups, st));
+  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
   if (prof) CUDA_TRY(cudaEventRecord(P->ev[1], st));
   LateralParams L = P->lat;
   L.out = image;
@@ -700,7 +714,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
   for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_gh,
-                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_segr,
+                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_blk, (void*)P->d_blkgrp,
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_tw, (void*)P->d_jt0,
                   (void*)P->d_jt1})
     free_dev(p);

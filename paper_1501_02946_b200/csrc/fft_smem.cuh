@@ -20,13 +20,40 @@ namespace fft {
 
 constexpr int kLogTwiddles = 14;  // table length 16384
 
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+// Packed FP32 (sm_100a FADD2 / FMUL2 / FFMA2): one issue slot per complex
+// add, two per complex multiply.  The compiler folds broadcast scalars,
+// operand swaps and negations into the packed instructions' operand modifiers.
+#define PATFFT_F2_BINOP(op)                                                                                  \
+  __device__ __forceinline__ float2 f2##op(float2 a, float2 b) {                                           \
+    float2 d;                                                                                               \
+    asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t" #op                 \
+        ".rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n}"                                                \
+        : "=f"(d.x), "=f"(d.y)                                                                              \
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));                                                          \
+    return d;                                                                                               \
+  }
+PATFFT_F2_BINOP(add)
+PATFFT_F2_BINOP(sub)
+PATFFT_F2_BINOP(mul)
+#undef PATFFT_F2_BINOP
+
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+// a * b = a.x * (b.x, b.y) + a.y * (-b.y, b.x)
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return f2fma(make_float2(a.y, a.y), make_float2(-b.y, b.x), f2mul(make_float2(a.x, a.x), b));
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return f2add(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return f2sub(a, b); }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return f2mul(a, make_float2(s, s)); }
 
 // exp(-+2 pi i j / 32)
 template <bool INV>

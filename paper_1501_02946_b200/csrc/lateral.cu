@@ -24,7 +24,7 @@ namespace {
 using fft::TileAddr;
 
 template <int PLOG>
-__global__ void __launch_bounds__(512) colfft_kernel(const LateralParams p) {
+__global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int u0 = blockIdx.x;
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(512) colfft_kernel(const LateralParams p) {
 }
 
 template <int PLOG>
-__global__ void __launch_bounds__(512) rowfft_kernel(const LateralParams p) {
+__global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int j1 = blockIdx.x;
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(512) rowfft_kernel(const LateralParams p) {
 }
 
 template <int PLOG>
-__global__ void __launch_bounds__(512) inv_col_kernel(const LateralParams p) {
+__global__ void __launch_bounds__(512, 2) inv_col_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int j1 = blockIdx.x;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(512) inv_col_kernel(const LateralParams p) {
 }
 
 template <int PLOG>
-__global__ void __launch_bounds__(512) inv_c2r_kernel(const LateralParams p) {
+__global__ void __launch_bounds__(512, 2) inv_c2r_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int n0 = blockIdx.x;

@@ -43,9 +43,10 @@ constexpr int kMaxPolyDegree = 12;
 struct SpreadParams {
   const float* samples;   // [M][T] float32, device
   const float* recs;      // per (row group) column-sorted records, see spread.cu
-  const int2* seg_range;  // per (row group, column segment): [lo, hi) into recs
+  const int4* blk;        // per CTA column: {lo, hi, c0, c1} -- records [lo, hi), columns [c0, c1)
+  const int* blk_grp;     // per CTA column: row group
   float* grid;            // [nrows][ncols][T] centred oversampled grid
-  int T, ncols, nrows, nseg, segw;
+  int T, ncols, nrows;
 };
 
 struct LateralParams {
@@ -83,7 +84,7 @@ struct NerParams {
 };
 
 // Kernel launchers
-cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int ngroups, cudaStream_t s);
+cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaStream_t s);
 int spread_rows_per_group(int n_lat, int K2);
 int spread_record_words(int K2);
 int spread_time_chunks(int T);
@@ -112,7 +113,7 @@ struct patfft_nedner_plan {
   int nrows = 1, ncols = 0, N1h = 0;
   int N0u = 1, N1u = 0, N1uh = 0, Tu = 0;
   int n_over_t = 0, K2 = 12, poly_degree = 8;
-  int R = 4, ngroups = 0, nseg = 1, segw = 0;
+  int R = 4, ngroups = 0, nblk = 0;
   int64_t n_records = 0;
   bool fused_ifft = true;
   bool custom_inverse = true;
@@ -129,7 +130,8 @@ struct patfft_nedner_plan {
   float* d_out = nullptr;       // [N0u][N1u][Tu] f32 (host path staging)
   double* d_out64 = nullptr;
   float* d_recs = nullptr;
-  int2* d_segr = nullptr;
+  int4* d_blk = nullptr;
+  int* d_blkgrp = nullptr;
   float* d_dp0 = nullptr;
   float* d_dp1 = nullptr;
   float* d_iw = nullptr;

@@ -36,21 +36,35 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Packed FP32 FMA (sm_100a FFMA2): two lanes of work per issue slot; a
+// broadcast scalar operand (s, s) is folded into the instruction.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
 template <int Q, int R, int RING>
-__device__ __forceinline__ void flush_q(float (&acc)[R][RING], float* __restrict__ colp, size_t row_stride,
+__device__ __forceinline__ void flush_q(float2 (&acc)[R][RING / 2], float* __restrict__ colp, size_t row_stride,
                                         int T, int rows_valid, bool store) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (store && r < rows_valid) colp[(size_t)r * row_stride + (size_t)c * T] = acc[r][Q * 4 + c];
-      acc[r][Q * 4 + c] = 0.f;
+    for (int c = 0; c < 2; ++c) {
+      if (store && r < rows_valid) {
+        colp[(size_t)r * row_stride + (size_t)(2 * c) * T] = acc[r][Q * 2 + c].x;
+        colp[(size_t)r * row_stride + (size_t)(2 * c + 1) * T] = acc[r][Q * 2 + c].y;
+      }
+      acc[r][Q * 2 + c] = make_float2(0.f, 0.f);
     }
   }
 }
 
 template <int R, int RING>
-__device__ __forceinline__ void flush_group(float (&acc)[R][RING], int g, float* __restrict__ base, size_t row_stride,
+__device__ __forceinline__ void flush_group(float2 (&acc)[R][RING / 2], int g, float* __restrict__ base, size_t row_stride,
                                             int T, int c0, int c1, int rows_valid, bool tvalid) {
   const int col = g * 4;
   const bool store = tvalid && col >= c0 && col < c1;
@@ -82,17 +96,16 @@ __global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams 
   float* rbuf = reinterpret_cast<float*>(smem4);             // [2][kChunk][RECW]
   float* sbuf = rbuf + 2 * kChunk * RECW;                    // [2][kChunk][kThreads]
 
-  const int gsx = blockIdx.x;
-  const int grp = gsx / p.nseg;
-  const int seg = gsx - grp * p.nseg;
-  const int c0 = seg * p.segw;
-  const int c1 = min(p.ncols, c0 + p.segw);
+  const int4 bk = p.blk[blockIdx.x];
+  const int grp = p.blk_grp[blockIdx.x];
+  const int c0 = bk.z;
+  const int c1 = bk.w;
   const int T = p.T;
   const int t0 = blockIdx.y * kThreads;
   const int tid = threadIdx.x;
   const int t = t0 + tid;
   const bool tvalid = t < T;
-  const int2 rg = p.seg_range[gsx];
+  const int2 rg = make_int2(bk.x, bk.y);
   const int nrec = rg.y - rg.x;
   const int nchunks = (nrec + kChunk - 1) / kChunk;
   const int row0 = grp * R;
@@ -134,11 +147,11 @@ __global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams 
     cp_commit();
   };
 
-  float acc[R][RING];
+  float2 acc[R][RING / 2];  // column pairs (2c, 2c+1)
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int c = 0; c < RING; ++c) acc[r][c] = 0.f;
+    for (int c = 0; c < RING / 2; ++c) acc[r][c] = make_float2(0.f, 0.f);
 
   const size_t row_stride = (size_t)p.ncols * T;
   float* base = p.grid + (size_t)row0 * row_stride + (tvalid ? t : 0);
@@ -182,10 +195,9 @@ __global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams 
         const float4 q = wq[j];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          acc[r][4 * j + 0] = fmaf(q.x, sv[r], acc[r][4 * j + 0]);
-          acc[r][4 * j + 1] = fmaf(q.y, sv[r], acc[r][4 * j + 1]);
-          acc[r][4 * j + 2] = fmaf(q.z, sv[r], acc[r][4 * j + 2]);
-          acc[r][4 * j + 3] = fmaf(q.w, sv[r], acc[r][4 * j + 3]);
+          const float2 svv = make_float2(sv[r], sv[r]);
+          acc[r][2 * j + 0] = ffma2(make_float2(q.x, q.y), svv, acc[r][2 * j + 0]);
+          acc[r][2 * j + 1] = ffma2(make_float2(q.z, q.w), svv, acc[r][2 * j + 1]);
         }
       }
     }
@@ -199,10 +211,10 @@ __global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams 
 }
 
 template <int K2, int R, int RING>
-cudaError_t go(const SpreadParams& p, int ngroups, cudaStream_t s) {
+cudaError_t go(const SpreadParams& p, int nblk, cudaStream_t s) {
   constexpr int RECW = 8 + RING;
   const size_t smem = sizeof(float) * 2 * kChunk * (RECW + kThreads);
-  dim3 grid((unsigned)(ngroups * p.nseg), (unsigned)((p.T + kThreads - 1) / kThreads));
+  dim3 grid((unsigned)nblk, (unsigned)((p.T + kThreads - 1) / kThreads));
   cudaError_t err;
   if (p.T % 4 == 0) {
     auto k = spread_kernel<K2, R, RING, true>;
@@ -223,31 +235,31 @@ int spread_ring(int K2) { return K2 <= 12 ? 16 : 32; }
 int spread_record_words(int K2) { return 8 + spread_ring(K2); }
 int spread_time_chunks(int T) { return (T + kThreads - 1) / kThreads; }
 
-cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int ngroups, cudaStream_t s) {
+cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaStream_t s) {
   if (R == 4) {
     switch (K2) {
-      case 2: return go<2, 4, 16>(p, ngroups, s);
-      case 4: return go<4, 4, 16>(p, ngroups, s);
-      case 6: return go<6, 4, 16>(p, ngroups, s);
-      case 8: return go<8, 4, 16>(p, ngroups, s);
-      case 10: return go<10, 4, 16>(p, ngroups, s);
-      case 12: return go<12, 4, 16>(p, ngroups, s);
+      case 2: return go<2, 4, 16>(p, nblk, s);
+      case 4: return go<4, 4, 16>(p, nblk, s);
+      case 6: return go<6, 4, 16>(p, nblk, s);
+      case 8: return go<8, 4, 16>(p, nblk, s);
+      case 10: return go<10, 4, 16>(p, nblk, s);
+      case 12: return go<12, 4, 16>(p, nblk, s);
     }
   } else if (R == 2) {
     switch (K2) {
-      case 14: return go<14, 2, 32>(p, ngroups, s);
-      case 16: return go<16, 2, 32>(p, ngroups, s);
+      case 14: return go<14, 2, 32>(p, nblk, s);
+      case 16: return go<16, 2, 32>(p, nblk, s);
     }
   } else if (R == 1) {
     switch (K2) {
-      case 2: return go<2, 1, 16>(p, ngroups, s);
-      case 4: return go<4, 1, 16>(p, ngroups, s);
-      case 6: return go<6, 1, 16>(p, ngroups, s);
-      case 8: return go<8, 1, 16>(p, ngroups, s);
-      case 10: return go<10, 1, 16>(p, ngroups, s);
-      case 12: return go<12, 1, 16>(p, ngroups, s);
-      case 14: return go<14, 1, 32>(p, ngroups, s);
-      case 16: return go<16, 1, 32>(p, ngroups, s);
+      case 2: return go<2, 1, 16>(p, nblk, s);
+      case 4: return go<4, 1, 16>(p, nblk, s);
+      case 6: return go<6, 1, 16>(p, nblk, s);
+      case 8: return go<8, 1, 16>(p, nblk, s);
+      case 10: return go<10, 1, 16>(p, nblk, s);
+      case 12: return go<12, 1, 16>(p, nblk, s);
+      case 14: return go<14, 1, 32>(p, nblk, s);
+      case 16: return go<16, 1, 32>(p, nblk, s);
     }
   }
   return cudaErrorInvalidValue;
