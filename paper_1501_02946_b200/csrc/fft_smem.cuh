@@ -70,8 +70,18 @@ __device__ __forceinline__ float2 w32(int j) {
   return make_float2(c[j & 31], INV ? s : -s);
 }
 
-struct PadAddr {  // single transform, 1 pad word per 32 (bank-conflict free radix-32 passes)
-  __device__ __forceinline__ int operator()(int i, int) const { return i + (i >> 5); }
+struct PadAddr {  // single transform, 1 pad element per 16 (bank-conflict free radix-16 passes)
+  __device__ __forceinline__ int operator()(int i, int) const { return i + (i >> 4); }
+};
+// Single transform of length 2^L, XOR-swizzled: the low 4 bits (the 8-byte
+// slot within a 128-byte row) are XOR-ed with bits 4..7 and with the top 4
+// bits.  Bijective, no padding, and conflict-free for the radix-16 passes,
+// the bit-reversed input scatter (stride 2^(L-5) between lanes) and the
+// stride-~4 interpolation gathers of the NER.
+struct SwzAddr {
+  int sh;  // L - 4 (31 when L < 8)
+  __device__ __forceinline__ int operator()(int i, int) const { return i ^ (((i >> 4) ^ (i >> sh)) & 15); }
+  static __device__ __forceinline__ SwzAddr for_log(int L) { return SwzAddr{L >= 8 ? L - 4 : 31}; }
 };
 struct TileAddr {  // [len][P] tile, batch fastest
   int plog;

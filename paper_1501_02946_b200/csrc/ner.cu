@@ -25,7 +25,7 @@
 namespace patfft {
 namespace {
 
-using fft::PadAddr;
+using fft::SwzAddr;
 
 constexpr int kMaxTargetsPerThread = 8;
 
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
   const int r = p.row0 + rl;         // global gh row: j0w * N1h + j1
   const int tid = threadIdx.x, nth = blockDim.x;
   const int T = p.T, n = p.n_over, L = p.log_n_over;
-  const PadAddr ad;
+  const SwzAddr ad = SwzAddr::for_log(L);
   // input row rl, time t lives at gh[((t / tci) * rows_local + rl) * tci + t % tci]
   // (tci = T for a single GPU; the power-of-two time slice per source rank
   // when sharded; the division is a shift/mask, shift = 31 for one chunk)
@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
       [&](int m, float2 v) { sbuf[ad(fft::brev(m, L), 0)] = v; });
   __syncthreads();
   fft::fft_inplace<false, 4, true>(sbuf, L, 0, p.tw, tid, nth, ad);
+  const SwzAddr gad = ad;
 
   // 2. targets
   const int j0w = r / p.N1h;
@@ -119,8 +120,8 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
           for (int d = (D % 2 ? D - 2 : D - 3); d >= 1; d -= 2) o = fmaf(o, z2, p.poly[j][d]);
           const float wa = fmaf(z, o, e);
           const float wb = fmaf(-z, o, e);
-          const float2 Fa = sbuf[ad((k0 + j - K + 1) & (n - 1), 0)];
-          const float2 Fb = sbuf[ad((k0 + K - j) & (n - 1), 0)];
+          const float2 Fa = sbuf[gad((k0 + j - K + 1) & (n - 1), 0)];
+          const float2 Fb = sbuf[gad((k0 + K - j) & (n - 1), 0)];
           acc.x = fmaf(wa, Fa.x, fmaf(wb, Fb.x, acc.x));
           acc.y = fmaf(wa, Fa.y, fmaf(wb, Fb.y, acc.y));
         }
@@ -163,8 +164,9 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
   __syncthreads();  // forward spectrum fully consumed
   if (p.fused_ifft) {
     const int Lu = p.log_tu;
+    const SwzAddr iad = SwzAddr::for_log(Lu);
     if (p.up > 1) {
-      for (int i = tid; i < Tu; i += nth) sbuf[ad(i, 0)] = make_float2(0.f, 0.f);
+      for (int i = tid; i < Tu; i += nth) sbuf[iad(i, 0)] = make_float2(0.f, 0.f);
       __syncthreads();
     }
 #pragma unroll
@@ -175,21 +177,21 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
       const float2 v = fft::cscale(vals[it], dfac);
       if (ls == -(T / 2) && p.up > 1) {
         const float2 hv = fft::cscale(v, 0.5f);
-        sbuf[ad(fft::brev(T / 2, Lu), 0)] = hv;
-        sbuf[ad(fft::brev(Tu - T / 2, Lu), 0)] = hv;
+        sbuf[iad(fft::brev(T / 2, Lu), 0)] = hv;
+        sbuf[iad(fft::brev(Tu - T / 2, Lu), 0)] = hv;
       } else {
-        sbuf[ad(fft::brev(ls >= 0 ? ls : Tu + ls, Lu), 0)] = v;
+        sbuf[iad(fft::brev(ls >= 0 ? ls : Tu + ls, Lu), 0)] = v;
       }
     }
     __syncthreads();
-    fft::fft_inplace<true, 4, true>(sbuf, Lu, 0, p.tw, tid, nth, ad);
+    fft::fft_inplace<true, 4, true>(sbuf, Lu, 0, p.tw, tid, nth, iad);
     // output row d, depth i lives at z[((i / tco) * rows_out + d) * tco + i % tco]
     const int tco = p.out_tchunk;
     const size_t zstride = (size_t)p.rows_out * tco;
     float2* __restrict__ z0 = p.z + (size_t)(drow0 - p.out_row0) * tco;
     float2* __restrict__ z1 = p.z + (size_t)((drow1 >= 0 ? drow1 : drow0) - p.out_row0) * tco;
     for (int i = tid; i < Tu; i += nth) {
-      const float2 v = sbuf[ad(i, 0)];
+      const float2 v = sbuf[iad(i, 0)];
       const size_t o = (i >> p.out_tshift) * zstride + (i & p.out_tmask);
       z0[o] = v;
       if (drow1 >= 0) z1[o] = v;
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
 
 size_t ner_smem_bytes(int n_over, int Tu) {
   const int m = n_over > Tu ? n_over : Tu;
-  return (size_t)(m + m / 32 + 1) * sizeof(float2);  // PadAddr: 1 word per 32
+  return (size_t)m * sizeof(float2);  // SwzAddr layout: no padding
 }
 
 int ner_threads(int n_over) {
