@@ -160,6 +160,99 @@ __device__ __forceinline__ void fft_inplace(float2* __restrict__ buf, int L, int
 
 __device__ __forceinline__ int brev(int i, int L) { return L ? (int)(__brev((unsigned)i) >> (32 - L)) : 0; }
 
+// ---------------------------------------------------------------------------
+// Compile-time variants: transform length 2^L, batch 2^PLOG and the CTA size
+// NTH are template parameters, so the pass schedule, strides, masks and
+// item loops fold to constants (used for the common power-of-two sizes; the
+// runtime versions above remain the fallback).
+// ---------------------------------------------------------------------------
+template <int L>
+struct SwzC {  // SwzAddr with a compile-time shift
+  static constexpr int sh = L >= 8 ? L - 4 : 31;
+  __device__ __forceinline__ int operator()(int i, int) const { return i ^ (((i >> 4) ^ (i >> sh)) & 15); }
+};
+template <int PLOG>
+struct TileC {
+  __device__ __forceinline__ int operator()(int i, int p) const { return (i << PLOG) + p; }
+};
+
+template <int R, bool INV, int L, int PLOG, int LOGH, int NTH, class Addr>
+__device__ __forceinline__ void dit_pass_ct(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
+                                            Addr addr) {
+  constexpr int PR = 1 << R;
+  constexpr int H = 1 << LOGH;
+  constexpr int ITEMS = 1 << (L - R + PLOG);
+  constexpr int ITER = (ITEMS + NTH - 1) / NTH;
+#pragma unroll
+  for (int j = 0; j < ITER; ++j) {
+    const int it = tid + j * NTH;
+    if ((ITEMS % NTH) != 0 && it >= ITEMS) break;
+    const int p = it & ((1 << PLOG) - 1);
+    const int q = it >> PLOG;
+    const int k = q & (H - 1);
+    const int base = ((q >> LOGH) << (LOGH + R)) + k;
+    float2 e[PR];
+#pragma unroll
+    for (int m = 0; m < PR; ++m) e[m] = buf[addr(base + m * H, p)];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      float2 wi = __ldg(&tw[k << (kLogTwiddles - LOGH - i - 1)]);
+      if (INV) wi.y = -wi.y;
+#pragma unroll
+      for (int r = 0; r < (1 << i); ++r) {
+        const float2 t = (r == 0) ? wi : cmul(wi, w32<INV>(r << (4 - i)));
+#pragma unroll
+        for (int m0 = 0; m0 < PR; m0 += (2 << i)) {
+          const int m = m0 + r;
+          const float2 x = cmul(e[m + (1 << i)], t);
+          e[m + (1 << i)] = csub(e[m], x);
+          e[m] = cadd(e[m], x);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < PR; ++m) buf[addr(base + m * H, p)] = e[m];
+  }
+}
+
+template <int L, int MAXR, bool EVEN, int LOGH>
+struct PassRadix {
+  static constexpr int left = L - LOGH;
+  static constexpr int passes = (left + MAXR - 1) / MAXR;
+  static constexpr int value = EVEN ? (left + passes - 1) / passes : (left < MAXR ? left : MAXR);
+};
+
+// Full compile-time transform (input bit-reversed); ends with __syncthreads.
+template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, int LOGH = 0, class Addr>
+__device__ __forceinline__ void fft_ct(float2* __restrict__ buf, const float2* __restrict__ tw, int tid, Addr addr) {
+  if constexpr (LOGH < L) {
+    constexpr int R = PassRadix<L, MAXR, EVEN, LOGH>::value;
+    dit_pass_ct<R, INV, L, PLOG, LOGH, NTH>(buf, tw, tid, addr);
+    __syncthreads();
+    fft_ct<INV, L, MAXR, EVEN, PLOG, NTH, LOGH + R>(buf, tw, tid, addr);
+  }
+}
+
+// staged_copy with compile-time sizes
+template <int B, int TOTAL, int NTH, class V, class Load, class Store>
+__device__ __forceinline__ void staged_copy_ct(int tid, Load load, Store store) {
+  constexpr int ITER = (TOTAL + NTH - 1) / NTH;
+#pragma unroll
+  for (int i0 = 0; i0 < ITER; i0 += B) {
+    V v[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int i = tid + (i0 + k) * NTH;
+      if (i0 + k < ITER && ((TOTAL % NTH) == 0 || i < TOTAL)) v[k] = load(i);
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int i = tid + (i0 + k) * NTH;
+      if (i0 + k < ITER && ((TOTAL % NTH) == 0 || i < TOTAL)) store(i, v[k]);
+    }
+  }
+}
+
 // Global -> shared staging with up to B independent loads in flight per
 // thread (all loads of a batch are issued before the first store).
 template <int B, class V, class Load, class Store>

@@ -47,14 +47,23 @@ __device__ __forceinline__ float2 cospi_sinpi(float r) {
   }
 }
 
-template <int K2, int D>
+// LOGT > 0: compile-time variant for T = 2^LOGT, n_over = 4T, upsample 1,
+// fused depth IFFT, NTH = T/4 threads (clamped to [64, 512]); LOGT = 0: all
+// sizes at run time.
+template <int K2, int D, int LOGT>
 __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
+  constexpr bool CT = LOGT > 0;
+  constexpr int CT_T = CT ? (1 << LOGT) : 1;
+  constexpr int CT_NTH = CT ? ((CT_T / 4) < 64 ? 64 : ((CT_T / 4) > 512 ? 512 : CT_T / 4)) : 1;
   extern __shared__ float2 sbuf[];
   constexpr int K = K2 / 2;
   const int rl = blockIdx.x;         // local row of the input array
   const int r = p.row0 + rl;         // global gh row: j0w * N1h + j1
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int T = p.T, n = p.n_over, L = p.log_n_over;
+  const int tid = threadIdx.x;
+  const int nth = CT ? CT_NTH : (int)blockDim.x;
+  const int T = CT ? CT_T : p.T;
+  const int n = CT ? 4 * CT_T : p.n_over;
+  const int L = CT ? LOGT + 2 : p.log_n_over;
   const SwzAddr ad = SwzAddr::for_log(L);
   // input row rl, time t lives at gh[((t / tci) * rows_local + rl) * tci + t % tci]
   // (tci = T for a single GPU; the power-of-two time slice per source rank
@@ -64,9 +73,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
   const size_t gstride = (size_t)p.rows_local * tci;
 
   // 1. rotated, windowed even extension -> bit-reversed smem
-  fft::staged_copy<8, float2>(
-      n, tid, nth,
-      [&](int m) {
+  auto load_ext = [&](int m) {
         const int i = (m + T) & (n - 1);  // sequence index stored at slot m
         float2 v = make_float2(0.f, 0.f);
         if (i < 2 * T && i != T) {
@@ -74,10 +81,17 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
           v = fft::cscale(__ldcs(&g[(t >> p.in_tshift) * gstride + (t & p.in_tmask)]), __ldg(&p.iw[i]));
         }
         return v;
-      },
-      [&](int m, float2 v) { sbuf[ad(fft::brev(m, L), 0)] = v; });
-  __syncthreads();
-  fft::fft_inplace<false, 4, true>(sbuf, L, 0, p.tw, tid, nth, ad);
+  };
+  auto store_brev = [&](int m, float2 v) { sbuf[ad(fft::brev(m, L), 0)] = v; };
+  if constexpr (CT) {
+    fft::staged_copy_ct<8, 4 * CT_T, CT_NTH, float2>(tid, load_ext, store_brev);
+    __syncthreads();
+    fft::fft_ct<false, LOGT + 2, 4, true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT + 2>());
+  } else {
+    fft::staged_copy<8, float2>(n, tid, nth, load_ext, store_brev);
+    __syncthreads();
+    fft::fft_inplace<false, 4, true>(sbuf, L, 0, p.tw, tid, nth, ad);
+  }
   const SwzAddr gad = ad;
 
   // 2. targets
@@ -160,12 +174,12 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
     dfac = f0 * f1;
   }
 
-  const int Tu = p.Tu;
+  const int Tu = CT ? CT_T : p.Tu;
   __syncthreads();  // forward spectrum fully consumed
-  if (p.fused_ifft) {
-    const int Lu = p.log_tu;
+  if (CT || p.fused_ifft) {
+    const int Lu = CT ? LOGT : p.log_tu;
     const SwzAddr iad = SwzAddr::for_log(Lu);
-    if (p.up > 1) {
+    if (!CT && p.up > 1) {
       for (int i = tid; i < Tu; i += nth) sbuf[iad(i, 0)] = make_float2(0.f, 0.f);
       __syncthreads();
     }
@@ -175,7 +189,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
       if (l >= T) break;
       const int ls = (l < T / 2) ? l : l - T;
       const float2 v = fft::cscale(vals[it], dfac);
-      if (ls == -(T / 2) && p.up > 1) {
+      if (!CT && ls == -(T / 2) && p.up > 1) {
         const float2 hv = fft::cscale(v, 0.5f);
         sbuf[iad(fft::brev(T / 2, Lu), 0)] = hv;
         sbuf[iad(fft::brev(Tu - T / 2, Lu), 0)] = hv;
@@ -184,12 +198,14 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
       }
     }
     __syncthreads();
-    fft::fft_inplace<true, 4, true>(sbuf, Lu, 0, p.tw, tid, nth, iad);
+    if constexpr (CT) fft::fft_ct<true, LOGT, 4, true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT>());
+    else fft::fft_inplace<true, 4, true>(sbuf, Lu, 0, p.tw, tid, nth, iad);
     // output row d, depth i lives at z[((i / tco) * rows_out + d) * tco + i % tco]
     const int tco = p.out_tchunk;
     const size_t zstride = (size_t)p.rows_out * tco;
     float2* __restrict__ z0 = p.z + (size_t)(drow0 - p.out_row0) * tco;
     float2* __restrict__ z1 = p.z + (size_t)((drow1 >= 0 ? drow1 : drow0) - p.out_row0) * tco;
+#pragma unroll 4
     for (int i = tid; i < Tu; i += nth) {
       const float2 v = sbuf[iad(i, 0)];
       const size_t o = (i >> p.out_tshift) * zstride + (i & p.out_tmask);
@@ -232,7 +248,7 @@ int ner_threads(int n_over) {
 }
 
 cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
-  const int threads = ner_threads(p.n_over);
+  int threads = ner_threads(p.n_over);
   const size_t smem = ner_smem_bytes(p.n_over, p.fused_ifft ? p.Tu : 0);
   const unsigned rows = (unsigned)p.rows_local;
   cudaError_t err = cudaSuccess;
@@ -242,10 +258,24 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
     kern<<<rows, threads, smem, s>>>(p);
     err = cudaGetLastError();
   };
+  // compile-time variant for the default window (2K = 12, degree 8), c_eff = 2,
+  // upsample 1 and T = 2^7 .. 2^11
+  const bool ct_ok = K2 == 12 && degree == 8 && p.fused_ifft && p.up == 1 && p.n_over == 4 * p.T &&
+                     p.Tu == p.T && p.log_n_over >= 9 && p.log_n_over <= 13;
+  if (ct_ok) {
+    threads = ner_threads(p.n_over);
+    switch (p.log_n_over - 2) {
+      case 7: go(ner_kernel<12, 8, 7>); return err;
+      case 8: go(ner_kernel<12, 8, 8>); return err;
+      case 9: go(ner_kernel<12, 8, 9>); return err;
+      case 10: go(ner_kernel<12, 8, 10>); return err;
+      case 11: go(ner_kernel<12, 8, 11>); return err;
+    }
+  }
 #define PATFFT_NER_CASE(k2)                          \
   case k2:                                           \
-    if (degree == 8) go(ner_kernel<k2, 8>);          \
-    else go(ner_kernel<k2, 12>);                     \
+    if (degree == 8) go(ner_kernel<k2, 8, 0>);       \
+    else go(ner_kernel<k2, 12, 0>);                  \
     break;
   switch (K2) {
     PATFFT_NER_CASE(2)
