@@ -23,13 +23,20 @@ namespace {
 
 using fft::TileAddr;
 
-template <int PLOG>
+constexpr int nth_for(int L, int PLOG) {
+  return ((L >= 4 ? (1 << (L - 4)) : 1) << PLOG) < 64 ? 64
+         : (((L >= 4 ? (1 << (L - 4)) : 1) << PLOG) > 512 ? 512 : ((L >= 4 ? (1 << (L - 4)) : 1) << PLOG));
+}
+
+// LC > 0: compile-time transform length 2^LC (launched with nth_for(LC, PLOG) threads)
+template <int PLOG, int LC>
 __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int u0 = blockIdx.x;
   const int t0 = blockIdx.y * 2 * P;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = threadIdx.x;
+  const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.T, n = p.ncols;
   const TileAddr ad{PLOG};
   const float* __restrict__ src = p.grid + (size_t)u0 * n * T;
@@ -41,7 +48,8 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
       },
       [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lcols), i & (P - 1))] = v; });
   __syncthreads();
-  fft::fft_inplace<false, 4, false>(sm, p.lcols, PLOG, p.tw, tid, nth, ad);
+  if constexpr (LC > 0) fft::fft_ct<false, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
+  else fft::fft_inplace<false, 4, false>(sm, p.lcols, PLOG, p.tw, tid, nth, ad);
   float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * T;
   for (int i = tid; i < p.ny * P; i += nth) {
     const int k = i >> PLOG, q = i & (P - 1);
@@ -55,13 +63,14 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
   }
 }
 
-template <int PLOG>
+template <int PLOG, int LC>
 __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int j1 = blockIdx.x;
   const int t0 = blockIdx.y * P;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = threadIdx.x;
+  const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.T, nr = p.nrows;
   const TileAddr ad{PLOG};
   fft::staged_copy<8, float2>(
@@ -72,7 +81,8 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
       },
       [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lrows), i & (P - 1))] = v; });
   __syncthreads();
-  fft::fft_inplace<false, 4, false>(sm, p.lrows, PLOG, p.tw, tid, nth, ad);
+  if constexpr (LC > 0) fft::fft_ct<false, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
+  else fft::fft_inplace<false, 4, false>(sm, p.lrows, PLOG, p.tw, tid, nth, ad);
   const bool nyq1 = (j1 == p.N1 / 2);
   const int N0 = p.N0, mask = nr - 1;
   const float dp1 = p.dp1[j1];
@@ -96,13 +106,14 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
   }
 }
 
-template <int PLOG>
+template <int PLOG, int LC>
 __global__ void __launch_bounds__(512, 2) inv_col_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int j1 = blockIdx.x;
   const int t0 = blockIdx.y * P;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = threadIdx.x;
+  const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.Tu, n = p.N0u;
   const TileAddr ad{PLOG};
   float2* __restrict__ z = p.z;
@@ -114,7 +125,8 @@ __global__ void __launch_bounds__(512, 2) inv_col_kernel(const LateralParams p) 
       },
       [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.l0u), i & (P - 1))] = v; });
   __syncthreads();
-  fft::fft_inplace<true, 4, false>(sm, p.l0u, PLOG, p.tw, tid, nth, ad);
+  if constexpr (LC > 0) fft::fft_ct<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
+  else fft::fft_inplace<true, 4, false>(sm, p.l0u, PLOG, p.tw, tid, nth, ad);
   for (int i = tid; i < n * P; i += nth) {
     const int row = i >> PLOG, q = i & (P - 1);
     const int t = t0 + q;
@@ -122,13 +134,14 @@ __global__ void __launch_bounds__(512, 2) inv_col_kernel(const LateralParams p) 
   }
 }
 
-template <int PLOG>
+template <int PLOG, int LC>
 __global__ void __launch_bounds__(512, 2) inv_c2r_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int n0 = blockIdx.x;
   const int t0 = blockIdx.y * 2 * P;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = threadIdx.x;
+  const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.Tu, n = p.N1u, half = n / 2;
   const TileAddr ad{PLOG};
   const float2* __restrict__ z = p.z + (size_t)n0 * p.N1uh * T;
@@ -150,7 +163,8 @@ __global__ void __launch_bounds__(512, 2) inv_c2r_kernel(const LateralParams p) 
         if (k != 0 && k != half) sm[ad(fft::brev(n - k, p.l1u), q)] = make_float2(v.x + v.w, v.z - v.y);
       });
   __syncthreads();
-  fft::fft_inplace<true, 4, false>(sm, p.l1u, PLOG, p.tw, tid, nth, ad);
+  if constexpr (LC > 0) fft::fft_ct<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
+  else fft::fft_inplace<true, 4, false>(sm, p.l1u, PLOG, p.tw, tid, nth, ad);
   float* __restrict__ out = p.out + (size_t)n0 * n * T;
   for (int i = tid; i < n * P; i += nth) {
     const int row = i >> PLOG, q = i & (P - 1);
@@ -187,12 +201,22 @@ int threads_for(int len, int plog) {
         err = cudaGetLastError();                                                                      \
       }                                                                                                \
     };                                                                                                 \
+    if (plog == 4) {                                                                                   \
+      switch (len) {                                                                                   \
+        case 64: run(NAME##_kernel<4, 6>); return err;                                                 \
+        case 128: run(NAME##_kernel<4, 7>); return err;                                                \
+        case 256: run(NAME##_kernel<4, 8>); return err;                                                \
+        case 512: run(NAME##_kernel<4, 9>); return err;                                                \
+      }                                                                                                \
+    }                                                                                                  \
+    if (plog == 3 && len == 1024) { run(NAME##_kernel<3, 10>); return err; }                           \
+    if (plog == 2 && len == 2048) { run(NAME##_kernel<2, 11>); return err; }                           \
     switch (plog) {                                                                                    \
-      case 4: run(NAME##_kernel<4>); break;                                                            \
-      case 3: run(NAME##_kernel<3>); break;                                                            \
-      case 2: run(NAME##_kernel<2>); break;                                                            \
-      case 1: run(NAME##_kernel<1>); break;                                                            \
-      default: run(NAME##_kernel<0>); break;                                                           \
+      case 4: run(NAME##_kernel<4, 0>); break;                                                         \
+      case 3: run(NAME##_kernel<3, 0>); break;                                                         \
+      case 2: run(NAME##_kernel<2, 0>); break;                                                         \
+      case 1: run(NAME##_kernel<1, 0>); break;                                                         \
+      default: run(NAME##_kernel<0, 0>); break;                                                        \
     }                                                                                                  \
     return err;                                                                                        \
   }
