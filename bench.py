@@ -365,7 +365,6 @@ def run_gpu_arm(args):
         step()
     _lib.check(lib.patfft_stream_sync(stream))
 
-    plan.set_profiling(True)
     clocks = Clocks(device)
     if dist is not None:
         dist.barrier()
@@ -384,6 +383,14 @@ def run_gpu_arm(args):
     clk = clocks.stop()
     if dist is not None:
         dist.barrier()
+    # per-stage breakdown: a separate pass with stage events (stages serialised,
+    # so each kernel's duration is attributable; the timed steps above overlap
+    # the spread with the lateral FFTs on two streams)
+    plan.set_profiling(True)
+    for _ in range(max(3, args.steps // 2)):
+        _lib.check(lib.patfft_l2_flush(d_flush, flush_bytes, stream))
+        step()
+    _lib.check(lib.patfft_stream_sync(stream))
     stages = plan.stage_times()
     plan.set_profiling(False)
     ms_step = float(np.mean(times))

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -160,6 +161,9 @@ void free_dev(void* p) {
 }
 
 }  // namespace
+
+static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* gh, cudaStream_t st, bool overlap,
+                           bool prof);
 
 extern "C" {
 
@@ -431,7 +435,16 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   }
 
   CUDA_TRY(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  if (const char* e = std::getenv("PATFFT_OVERLAP_CHUNKS")) P->overlap_chunks = std::max(1, std::min(4, std::atoi(e)));
+  {
+    int lo = 0, hi = 0;
+    CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(cudaStreamCreateWithPriority(&P->stream2, cudaStreamNonBlocking, hi));
+  }
   for (auto& e : P->ev) CUDA_TRY(cudaEventCreate(&e));
+  for (auto& e : P->ev_chunk) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
 
   // ---- cuFFT only for sizes the shared-memory kernels do not cover --------
   if (!P->custom_inverse) {
@@ -561,21 +574,7 @@ int patfft_nedner_shard_forward(patfft_nedner_plan* P, const float* samples_slic
   std::lock_guard<std::mutex> lk(P->mu);
   CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
-  SpreadParams sp;
-  sp.samples = samples_slice;
-  sp.recs = P->d_recs;
-  sp.blk = P->d_blk;
-  sp.blk_grp = P->d_blkgrp;
-  sp.grid = P->d_grid;
-  sp.T = P->Tr;
-  sp.ncols = P->ncols;
-  sp.nrows = P->nrows;
-  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
-  LateralParams L = P->lat;
-  L.gh = static_cast<float2*>(gh_send);
-  CUDA_TRY(launch_lateral_col(L, st));
-  CUDA_TRY(launch_lateral_row(L, st));
-  return PATFFT_OK;
+  return enqueue_forward(P, samples_slice, static_cast<float2*>(gh_send), st, true, false);
 }
 
 int patfft_nedner_shard_ner(patfft_nedner_plan* P, const void* gh_recv, void* z_send, void* stream) {
@@ -615,27 +614,73 @@ int patfft_nedner_output_shape(const patfft_nedner_plan* P, int64_t shape[3]) {
   return 2;
 }
 
-static int execute_device_locked(patfft_nedner_plan* P, const float* samples, float* image, cudaStream_t st) {
-  if (P->world != 1) return fail(PATFFT_ERR_PARAMETER, "sharded plan: use the patfft_nedner_shard_* stages");
-  const bool prof = P->profiling;
-  if (prof) CUDA_TRY(cudaEventRecord(P->ev[0], st));
+}  // extern "C"
+
+// Spread + lateral forward FFTs of the plan's local time range into `gh`.
+// overlap: the time axis is cut into chunks (multiples of 128 samples); the
+// FFMA-bound spread of chunk c+1 runs on `st` while the memory/SMEM-bound
+// lateral FFTs of chunk c run on the plan's second (higher-priority) stream.
+// Without overlap (profiling) the three kernels run back to back on `st`
+// with the stage events in between.
+static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* gh, cudaStream_t st, bool overlap,
+                           bool prof) {
+  const int T = P->Tr;  // == P->T for a single GPU
   SpreadParams sp;
   sp.samples = samples;
   sp.recs = P->d_recs;
   sp.blk = P->d_blk;
   sp.blk_grp = P->d_blkgrp;
   sp.grid = P->d_grid;
-  sp.T = P->T;
+  sp.T = T;
   sp.ncols = P->ncols;
   sp.nrows = P->nrows;
-  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
-  if (prof) CUDA_TRY(cudaEventRecord(P->ev[1], st));
+  LateralParams L = P->lat;
+  L.gh = gh;
+  const int nc = overlap ? std::max(1, std::min(P->overlap_chunks, T / 128)) : 1;
+  if (nc == 1) {
+    sp.t_begin = L.t_begin = 0;
+    sp.t_end = L.t_end = T;
+    CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
+    if (prof) CUDA_TRY(cudaEventRecord(P->ev[1], st));
+    CUDA_TRY(launch_lateral_col(L, st));
+    if (prof) CUDA_TRY(cudaEventRecord(P->ev[2], st));
+    CUDA_TRY(launch_lateral_row(L, st));
+    if (prof) CUDA_TRY(cudaEventRecord(P->ev[3], st));
+    return PATFFT_OK;
+  }
+  const int chunk = ((T + nc - 1) / nc + 127) / 128 * 128;
+  CUDA_TRY(cudaEventRecord(P->ev_fork, st));
+  CUDA_TRY(cudaStreamWaitEvent(P->stream2, P->ev_fork, 0));
+  int used = 0;
+  for (int k = 0; k < nc; ++k) {
+    const int tb = k * chunk, te = std::min(T, tb + chunk);
+    if (tb >= te) break;
+    sp.t_begin = tb;
+    sp.t_end = te;
+    CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
+    CUDA_TRY(cudaEventRecord(P->ev_chunk[k], st));
+    used = k + 1;
+  }
+  for (int k = 0; k < used; ++k) {
+    L.t_begin = k * chunk;
+    L.t_end = std::min(T, L.t_begin + chunk);
+    CUDA_TRY(cudaStreamWaitEvent(P->stream2, P->ev_chunk[k], 0));
+    CUDA_TRY(launch_lateral_col(L, P->stream2));
+    CUDA_TRY(launch_lateral_row(L, P->stream2));
+  }
+  CUDA_TRY(cudaEventRecord(P->ev_join, P->stream2));
+  CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
+  return PATFFT_OK;
+}
+
+static int execute_device_locked(patfft_nedner_plan* P, const float* samples, float* image, cudaStream_t st) {
+  if (P->world != 1) return fail(PATFFT_ERR_PARAMETER, "sharded plan: use the patfft_nedner_shard_* stages");
+  const bool prof = P->profiling;
+  if (prof) CUDA_TRY(cudaEventRecord(P->ev[0], st));
+  int rc = enqueue_forward(P, samples, P->d_gh, st, !prof, prof);
+  if (rc) return rc;
   LateralParams L = P->lat;
   L.out = image;
-  CUDA_TRY(launch_lateral_col(L, st));
-  if (prof) CUDA_TRY(cudaEventRecord(P->ev[2], st));
-  CUDA_TRY(launch_lateral_row(L, st));
-  if (prof) CUDA_TRY(cudaEventRecord(P->ev[3], st));
   if (P->up > 1 || !P->fused_ifft)
     CUDA_TRY(cudaMemsetAsync(P->d_z, 0, sizeof(float2) * (size_t)P->N0u * P->N1uh * P->Tu, st));
   CUDA_TRY(launch_ner(P->ner, P->K2, P->poly_degree, st));
@@ -663,6 +708,8 @@ static int execute_device_locked(patfft_nedner_plan* P, const float* samples, fl
   }
   return PATFFT_OK;
 }
+
+extern "C" {
 
 int patfft_nedner_execute_device(patfft_nedner_plan* P, const float* samples, float* image, void* stream) {
   if (!P || !samples || !image) return fail(PATFFT_ERR_PARAMETER, "null argument");
@@ -718,8 +765,14 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_tw, (void*)P->d_jt0,
                   (void*)P->d_jt1})
     free_dev(p);
+  if (P->stream2) cudaStreamSynchronize(P->stream2);
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : P->ev_chunk)
+    if (e) cudaEventDestroy(e);
+  if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+  if (P->ev_join) cudaEventDestroy(P->ev_join);
+  if (P->stream2) cudaStreamDestroy(P->stream2);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
 }

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int u0 = blockIdx.x;
-  const int t0 = blockIdx.y * 2 * P;
+  const int t0 = p.t_begin + blockIdx.y * 2 * P;
   const int tid = threadIdx.x;
   const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.T, n = p.ncols;
@@ -44,7 +44,8 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
       n * P, tid, nth,
       [&](int i) {
         const int row = i >> PLOG, t = t0 + 2 * (i & (P - 1));
-        return (t < T) ? __ldcs(reinterpret_cast<const float2*>(src + (size_t)row * T + t)) : make_float2(0.f, 0.f);
+        return (t < p.t_end) ? __ldcs(reinterpret_cast<const float2*>(src + (size_t)row * T + t))
+                             : make_float2(0.f, 0.f);
       },
       [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lcols), i & (P - 1))] = v; });
   __syncthreads();
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
   for (int i = tid; i < p.ny * P; i += nth) {
     const int k = i >> PLOG, q = i & (P - 1);
     const int t = t0 + 2 * q;
-    if (t >= T) continue;
+    if (t >= p.t_end) continue;
     const float2 zk = sm[ad(k, q)];
     const float2 zm = fft::conjf2(sm[ad((n - k) & (n - 1), q)]);
     const float2 d = fft::csub(zk, zm);
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int j1 = blockIdx.x;
-  const int t0 = blockIdx.y * P;
+  const int t0 = p.t_begin + blockIdx.y * P;
   const int tid = threadIdx.x;
   const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.T, nr = p.nrows;
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
       nr * P, tid, nth,
       [&](int i) {
         const int row = i >> PLOG, t = t0 + (i & (P - 1));
-        return (t < T) ? __ldcs(p.Y + ((size_t)row * p.ny + j1) * T + t) : make_float2(0.f, 0.f);
+        return (t < p.t_end) ? __ldcs(p.Y + ((size_t)row * p.ny + j1) * T + t) : make_float2(0.f, 0.f);
       },
       [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lrows), i & (P - 1))] = v; });
   __syncthreads();
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
   for (int i = tid; i < N0 * P; i += nth) {
     const int j0w = i >> PLOG, q = i & (P - 1);
     const int t = t0 + q;
-    if (t >= T) continue;
+    if (t >= p.t_end) continue;
     const int a = (N0 > 1) ? (j0w < N0 / 2 ? j0w : j0w - N0) : 0;
     const bool nyq0 = (N0 > 1) && (a == -(N0 / 2));
     float2 v;
@@ -231,11 +232,11 @@ PATFFT_DEF_LAUNCH(inv_c2r)
 }  // namespace
 
 cudaError_t launch_lateral_col(const LateralParams& p, cudaStream_t s) {
-  return launch_colfft(p, p.ncols, dim3((unsigned)p.nrows, (unsigned)p.T), 2, s);
+  return launch_colfft(p, p.ncols, dim3((unsigned)p.nrows, (unsigned)(p.t_end - p.t_begin)), 2, s);
 }
 
 cudaError_t launch_lateral_row(const LateralParams& p, cudaStream_t s) {
-  return launch_rowfft(p, p.nrows, dim3((unsigned)p.ny, (unsigned)p.T), 1, s);
+  return launch_rowfft(p, p.nrows, dim3((unsigned)p.ny, (unsigned)(p.t_end - p.t_begin)), 1, s);
 }
 
 cudaError_t launch_lateral_inverse(const LateralParams& p, cudaStream_t s) {

@@ -47,6 +47,7 @@ struct SpreadParams {
   const int* blk_grp;     // per CTA column: row group
   float* grid;            // [nrows][ncols][T] centred oversampled grid
   int T, ncols, nrows;
+  int t_begin, t_end;     // time range processed by this launch (multiples of 128)
 };
 
 struct LateralParams {
@@ -58,6 +59,7 @@ struct LateralParams {
   const float* dp0;    // [N0] deapodisation (wrapped index)
   const float* dp1;    // [N1]
   int T, nrows, lrows, ncols, lcols, ny, N0, N1;
+  int t_begin, t_end;  // forward kernels: time range processed by this launch
   // inverse
   float2* z;           // [N0u][N1uh][Tu]
   float* out;          // [N0u][N1u][Tu]
@@ -106,6 +108,9 @@ cudaError_t launch_fill(float* dst, size_t n, float v, cudaStream_t s);
 struct patfft_nedner_plan {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // lateral FFTs overlapped with the spread
+  cudaEvent_t ev_chunk[4] = {}, ev_fork = nullptr, ev_join = nullptr;
+  int overlap_chunks = 1;  // time chunks of the overlapped forward stages (1 = off)
   std::mutex mu;
 
   // sizes

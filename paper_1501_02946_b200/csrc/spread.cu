@@ -101,10 +101,10 @@ __global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams 
   const int c0 = bk.z;
   const int c1 = bk.w;
   const int T = p.T;
-  const int t0 = blockIdx.y * kThreads;
+  const int t0 = p.t_begin + blockIdx.y * kThreads;
   const int tid = threadIdx.x;
   const int t = t0 + tid;
-  const bool tvalid = t < T;
+  const bool tvalid = t < p.t_end;
   const int2 rg = make_int2(bk.x, bk.y);
   const int nrec = rg.y - rg.x;
   const int nchunks = (nrec + kChunk - 1) / kChunk;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams 
   const int rec_lane = tid / PIECES;
   constexpr int REC_STEP = kThreads / PIECES;
   const int tp = t0 + piece * PIECE;
-  const int src_bytes = max(0, min(PIECE, T - tp)) * 4;
+  const int src_bytes = max(0, min(PIECE, p.t_end - tp)) * 4;
 
   int mnext[PER_THREAD];
   auto load_m = [&](int c) {
@@ -214,7 +214,7 @@ template <int K2, int R, int RING>
 cudaError_t go(const SpreadParams& p, int nblk, cudaStream_t s) {
   constexpr int RECW = 8 + RING;
   const size_t smem = sizeof(float) * 2 * kChunk * (RECW + kThreads);
-  dim3 grid((unsigned)nblk, (unsigned)((p.T + kThreads - 1) / kThreads));
+  dim3 grid((unsigned)nblk, (unsigned)((p.t_end - p.t_begin + kThreads - 1) / kThreads));
   cudaError_t err;
   if (p.T % 4 == 0) {
     auto k = spread_kernel<K2, R, RING, true>;
