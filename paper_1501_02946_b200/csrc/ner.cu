@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
       }
     }
     __syncthreads();
-    if constexpr (CT) fft::fft_ct<true, LOGT, 4, true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT>());
+    if constexpr (CT) fft::fft_ct<true, LOGT, (CT_NTH * 4 >= CT_T ? 2 : 4), true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT>());
     else fft::fft_inplace<true, 4, true>(sbuf, Lu, 0, p.tw, tid, nth, iad);
     // output row d, depth i lives at z[((i / tco) * rows_out + d) * tco + i % tco]
     const int tco = p.out_tchunk;
