@@ -82,6 +82,27 @@ def main():
     recon_case("recon_3d_rect16x24",
                synth.SyntheticRecord(pos, w, samples, 20e-9, synth.SOUND_SPEED, synth.PITCH, nl))
 
+    # 8. wide window (K = 8 -> 16 taps, the 32-slot spread ring) and narrow K = 2
+    recon_case("recon_3d_specK8", synth.make_3d(18, 16, 32, 20e-9, "jittered", 2), spec={"c": 2.0, "K": 8})
+    recon_case("recon_2d_specK2", synth.make_2d(seed=19, n=32, nt=128), spec={"c": 2.0, "K": 2})
+    # 9. explicit window shape and a larger oversampling factor (c = 2.5)
+    recon_case("recon_3d_spec_c25", synth.make_3d(20, 16, 32, 20e-9, "uniform", 2),
+               spec={"c": 2.5, "K": 6, "alpha": 12.0, "beta": 2.3})
+    # 10. upsample 3 (non-power-of-two depth and lateral inverse sizes)
+    recon_case("recon_3d_up3", synth.make_3d(21, 8, 16, 20e-9, "jittered", 1), upsample=3)
+    # 11. every sensor exactly on the aperture corner / edges (wrap-around taps on both axes)
+    rng = np.random.default_rng(22)
+    n = 16
+    half = n * synth.PITCH / 2
+    edge = np.concatenate([rng.uniform(-half, half, size=(200, 2)),
+                           np.array([[-half, -half], [half, half], [-half, half], [half, -half],
+                                     [0.0, half], [half, 0.0], [-half, 0.0], [0.0, -half]])])
+    balls = [(0.2e-3, 0.1e-3, 2.0e-3, 0.6e-3, 1.0)]
+    samples = synth.ball_traces(edge, 32, 20e-9, synth.SOUND_SPEED, balls)
+    w = np.full(edge.shape[0], (n * synth.PITCH) ** 2 / edge.shape[0])
+    recon_case("recon_3d_edges16", synth.SyntheticRecord(edge, w, samples, 20e-9, synth.SOUND_SPEED, synth.PITCH,
+                                                         (n, n)))
+
     # component goldens: NER (per-row targets) and NED (1 and 2 axes)
     rng = np.random.default_rng(21)
     n = 64

@@ -108,3 +108,34 @@ def test_gpu_accepts_reference_style_record_object():
     f = pb.reconstruct_nedner(r)
     want, _ = O.reconstruct_nedner(s.positions, s.weights, s.samples, s.dt, s.sound_speed, s.dx, s.n_lateral)
     assert rel_l2(f.values, want) <= TOL
+
+
+def test_gpu_full_size_cfg3_matches_oracle():
+    # BASELINE config 3 at full size (128^2 sensors x 512): the oracle takes ~10-20 s
+    s = synth.CONFIGS["cfg3"]()
+    f = pb.reconstruct_nedner(s.as_record())
+    want, _ = O.reconstruct_nedner(s.positions, s.weights, s.samples, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    err = rel_l2(f.values, want)
+    print(f"cfg3 full size: rel-L2 {err:.3e}")
+    assert err <= TOL
+
+
+def test_gpu_full_size_cfg4_properties():
+    # BASELINE config 4 (256^2 clustered x 1024): size-independent properties --
+    # linearity, bit-determinism and finite output (the oracle needs ~2 min here)
+    s = synth.CONFIGS["cfg4"]()
+    r1 = s.as_record()
+    rng = np.random.default_rng(1)
+    noise = rng.standard_normal(r1.samples.shape)
+    r2 = s.as_record()
+    r2.samples = noise
+    r3 = s.as_record()
+    r3.samples = 0.5 * r1.samples - 2.0 * noise
+    f1 = pb.reconstruct_nedner(r1).values
+    f1b = pb.reconstruct_nedner(r1).values
+    f2 = pb.reconstruct_nedner(r2).values
+    f3 = pb.reconstruct_nedner(r3).values
+    assert f1.shape == (256, 256, 1024)
+    assert np.array_equal(f1, f1b)
+    assert np.all(np.isfinite(f1))
+    assert rel_l2(f3, 0.5 * f1 - 2.0 * f2) <= 1e-5
