@@ -244,6 +244,32 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_t) / n_ext, &P->win_t, &err))
     return fail(PATFFT_ERR_PARAMETER, err);
   P->fused_ifft = is_pow2(P->Tu) && P->Tu <= 16384;
+
+  // An explicit alpha/beta fixes the window in frequency units; the GPU grids
+  // are powers of two, so when its effective oversampling differs from the
+  // reference's (even 11-smooth length) the same (alpha, beta, K) can cover a
+  // different part of the window.  Probe the accuracy at the GPU sizes and
+  // refuse loudly instead of returning a silently different answer.
+  if (!std::isnan(d->spec_alpha) || !std::isnan(d->spec_beta)) {
+    struct Probe { const Window* w; int n, n_over, n_over_ref; };
+    std::vector<Probe> probes;
+    for (int a = 0; a < d->n_lat; ++a)
+      probes.push_back({&P->win_lat[a], d->out_dims[a], n_over_lat[a], even_fast_len(c * d->out_dims[a])});
+    probes.push_back({&P->win_t, n_ext, P->n_over_t, even_fast_len(c * n_ext)});
+    for (const Probe& pr : probes) {
+      if (pr.n_over == pr.n_over_ref || pr.n_over > 8192) continue;
+      const double e = window_relative_error(*pr.w, pr.n, pr.n_over);
+      if (!(e <= 1e-6)) {
+        char buf[320];
+        std::snprintf(buf, sizeof buf,
+                      "window (c=%g, K=%d, alpha=%g, beta=%g) loses accuracy at the GPU's power-of-two oversampled "
+                      "length %d (reference uses %d; probe error %.2e): use the default alpha/beta or a c with c*N a "
+                      "power of two",
+                      c, K, pr.w->alpha, pr.w->beta, pr.n_over, pr.n_over_ref, e);
+        return fail(PATFFT_ERR_UNSUPPORTED, buf);
+      }
+    }
+  }
   if (P->T > 8 * ner_threads(P->n_over_t))
     return fail(PATFFT_ERR_UNSUPPORTED, "depth too long for the NER CTA layout");
   P->custom_inverse = is_pow2(P->N0u) && is_pow2(P->N1u) && P->N0u <= 16384 && P->N1u <= 16384 && P->N1u >= 2;

@@ -33,6 +33,7 @@ double bessel_i0(double x);                   // scipy.special.i0 equivalent
 double kb_psi(const Window& w, double th);    // window_eval (nufft.py:159-165)
 double kb_psihat(const Window& w, double x);  // window_ft_eval (nufft.py:168-187)
 int even_fast_len(double target);             // next_even_fast_len (nufft.py:83-89)
+double window_relative_error(const Window& w, int n, int n_over);  // accuracy probe (window.cpp)
 
 // ---------------------------------------------------------------------------
 // Device-side parameter blocks

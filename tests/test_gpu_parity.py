@@ -23,11 +23,21 @@ def _record(g):
                            float(g["dx"]), tuple(int(n) for n in g["n_lateral"]))
 
 
+# explicit (alpha, beta) at an oversampling whose reference length is not a
+# power of two: the GPU refuses (DeviceError) instead of answering differently
+REFUSED = {"recon_3d_spec_c25.npz"}
+
+
 @pytest.mark.parametrize("path", golden_recon_files(), ids=os.path.basename)
 def test_gpu_matches_reference_golden(path):
     g = np.load(path)
     c, K, a, b = golden_spec(g)
     spec = pb.WindowSpec(c=c, K=K, alpha=a, beta=b)
+    if os.path.basename(path) in REFUSED:
+        with pytest.raises(pb.DeviceError, match="power-of-two"):
+            pb.reconstruct_nedner(_record(g), out_dims=tuple(int(n) for n in g["out_dims"]),
+                                  upsample=int(g["upsample"]), spec=spec)
+        return
     f = pb.reconstruct_nedner(_record(g), out_dims=tuple(int(n) for n in g["out_dims"]),
                               upsample=int(g["upsample"]), spec=spec)
     assert f.values.shape == g["values"].shape
