@@ -71,6 +71,18 @@ typedef struct patfft_nedner_plan patfft_nedner_plan;
 int patfft_nedner_plan_create(const patfft_nedner_desc* desc, const double* grid_positions,
                               const double* sensor_scale, int device, patfft_nedner_plan** out);
 
+/* Complete-grid variants (every lateral grid node has exactly one sensor):
+ *   time_eval = 0 : reconstruct_equispaced  (recon.py:345-355) -- plain lateral
+ *                   FFT of the cube, NER NUFFT along time;
+ *   time_eval = 1 : reconstruct_interp_fft  (recon.py:382-389) -- plain lateral
+ *                   FFT, linear interpolation of the length-2N_t FFT.
+ *   grid_index : M, flat lateral grid index (row-major over n_lateral) of each
+ *                sensor row, as recon.py:311-324 computes it.
+ * Weights are not used (the reference ignores them on these paths); execute
+ * with the same patfft_nedner_execute* calls.                              */
+int patfft_equispaced_plan_create(const patfft_nedner_desc* desc, const int64_t* grid_index, int time_eval,
+                                  int device, patfft_nedner_plan** out);
+
 /* Output volume shape (N0*up, N1*up, Nt*up) or (N*up, Nt*up); returns rank. */
 int patfft_nedner_output_shape(const patfft_nedner_plan* plan, int64_t shape[3]);
 

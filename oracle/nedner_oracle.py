@@ -301,11 +301,24 @@ def fhat_rows(gh_rows, j2_rows, nt, spec):
     return 0.5 * phi * scale
 
 
-def assemble_fhat(gh, nt, spec, ratios):
+def fhat_rows_interp(gh_rows, j2_rows, nt):
+    """Steps 2-3 with linear interpolation of the 2T FFT (recon.py:297-303)."""
+    kap_e, scale = ner_targets(j2_rows, nt)
+    spect = sfft.fft(even_extension(gh_rows), axis=-1)
+    i0 = np.floor(kap_e).astype(np.int64)
+    frac = kap_e - i0
+    r = np.arange(spect.shape[0])[:, None]
+    phi = spect[r, i0 % (2 * nt)] * (1.0 - frac) + spect[r, (i0 + 1) % (2 * nt)] * frac
+    return 0.5 * phi * scale
+
+
+def assemble_fhat(gh, nt, spec, ratios, time_eval="nufft"):
     """Warped time-axis NER + amplitude + band over the whole lateral grid (recon.py:274-308)."""
     n_lateral = gh.shape[:-1]
     nrows = int(np.prod(n_lateral)) if n_lateral else 1
     j2 = lateral_freq_sq(n_lateral, ratios).reshape(nrows)
+    if time_eval == "interp":
+        return fhat_rows_interp(gh.reshape(nrows, nt), j2, nt).reshape(gh.shape)
     return fhat_rows(gh.reshape(nrows, nt), j2, nt, spec).reshape(gh.shape)
 
 
@@ -381,6 +394,38 @@ def reconstruct_nedner(positions, weights, samples, dt, sound_speed, dx, n_later
     ratios = lateral_ratios(nt, dt, sound_speed, dx, n_lateral)
     fhat = assemble_fhat(gh, nt, spec, ratios)                                    # recon.py:378
     return invert_spectrum(fhat, upsample)                                        # recon.py:379
+
+
+def full_grid_cube(positions, samples, dx, n_lateral):
+    """Samples placed on the complete lateral grid, centred (recon.py:311-333)."""
+    pos = np.atleast_2d(np.asarray(positions, dtype=np.float64)) / dx
+    if pos.shape[1] != len(n_lateral):
+        pos = pos.T
+    idx = np.rint(pos).astype(np.int64)
+    if np.max(np.abs(pos - idx)) > 1e-6:
+        raise ValueError("record positions do not form the complete sensor grid")
+    for ax, n in enumerate(n_lateral):
+        idx[:, ax] += n // 2
+    flat = np.ravel_multi_index(tuple(idx.T), n_lateral)
+    if len(np.unique(flat)) != int(np.prod(n_lateral)) or flat.size != int(np.prod(n_lateral)):
+        raise ValueError("record positions do not form the complete sensor grid")
+    cube = np.empty((int(np.prod(n_lateral)), samples.shape[1]))
+    cube[flat] = samples
+    return cube.reshape(tuple(n_lateral) + (samples.shape[1],))
+
+
+def reconstruct_equispaced(positions, samples, dt, sound_speed, dx, n_lateral, upsample=1,
+                           spec=(2.0, 6, None, None), time_eval="nufft"):
+    """reconstruct_equispaced (recon.py:345-355) / reconstruct_interp_fft (recon.py:382-389)."""
+    n_lateral = tuple(int(n) for n in np.atleast_1d(n_lateral))
+    samples = np.asarray(samples, dtype=np.float64)
+    cube = full_grid_cube(positions, samples, dx, n_lateral)
+    lat = tuple(range(cube.ndim - 1))
+    gh = sfft.fftn(np.fft.ifftshift(cube, axes=lat).astype(np.complex128), axes=lat)
+    nt = samples.shape[1]
+    ratios = lateral_ratios(nt, dt, sound_speed, dx, n_lateral)
+    fhat = assemble_fhat(gh, nt, spec, ratios, time_eval=time_eval)
+    return invert_spectrum(fhat, upsample)
 
 
 def out_spacing(dx, dt, sound_speed, nlat, upsample):

@@ -8,11 +8,14 @@ behind the C ABI in ``include/patfft_b200.h``.
 
 from .errors import DataValidationError, DeviceError, NumericalError, ParameterError
 from .recon import (
+    EquispacedPlan,
     NedNerPlan,
     ScalarField,
     SensorRecord,
     amplitude_factor,
     kappa,
+    reconstruct_equispaced,
+    reconstruct_interp_fft,
     reconstruct_nedner,
 )
 from .window import WindowSpec
@@ -24,12 +27,15 @@ __all__ = [
     "DeviceError",
     "NumericalError",
     "ParameterError",
+    "EquispacedPlan",
     "NedNerPlan",
     "ScalarField",
     "SensorRecord",
     "WindowSpec",
     "amplitude_factor",
     "kappa",
+    "reconstruct_equispaced",
+    "reconstruct_interp_fft",
     "reconstruct_nedner",
     "__version__",
 ]

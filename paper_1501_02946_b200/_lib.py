@@ -44,6 +44,8 @@ _P = ctypes.c_void_p
 _D = ctypes.POINTER(ctypes.c_double)
 _SIGS = {
     "patfft_nedner_plan_create": (ctypes.c_int, [ctypes.POINTER(NednerDesc), _D, _D, ctypes.c_int, ctypes.POINTER(_P)]),
+    "patfft_equispaced_plan_create": (ctypes.c_int, [ctypes.POINTER(NednerDesc), ctypes.POINTER(ctypes.c_int64),
+                                                     ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
     "patfft_nedner_output_shape": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
     "patfft_nedner_execute": (ctypes.c_int, [_P, _P, _P, _D]),
     "patfft_nedner_execute_device": (ctypes.c_int, [_P, _P, _P, _P]),

@@ -170,9 +170,13 @@ extern "C" {
 const char* patfft_last_error(void) { return g_err.c_str(); }
 const char* patfft_version(void) { return "patfft-b200 0.2.0 (sm_100a)"; }
 
+// mode 0: NEDNER (scattered sensors, reconstruct_nedner)
+// mode 1: equispaced grid + NER NUFFT (reconstruct_equispaced, recon.py:345-355)
+// mode 2: equispaced grid + linear interpolation (reconstruct_interp_fft, recon.py:382-389)
 static int create_plan(const patfft_nedner_desc* d, const double* gpos, const double* sscale, int device, int rank,
-                       int world, patfft_nedner_plan** out) {
-  if (!d || !gpos || !sscale || !out) return fail(PATFFT_ERR_PARAMETER, "null argument");
+                       int world, int mode, const int64_t* gidx, patfft_nedner_plan** out) {
+  if (!d || !out || (mode == 0 && (!gpos || !sscale)) || (mode != 0 && !gidx))
+    return fail(PATFFT_ERR_PARAMETER, "null argument");
   if (world < 1 || rank < 0 || rank >= world) return fail(PATFFT_ERR_PARAMETER, "invalid rank / world size");
   *out = nullptr;
   if (d->n_lat != 1 && d->n_lat != 2) return fail(PATFFT_ERR_PARAMETER, "NED transforms support 1 or 2 position axes");
@@ -230,6 +234,16 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n) / d->out_dims[a], &P->win_lat[a], &err))
       return fail(PATFFT_ERR_PARAMETER, err);
   }
+  P->mode = mode;
+  if (mode != 0) {  // the full grid itself is the lateral FFT input: no oversampling, no window
+    for (int a = 0; a < d->n_lat; ++a)
+      if (!is_pow2(d->out_dims[a]) || d->out_dims[a] < 4)
+        return fail(PATFFT_ERR_UNSUPPORTED, "GPU equispaced path needs power-of-two lateral grids (>= 4)");
+    if ((int64_t)d->n_sensors != (int64_t)P->N0 * P->N1)
+      return fail(PATFFT_ERR_PARAMETER, "record positions do not form the complete sensor grid");
+    n_over_lat[0] = d->n_lat == 2 ? d->out_dims[0] : 1;
+    n_over_lat[d->n_lat - 1] = d->out_dims[d->n_lat - 1];
+  }
   P->nrows = d->n_lat == 2 ? n_over_lat[0] : 1;
   P->ncols = n_over_lat[d->n_lat - 1];
   const Window& wrow = P->win_lat[0];
@@ -237,11 +251,13 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
 
   // ---- NER window (nufft.py:273-285), power-of-two oversampled length ----
   const int n_ext = 2 * P->T;  // NER always works on the full record length
-  const int64_t n_over_t = next_pow2((int64_t)std::ceil(c * n_ext));
+  // interp mode: plain length-2T FFT of the extension (recon.py:298)
+  const int64_t n_over_t = mode == 2 ? n_ext : next_pow2((int64_t)std::ceil(c * n_ext));
+  if (mode == 2 && !is_pow2(n_ext)) return fail(PATFFT_ERR_UNSUPPORTED, "GPU interp path needs a power-of-two N_t");
   if (n_over_t > 16384)
     return fail(PATFFT_ERR_UNSUPPORTED, "GPU NER supports oversampled depth lengths up to 16384 (N_t <= 4096 at c=2)");
   P->n_over_t = (int)n_over_t;
-  if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_t) / n_ext, &P->win_t, &err))
+  if (mode != 2 && !resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_t) / n_ext, &P->win_t, &err))
     return fail(PATFFT_ERR_PARAMETER, err);
   P->fused_ifft = is_pow2(P->Tu) && P->Tu <= 16384;
 
@@ -250,7 +266,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // reference's (even 11-smooth length) the same (alpha, beta, K) can cover a
   // different part of the window.  Probe the accuracy at the GPU sizes and
   // refuse loudly instead of returning a silently different answer.
-  if (!std::isnan(d->spec_alpha) || !std::isnan(d->spec_beta)) {
+  if (mode == 0 && (!std::isnan(d->spec_alpha) || !std::isnan(d->spec_beta))) {
     struct Probe { const Window* w; int n, n_over, n_over_ref; };
     std::vector<Probe> probes;
     for (int a = 0; a < d->n_lat; ++a)
@@ -285,6 +301,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   P->rows_mine = P->row_starts[rank + 1] - P->row_begin;
   P->Tr = P->T / world;
   if (world > 1) {
+    if (mode != 0) return fail(PATFFT_ERR_UNSUPPORTED, "sharding is implemented for the NEDNER path");
     if (P->up != 1) return fail(PATFFT_ERR_UNSUPPORTED, "sharded reconstruction requires upsample == 1");
     if (P->T % world || !is_pow2(P->Tr) || P->Tr < 2)
       return fail(PATFFT_ERR_UNSUPPORTED, "sharded reconstruction requires N_t / world to be a power of two");
@@ -299,9 +316,10 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   const int RECW = spread_record_words(K2);
   P->R = R;
   P->ngroups = (nrows + R - 1) / R;
+  const int Mrec = mode == 0 ? M : 0;  // the equispaced modes gather instead of spreading
   std::vector<int> ucol(M), urow(M);
   std::vector<double> wcolv((size_t)M * K2), wrowv((size_t)M * K2);
-  for (int m = 0; m < M; ++m) {
+  for (int m = 0; m < Mrec; ++m) {
     const double xc = gpos[(size_t)m * d->n_lat + (d->n_lat - 1)];
     if (!std::isfinite(xc)) return fail(PATFFT_ERR_DATA, "sensor positions must be finite");
     axis_taps(xc, wcol, ncols, &ucol[m], &wcolv[(size_t)m * K2]);
@@ -320,7 +338,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   {
     std::vector<float> wr_acc;
     std::vector<int> grp_seen;
-    for (int m = 0; m < M; ++m) {
+    for (int m = 0; m < Mrec; ++m) {
       const double sc = sscale[m];
       // row weights of this sensor, accumulated per row group (a row can be
       // hit twice when nrows < 2K and the taps wrap)
@@ -411,8 +429,12 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
       dp[jw] = (float)(s0 / (2.0 * M_PI * w.c_eff * kb_psi(w, 2.0 * M_PI * j / N)));
     }
   };
-  if (d->n_lat == 2) deapod(wrow, P->N0, dp0);
-  deapod(wcol, P->N1, dp1);
+  if (mode == 0) {
+    if (d->n_lat == 2) deapod(wrow, P->N0, dp0);
+    deapod(wcol, P->N1, dp1);
+  } else {
+    std::fill(dp1.begin(), dp1.end(), 1.0f);  // plain lateral FFT: no window to undo
+  }
 
   // ---- lateral frequency tables (recon.py:200-215) ------------------------
   std::vector<double> jt0(P->N0, 0.0), jt1(P->N1h);
@@ -436,7 +458,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   }
   NerParams& q = P->ner;
   P->poly_degree = 8;
-  if (fit_ner_poly(wt, 8, &q) > 2e-8) {
+  if (mode != 2 && fit_ner_poly(wt, 8, &q) > 2e-8) {
     P->poly_degree = 12;
     if (fit_ner_poly(wt, 12, &q) > 1e-6)
       return fail(PATFFT_ERR_UNSUPPORTED, "window transform not representable by the tap polynomials");
@@ -445,6 +467,17 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // ---- device buffers -----------------------------------------------------
   int rc;
   if ((rc = upload(&P->d_recs, recbuf))) return rc;
+  if (mode != 0) {
+    std::vector<int> gi(M);
+    std::vector<char> seen((size_t)M, 0);
+    for (int m = 0; m < M; ++m) {
+      if (gidx[m] < 0 || gidx[m] >= M || seen[gidx[m]])
+        return fail(PATFFT_ERR_PARAMETER, "record positions do not form the complete sensor grid");
+      seen[gidx[m]] = 1;
+      gi[m] = (int)gidx[m];
+    }
+    if ((rc = upload(&P->d_gidx, gi))) return rc;
+  }
   if ((rc = upload(&P->d_blk, blk))) return rc;
   if ((rc = upload(&P->d_blkgrp, blk_grp))) return rc;
   if ((rc = upload(&P->d_dp0, dp0))) return rc;
@@ -513,6 +546,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   q.n_lat = P->n_lat;
   q.fused_ifft = P->fused_ifft ? 1 : 0;
   q.c_eff = wt.c_eff;
+  q.interp = mode == 2 ? 1 : 0;
   q.scale = (float)(1.0 / (double(P->N0) * double(P->N1) * double(Tfull)));
   if (world == 1) {
     q.row0 = 0;
@@ -568,12 +602,18 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
 
 int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, const double* sscale, int device,
                               patfft_nedner_plan** out) {
-  return create_plan(d, gpos, sscale, device, 0, 1, out);
+  return create_plan(d, gpos, sscale, device, 0, 1, 0, nullptr, out);
+}
+
+int patfft_equispaced_plan_create(const patfft_nedner_desc* d, const int64_t* grid_index, int time_eval, int device,
+                                  patfft_nedner_plan** out) {
+  if (time_eval != 0 && time_eval != 1) return fail(PATFFT_ERR_PARAMETER, "time_eval must be 0 (nufft) or 1 (interp)");
+  return create_plan(d, nullptr, nullptr, device, 0, 1, time_eval == 0 ? 1 : 2, grid_index, out);
 }
 
 int patfft_nedner_plan_create_sharded(const patfft_nedner_desc* d, const double* gpos, const double* sscale,
                                       int device, int rank, int world, patfft_nedner_plan** out) {
-  return create_plan(d, gpos, sscale, device, rank, world, out);
+  return create_plan(d, gpos, sscale, device, rank, world, 0, nullptr, out);
 }
 
 int patfft_nedner_shard_info(const patfft_nedner_plan* P, int64_t info[8]) {
@@ -662,11 +702,12 @@ static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* 
   sp.nrows = P->nrows;
   LateralParams L = P->lat;
   L.gh = gh;
-  const int nc = overlap ? std::max(1, std::min(P->overlap_chunks, T / 128)) : 1;
+  const int nc = (overlap && P->mode == 0) ? std::max(1, std::min(P->overlap_chunks, T / 128)) : 1;
   if (nc == 1) {
     sp.t_begin = L.t_begin = 0;
     sp.t_end = L.t_end = T;
-    CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
+    if (P->mode == 0) CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
+    else CUDA_TRY(launch_gather_rows(samples, P->d_gidx, P->d_grid, P->M, T, st));
     if (prof) CUDA_TRY(cudaEventRecord(P->ev[1], st));
     CUDA_TRY(launch_lateral_col(L, st));
     if (prof) CUDA_TRY(cudaEventRecord(P->ev[2], st));
@@ -787,7 +828,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
   for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_gh,
-                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_blk, (void*)P->d_blkgrp,
+                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_tw, (void*)P->d_jt0,
                   (void*)P->d_jt1})
     free_dev(p);

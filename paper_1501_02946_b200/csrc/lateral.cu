@@ -15,6 +15,8 @@
 //            per transform -> real image rows.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "fft_smem.cuh"
 #include "patfft_internal.h"
 
@@ -174,10 +176,19 @@ __global__ void __launch_bounds__(512, 2) inv_c2r_kernel(const LateralParams p) 
   }
 }
 
+int tile_bytes() {
+  static int b = [] {
+    const char* e = std::getenv("PATFFT_TILE_KB");
+    const int kb = e ? std::atoi(e) : 64;
+    return (kb >= 8 && kb <= 128 ? kb : 64) * 1024;
+  }();
+  return b;
+}
+
 int plog_for(int len) {
-  // P transforms per tile, tile <= 64 KB of float2
+  // P transforms per tile, tile <= tile_bytes() of float2
   int plog = 4;
-  while (plog > 0 && ((size_t)len << plog) * sizeof(float2) > 65536) --plog;
+  while (plog > 0 && ((size_t)len << plog) * sizeof(float2) > (size_t)tile_bytes()) --plog;
   return plog;
 }
 
@@ -210,7 +221,13 @@ int threads_for(int len, int plog) {
         case 512: run(NAME##_kernel<4, 9>); return err;                                                \
       }                                                                                                \
     }                                                                                                  \
-    if (plog == 3 && len == 1024) { run(NAME##_kernel<3, 10>); return err; }                           \
+    if (plog == 3) {                                                                                   \
+      switch (len) {                                                                                   \
+        case 256: run(NAME##_kernel<3, 8>); return err;                                                \
+        case 512: run(NAME##_kernel<3, 9>); return err;                                                \
+        case 1024: run(NAME##_kernel<3, 10>); return err;                                              \
+      }                                                                                                \
+    }                                                                                                  \
     if (plog == 2 && len == 2048) { run(NAME##_kernel<2, 11>); return err; }                           \
     switch (plog) {                                                                                    \
       case 4: run(NAME##_kernel<4, 0>); break;                                                         \

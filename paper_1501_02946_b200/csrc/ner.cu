@@ -73,12 +73,17 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
   const size_t gstride = (size_t)p.rows_local * tci;
 
   // 1. rotated, windowed even extension -> bit-reversed smem
+  // interp mode (reconstruct_interp_fft, recon.py:297-303): plain length-2T
+  // FFT of the unwindowed, unrotated extension; NUFFT mode: rotated by -T
+  // and pre-windowed (see the header comment).
+  const bool interp = !CT && p.interp;
   auto load_ext = [&](int m) {
-        const int i = (m + T) & (n - 1);  // sequence index stored at slot m
+        const int i = interp ? m : ((m + T) & (n - 1));  // sequence index stored at slot m
         float2 v = make_float2(0.f, 0.f);
         if (i < 2 * T && i != T) {
           const int t = i < T ? i : 2 * T - i;
-          v = fft::cscale(__ldcs(&g[(t >> p.in_tshift) * gstride + (t & p.in_tmask)]), __ldg(&p.iw[i]));
+          const float2 gv = __ldcs(&g[(t >> p.in_tshift) * gstride + (t & p.in_tmask)]);
+          v = interp ? gv : fft::cscale(gv, __ldg(&p.iw[i]));
         }
         return v;
   };
@@ -113,6 +118,17 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
         double kap = sqrt(r2);
         if (ls < 0) kap = -kap;
         const double ke = 2.0 * kap;
+        if (interp) {  // linear interpolation between the two nearest bins
+          const double i0d = floor(ke);
+          const int i0 = (int)i0d;
+          const float fr = (float)(ke - i0d);
+          const float2 Fa = sbuf[gad(i0 & (n - 1), 0)];
+          const float2 Fb = sbuf[gad((i0 + 1) & (n - 1), 0)];
+          const float amp = __fdividef(2.f * (float)lv, (float)kap);
+          const float a = 0.5f * amp * p.scale;
+          vals[it] = make_float2(a * fmaf(fr, Fb.x - Fa.x, Fa.x), a * fmaf(fr, Fb.y - Fa.y, Fa.y));
+          continue;
+        }
         const double xi = __dmul_rn(p.c_eff, ke);
         const double k0d = floor(xi);
         const int k0 = (int)k0d;

@@ -77,6 +77,7 @@ struct NerParams {
   int T, n_over, log_n_over, Tu, log_tu;
   int N0, N1, N1h, N0u, N1uh, up, n_lat;
   int fused_ifft;      // 1: inverse depth FFT in shared memory, 0: write spectrum
+  int interp;          // 1: linear interpolation of the plain 2T FFT (reconstruct_interp_fft)
   // row / time layout (single GPU: row0 = out_row0 = 0, rows_local = N0*N1h,
   // rows_out = N0u*N1uh, in_tchunk = T, out_tchunk = Tu)
   int row0, rows_local, in_tchunk, in_tshift, in_tmask;
@@ -100,6 +101,7 @@ int ner_threads(int n_over);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);
 cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s);
 cudaError_t launch_fill(float* dst, size_t n, float v, cudaStream_t s);
+cudaError_t launch_gather_rows(const float* samples, const int* gidx, float* grid, int M, int T, cudaStream_t s);
 
 }  // namespace patfft
 
@@ -115,6 +117,7 @@ struct patfft_nedner_plan {
   std::mutex mu;
 
   // sizes
+  int mode = 0;  // 0 NEDNER, 1 equispaced NUFFT, 2 equispaced interp
   int n_lat = 2, N0 = 1, N1 = 0, T = 0, up = 1, M = 0;
   int nrows = 1, ncols = 0, N1h = 0;
   int N0u = 1, N1u = 0, N1uh = 0, Tu = 0;
@@ -136,6 +139,7 @@ struct patfft_nedner_plan {
   float* d_out = nullptr;       // [N0u][N1u][Tu] f32 (host path staging)
   double* d_out64 = nullptr;
   float* d_recs = nullptr;
+  int* d_gidx = nullptr;      // equispaced modes: grid row of each sensor
   int4* d_blk = nullptr;
   int* d_blkgrp = nullptr;
   float* d_dp0 = nullptr;

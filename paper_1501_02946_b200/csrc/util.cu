@@ -18,6 +18,16 @@ __global__ void fill_kernel(float* __restrict__ d, size_t n, float v) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     d[i] = v;
 }
+// grid[gidx[m]][t] = samples[m][t] (full-grid cube, recon.py:327-333)
+__global__ void gather_rows_kernel(const float2* __restrict__ s, const int* __restrict__ gidx, float2* __restrict__ g,
+                                   int M, int Th) {
+  const size_t n = (size_t)M * Th;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / Th);
+    const int t = (int)(i - (size_t)m * Th);
+    g[(size_t)__ldg(&gidx[m]) * Th + t] = __ldcs(&s[i]);
+  }
+}
 unsigned grid_for(size_t n) {
   const size_t b = (n + 255) / 256;
   const size_t cap = 148 * 32;
@@ -31,6 +41,12 @@ cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStrea
 }
 cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s) {
   f32_to_f64_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_gather_rows(const float* samples, const int* gidx, float* grid, int M, int T, cudaStream_t s) {
+  const int Th = T / 2;  // T is even: move float2 pairs
+  gather_rows_kernel<<<grid_for((size_t)M * Th), 256, 0, s>>>(reinterpret_cast<const float2*>(samples), gidx,
+                                                              reinterpret_cast<float2*>(grid), M, Th);
   return cudaGetLastError();
 }
 cudaError_t launch_fill(float* dst, size_t n, float v, cudaStream_t s) {

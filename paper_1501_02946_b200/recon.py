@@ -35,7 +35,10 @@ __all__ = [
     "kappa",
     "amplitude_factor",
     "NedNerPlan",
+    "EquispacedPlan",
     "reconstruct_nedner",
+    "reconstruct_equispaced",
+    "reconstruct_interp_fft",
 ]
 
 WEIGHT_SUM_RTOL = 1e-6  # recon.py:48
@@ -311,6 +314,76 @@ class NedNerPlan:
             pass
 
 
+def _grid_index_map(positions, dx, n_lateral):
+    """Flat full-grid index of every sensor row, or None (recon.py:311-324)."""
+    pos = np.atleast_2d(np.asarray(positions, dtype=np.float64)) / dx
+    if pos.shape[1] != len(n_lateral):
+        pos = pos.T
+    idx = np.rint(pos).astype(np.int64)
+    if np.max(np.abs(pos - idx)) > 1e-6:
+        return None
+    for ax, n in enumerate(n_lateral):
+        idx[:, ax] += n // 2
+        if np.any((idx[:, ax] < 0) | (idx[:, ax] >= n)):
+            return None
+    flat = np.ravel_multi_index(tuple(idx.T), n_lateral)
+    total = int(np.prod(n_lateral))
+    if len(np.unique(flat)) != total or flat.size != total:
+        return None
+    return flat
+
+
+class EquispacedPlan(NedNerPlan):
+    """Device plan for a complete sensor grid (recon.py:345-355 / 382-389).
+
+    ``time_eval`` is "nufft" (reconstruct_equispaced) or "interp"
+    (reconstruct_interp_fft).  Raises ParameterError if the positions do not
+    form the complete grid, like the reference.
+    """
+
+    def __init__(self, positions, n_time, dt, sound_speed, dx, n_lateral, time_eval="nufft", upsample=1,
+                 spec: WindowSpec | None = None, device: int = 0):
+        _check_upsample(upsample)
+        if time_eval not in ("nufft", "interp"):
+            raise ParameterError(f"unknown time_eval {time_eval!r}")  # recon.py:304-305
+        lib = _lib.load()
+        n_lateral = tuple(int(n) for n in np.atleast_1d(n_lateral))
+        flat = _grid_index_map(positions, dx, n_lateral)
+        if flat is None:
+            raise ParameterError("record positions do not form the complete sensor grid")  # recon.py:328-330
+        spec = spec if spec is not None else WindowSpec()
+        nlat = len(n_lateral)
+        dy = sound_speed * dt
+        desc = _lib.NednerDesc()
+        desc.n_lat = nlat
+        desc.out_dims[0] = n_lateral[0]
+        desc.out_dims[1] = n_lateral[-1] if nlat == 2 else 0
+        desc.n_time = int(n_time)
+        desc.upsample = int(upsample)
+        desc.n_sensors = flat.size
+        ratios = [n_time * dy / (n * dx) for n in n_lateral]
+        desc.lat_ratio[0] = ratios[0]
+        desc.lat_ratio[1] = ratios[-1]
+        desc.spec_c = float(spec.c)
+        desc.spec_K = int(spec.K)
+        desc.spec_alpha = math.nan if spec.alpha is None else float(spec.alpha)
+        desc.spec_beta = math.nan if spec.beta is None else float(spec.beta)
+        gidx = np.ascontiguousarray(flat, dtype=np.int64)
+        handle = ctypes.c_void_p()
+        _lib.check(lib.patfft_equispaced_plan_create(ctypes.byref(desc), gidx.ctypes.data_as(
+            ctypes.POINTER(ctypes.c_int64)), 0 if time_eval == "nufft" else 1, int(device), ctypes.byref(handle)))
+        self._lib = lib
+        self._h = handle
+        shape = (ctypes.c_int64 * 3)()
+        rank = lib.patfft_nedner_output_shape(handle, shape)
+        self.out_shape = tuple(int(shape[i]) for i in range(rank))
+        self.n_sensors = flat.size
+        self.n_time = int(n_time)
+        self.spacing = tuple(s / upsample for s in ((dx,) * nlat + (dy,)))
+        self.device = int(device)
+        self._lock = threading.Lock()
+
+
 # small LRU of plans keyed on the sensor layout, so repeated drop-in calls
 # on one geometry (the batched-frames use case) reuse the device plan
 _CACHE: "OrderedDict[tuple, NedNerPlan]" = OrderedDict()
@@ -318,19 +391,23 @@ _CACHE_LOCK = threading.Lock()
 _CACHE_SIZE = 4
 
 
-def _plan_for(rec, dims, upsample, spec, device) -> NedNerPlan:
+def _plan_for(rec, dims, upsample, spec, device, kind="nedner") -> NedNerPlan:
     pos = np.ascontiguousarray(np.atleast_2d(np.asarray(rec.positions, dtype=np.float64)))
     w = np.ascontiguousarray(np.asarray(rec.weights, dtype=np.float64).ravel())
-    key = (pos.shape, hash(pos.tobytes()), hash(w.tobytes()), int(rec.samples.shape[1]), float(rec.dt),
-           float(rec.sound_speed), float(rec.dx), tuple(rec.n_lateral), dims, int(upsample),
-           (spec.c, spec.K, spec.alpha, spec.beta), int(device))
+    key = (kind, pos.shape, hash(pos.tobytes()), hash(w.tobytes()) if kind == "nedner" else 0,
+           int(rec.samples.shape[1]), float(rec.dt), float(rec.sound_speed), float(rec.dx), tuple(rec.n_lateral),
+           dims, int(upsample), (spec.c, spec.K, spec.alpha, spec.beta), int(device))
     with _CACHE_LOCK:
         plan = _CACHE.get(key)
         if plan is not None:
             _CACHE.move_to_end(key)
             return plan
-    plan = NedNerPlan(pos, w, rec.samples.shape[1], rec.dt, rec.sound_speed, rec.dx, rec.n_lateral,
-                      out_dims=dims, upsample=upsample, spec=spec, device=device)
+    if kind == "nedner":
+        plan = NedNerPlan(pos, w, rec.samples.shape[1], rec.dt, rec.sound_speed, rec.dx, rec.n_lateral,
+                          out_dims=dims, upsample=upsample, spec=spec, device=device)
+    else:
+        plan = EquispacedPlan(pos, rec.samples.shape[1], rec.dt, rec.sound_speed, rec.dx, rec.n_lateral,
+                              time_eval=kind, upsample=upsample, spec=spec, device=device)
     with _CACHE_LOCK:
         _CACHE[key] = plan
         while len(_CACHE) > _CACHE_SIZE:
@@ -350,5 +427,34 @@ def reconstruct_nedner(rec, out_dims=None, upsample: int = 1, spec: WindowSpec |
     elif not isinstance(spec, WindowSpec):  # e.g. the reference's own WindowSpec
         spec = WindowSpec(c=spec.c, K=spec.K, alpha=spec.alpha, beta=spec.beta)
     plan = _plan_for(rec, dims, int(upsample), spec, device)
+    img, resid = plan.execute(np.asarray(rec.samples, dtype=np.float64))
+    return ScalarField(img, plan.spacing, meta={"imag_residual": float(resid)})
+
+
+def _as_spec(spec):
+    if spec is None:
+        return WindowSpec()
+    if not isinstance(spec, WindowSpec):  # e.g. the reference's own WindowSpec
+        return WindowSpec(c=spec.c, K=spec.K, alpha=spec.alpha, beta=spec.beta)
+    return spec
+
+
+def reconstruct_equispaced(rec, upsample: int = 1, spec: WindowSpec | None = None, *, device: int = 0) -> ScalarField:
+    """Reconstruct from a complete sensor grid (recon.py:345-355) on the GPU.
+
+    Raises ParameterError if the record does not cover the full grid.
+    """
+    _check_upsample(upsample)
+    n_lateral = tuple(int(n) for n in np.atleast_1d(rec.n_lateral))
+    plan = _plan_for(rec, n_lateral, int(upsample), _as_spec(spec), device, kind="nufft")
+    img, resid = plan.execute(np.asarray(rec.samples, dtype=np.float64))
+    return ScalarField(img, plan.spacing, meta={"imag_residual": float(resid)})
+
+
+def reconstruct_interp_fft(rec, upsample: int = 1, *, device: int = 0) -> ScalarField:
+    """Baseline: linear interpolation of the time-axis FFT (recon.py:382-389) on the GPU."""
+    _check_upsample(upsample)
+    n_lateral = tuple(int(n) for n in np.atleast_1d(rec.n_lateral))
+    plan = _plan_for(rec, n_lateral, int(upsample), WindowSpec(), device, kind="interp")
     img, resid = plan.execute(np.asarray(rec.samples, dtype=np.float64))
     return ScalarField(img, plan.spacing, meta={"imag_residual": float(resid)})

@@ -103,6 +103,33 @@ def main():
     recon_case("recon_3d_edges16", synth.SyntheticRecord(edge, w, samples, 20e-9, synth.SOUND_SPEED, synth.PITCH,
                                                          (n, n)))
 
+    # 12. complete grids: reconstruct_equispaced and reconstruct_interp_fft
+    def grid_case(name, n_lateral, nt, seed, upsample=1, shuffle=True):
+        rng = np.random.default_rng(seed)
+        axes = [(np.arange(n) - n // 2) * synth.PITCH for n in n_lateral]
+        mesh = np.meshgrid(*axes, indexing="ij")
+        pos = np.stack([m.ravel() for m in mesh], axis=-1)
+        if shuffle:
+            pos = pos[rng.permutation(pos.shape[0])]
+        if len(n_lateral) == 2:
+            balls = [(0.3e-3, -0.2e-3, 1.6e-3, 0.5e-3, 1.0), (-0.4e-3, 0.3e-3, 1.0e-3, 0.3e-3, 0.7)]
+            samples = synth.ball_traces(pos, nt, 20e-9, synth.SOUND_SPEED, balls)
+        else:
+            t = np.arange(nt) * 20e-9
+            dist = np.hypot(pos[:, 0] - 0.4e-3, 1.5e-3)
+            samples = np.exp(-((t[None, :] - dist[:, None] / synth.SOUND_SPEED) ** 2) / (2 * (40e-9) ** 2))
+        w = np.full(pos.shape[0], float(np.prod([n * synth.PITCH for n in n_lateral])) / pos.shape[0])
+        r = _record(pos, w, samples, 20e-9, synth.SOUND_SPEED, synth.PITCH, n_lateral)
+        eq = rrecon.reconstruct_equispaced(r, upsample=upsample)
+        ip = rrecon.reconstruct_interp_fft(r, upsample=upsample)
+        _save(name, positions=pos, weights=w, samples=samples, dt=20e-9, sound_speed=synth.SOUND_SPEED,
+              dx=synth.PITCH, n_lateral=np.asarray(n_lateral), upsample=upsample,
+              values_equispaced=eq.values, values_interp=ip.values, spacing=np.asarray(eq.spacing))
+
+    grid_case("grid_3d_16x16x64", (16, 16), 64, 23)
+    grid_case("grid_3d_8x16x32_up2", (8, 16), 32, 24, upsample=2)
+    grid_case("grid_2d_64x128", (64,), 128, 25)
+
     # component goldens: NER (per-row targets) and NED (1 and 2 axes)
     rng = np.random.default_rng(21)
     n = 64

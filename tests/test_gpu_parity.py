@@ -149,3 +149,26 @@ def test_gpu_full_size_cfg4_properties():
     assert np.array_equal(f1, f1b)
     assert np.all(np.isfinite(f1))
     assert rel_l2(f3, 0.5 * f1 - 2.0 * f2) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["grid_3d_16x16x64", "grid_3d_8x16x32_up2", "grid_2d_64x128"])
+def test_gpu_equispaced_and_interp_match_reference(name):
+    from conftest import GOLDEN
+
+    g = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    rec = pb.SensorRecord(g["positions"], g["weights"], g["samples"], float(g["dt"]), float(g["sound_speed"]),
+                          float(g["dx"]), tuple(int(n) for n in g["n_lateral"]))
+    up = int(g["upsample"])
+    eq = pb.reconstruct_equispaced(rec, upsample=up)
+    ip = pb.reconstruct_interp_fft(rec, upsample=up)
+    e1, e2 = rel_l2(eq.values, g["values_equispaced"]), rel_l2(ip.values, g["values_interp"])
+    print(f"{name}: equispaced rel-L2 {e1:.3e}, interp rel-L2 {e2:.3e}")
+    assert eq.values.shape == g["values_equispaced"].shape
+    np.testing.assert_allclose(eq.spacing, g["spacing"], rtol=1e-15)
+    assert e1 <= TOL and e2 <= TOL
+
+
+def test_gpu_equispaced_rejects_incomplete_grid():
+    s = synth.make_3d(9, 16, 32, 20e-9, "jittered", 1)
+    with pytest.raises(pb.ParameterError, match="complete sensor grid"):
+        pb.reconstruct_equispaced(s.as_record())

@@ -63,3 +63,24 @@ def test_oracle_zero_data_gives_zero_image():
     img, _ = O.reconstruct_nedner(g["positions"], g["weights"], np.zeros_like(g["samples"]), float(g["dt"]),
                                   float(g["sound_speed"]), float(g["dx"]), tuple(g["n_lateral"]))
     assert not np.any(img)
+
+
+@pytest.mark.parametrize("name", ["grid_3d_16x16x64", "grid_3d_8x16x32_up2", "grid_2d_64x128"])
+def test_oracle_equispaced_and_interp_match_reference(name):
+    g = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    args = (g["positions"], g["samples"], float(g["dt"]), float(g["sound_speed"]), float(g["dx"]),
+            tuple(int(n) for n in g["n_lateral"]))
+    eq, _ = O.reconstruct_equispaced(*args, upsample=int(g["upsample"]))
+    ip, _ = O.reconstruct_equispaced(*args, upsample=int(g["upsample"]), time_eval="interp")
+    assert rel_l2(eq, g["values_equispaced"]) <= 1e-12
+    assert rel_l2(ip, g["values_interp"]) <= 1e-12
+
+
+def test_oracle_full_grid_nedner_equals_equispaced():
+    # on a complete grid with h_m = dx^(d-1) NEDNER reduces to the equispaced path
+    g = np.load(os.path.join(GOLDEN, "grid_3d_16x16x64.npz"))
+    nl = tuple(int(n) for n in g["n_lateral"])
+    w = np.full(g["positions"].shape[0], float(g["dx"]) ** 2)
+    ned, _ = O.reconstruct_nedner(g["positions"], w, g["samples"], float(g["dt"]), float(g["sound_speed"]),
+                                  float(g["dx"]), nl)
+    assert rel_l2(ned, g["values_equispaced"]) <= 1e-8
