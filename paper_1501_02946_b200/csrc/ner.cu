@@ -80,7 +80,9 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
   auto load_ext = [&](int m) {
         const int i = interp ? m : ((m + T) & (n - 1));  // sequence index stored at slot m
         float2 v = make_float2(0.f, 0.f);
-        if (i < 2 * T && i != T) {
+        // CT: ext[0] = g0 is left out, so the windowed sequence is exactly even
+        // around slot 0 and its transform D(kappa) is even; g0 is added exactly below
+        if (i < 2 * T && i != T && !(CT && i == 0)) {
           const int t = i < T ? i : 2 * T - i;
           const float2 gv = __ldcs(&g[(t >> p.in_tshift) * gstride + (t & p.in_tmask)]);
           v = interp ? gv : fft::cscale(gv, __ldg(&p.iw[i]));
@@ -105,7 +107,68 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
   const double j2 = p.jt0[j0w] + p.jt1[j1];  // recon.py:210-214 summation order
   const double halfT = (double)T / 2.0;
   const double band_r2 = halfT * halfT;
+  // interpolated D(kappa_e) (2K taps, polynomial weights) for kappa_e >= 0
+  auto interp_D = [&](double ke) {
+    const double xi = __dmul_rn(p.c_eff, ke);
+    const double k0d = floor(xi);
+    const int k0 = (int)k0d;
+    const float z = (float)(xi - k0d) - 0.5f;
+    const float z2 = z * z;
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      // tap j (dk = j-K+1) and its mirror K2-1-j share one polynomial:
+      // w_j = E(z^2) + z O(z^2), w_mirror = E(z^2) - z O(z^2)
+      float e = p.poly[j][D], o = p.poly[j][D - 1];
+      if (D % 2) {
+        e = p.poly[j][D - 1];
+        o = p.poly[j][D];
+      }
+#pragma unroll
+      for (int d = (D % 2 ? D - 3 : D - 2); d >= 0; d -= 2) e = fmaf(e, z2, p.poly[j][d]);
+#pragma unroll
+      for (int d = (D % 2 ? D - 2 : D - 3); d >= 1; d -= 2) o = fmaf(o, z2, p.poly[j][d]);
+      const float wa = fmaf(z, o, e);
+      const float wb = fmaf(-z, o, e);
+      const float2 Fa = sbuf[gad((k0 + j - K + 1) & (n - 1), 0)];
+      const float2 Fb = sbuf[gad((k0 + K - j) & (n - 1), 0)];
+      acc.x = fmaf(wa, Fa.x, fmaf(wb, Fb.x, acc.x));
+      acc.y = fmaf(wa, Fa.y, fmaf(wb, Fb.y, acc.y));
+    }
+    return acc;
+  };
+
+  constexpr int kPairs = 4;  // CT: |l| in [0, T/2], at most 4 per thread
   float2 vals[kMaxTargetsPerThread];
+  float2 valsP[kPairs], valsM[kPairs];
+  if constexpr (CT) {
+    // NER(+-l) = exp(-+ i pi kappa_e) D(kappa_e) + g0 with kappa_e = 2 kappa(j, |l|) >= 0:
+    // one interpolation serves both signs of l (recon.py:282-308 targets)
+    const float2 g0 = __ldg(&g[0]);
+#pragma unroll
+    for (int it = 0; it < kPairs; ++it) {
+      const int lh = tid + it * nth;
+      float2 vp = make_float2(0.f, 0.f), vm = make_float2(0.f, 0.f);
+      if (lh <= T / 2 && lh > 0) {
+        const double lv = __dmul_rn(__dmul_rn((double)lh, 1.0 / (double)T), (double)T);  // fftfreq(T)*T
+        const double r2 = __dadd_rn(j2, __dmul_rn(lv, lv));
+        if (r2 <= band_r2) {
+          const double kap = sqrt(r2);
+          const double ke = 2.0 * kap;
+          const float2 Dv = interp_D(ke);
+          const double red = ke - 2.0 * floor(0.5 * ke + 0.5);
+          const float2 cs = cospi_sinpi((float)red);  // (cos, sin)(pi kappa_e)
+          const float amp = __fdividef(2.f * (float)lv, (float)kap);
+          const float a = 0.5f * amp * p.scale;
+          const float rx = Dv.x * cs.x, ry = Dv.y * cs.x, sx = Dv.x * cs.y, sy = Dv.y * cs.y;
+          vp = make_float2(a * (rx + sy + g0.x), a * (ry - sx + g0.y));  // e^{-i pi ke} D + g0
+          vm = make_float2(a * (rx - sy + g0.x), a * (ry + sx + g0.y));  // e^{+i pi ke} D + g0
+        }
+      }
+      valsP[it] = vp;
+      valsM[it] = vm;
+    }
+  } else {
 #pragma unroll
   for (int it = 0; it < kMaxTargetsPerThread; ++it) {
     const int l = tid + it * nth;
@@ -129,32 +192,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
           vals[it] = make_float2(a * fmaf(fr, Fb.x - Fa.x, Fa.x), a * fmaf(fr, Fb.y - Fa.y, Fa.y));
           continue;
         }
-        const double xi = __dmul_rn(p.c_eff, ke);
-        const double k0d = floor(xi);
-        const int k0 = (int)k0d;
-        const float z = (float)(xi - k0d) - 0.5f;
-        const float z2 = z * z;
-        float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          // tap j (dk = j-K+1) and its mirror K2-1-j share one polynomial:
-          // w_j = E(z^2) + z O(z^2), w_mirror = E(z^2) - z O(z^2)
-          float e = p.poly[j][D], o = p.poly[j][D - 1];
-          if (D % 2) {
-            e = p.poly[j][D - 1];
-            o = p.poly[j][D];
-          }
-#pragma unroll
-          for (int d = (D % 2 ? D - 3 : D - 2); d >= 0; d -= 2) e = fmaf(e, z2, p.poly[j][d]);
-#pragma unroll
-          for (int d = (D % 2 ? D - 2 : D - 3); d >= 1; d -= 2) o = fmaf(o, z2, p.poly[j][d]);
-          const float wa = fmaf(z, o, e);
-          const float wb = fmaf(-z, o, e);
-          const float2 Fa = sbuf[gad((k0 + j - K + 1) & (n - 1), 0)];
-          const float2 Fb = sbuf[gad((k0 + K - j) & (n - 1), 0)];
-          acc.x = fmaf(wa, Fa.x, fmaf(wb, Fb.x, acc.x));
-          acc.y = fmaf(wa, Fa.y, fmaf(wb, Fb.y, acc.y));
-        }
+        const float2 acc = interp_D(ke);
         // exp(-i pi kappa_e), kappa_e reduced mod 2 in float64
         const double red = ke - 2.0 * floor(0.5 * ke + 0.5);
         const float2 cs = cospi_sinpi((float)red);
@@ -164,6 +202,7 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
       }
     }
     vals[it] = out;
+  }
   }
 
   // destination rows in the (possibly upsampled) half spectrum z
@@ -199,19 +238,29 @@ __global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
       for (int i = tid; i < Tu; i += nth) sbuf[iad(i, 0)] = make_float2(0.f, 0.f);
       __syncthreads();
     }
+    if constexpr (CT) {  // up == 1: +l at index l, -l at index T - l
+#pragma unroll
+      for (int it = 0; it < kPairs; ++it) {
+        const int lh = tid + it * nth;
+        if (lh > T / 2) break;
+        if (lh < T / 2) sbuf[iad(fft::brev(lh, Lu), 0)] = fft::cscale(valsP[it], dfac);
+        if (lh > 0) sbuf[iad(fft::brev(T - lh, Lu), 0)] = fft::cscale(valsM[it], dfac);
+      }
+    } else {
 #pragma unroll
     for (int it = 0; it < kMaxTargetsPerThread; ++it) {
       const int l = tid + it * nth;
       if (l >= T) break;
       const int ls = (l < T / 2) ? l : l - T;
       const float2 v = fft::cscale(vals[it], dfac);
-      if (!CT && ls == -(T / 2) && p.up > 1) {
+      if (ls == -(T / 2) && p.up > 1) {
         const float2 hv = fft::cscale(v, 0.5f);
         sbuf[iad(fft::brev(T / 2, Lu), 0)] = hv;
         sbuf[iad(fft::brev(Tu - T / 2, Lu), 0)] = hv;
       } else {
         sbuf[iad(fft::brev(ls >= 0 ? ls : Tu + ls, Lu), 0)] = v;
       }
+    }
     }
     __syncthreads();
     if constexpr (CT) fft::fft_ct<true, LOGT, (CT_NTH * 4 >= CT_T ? 2 : 4), true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT>());
