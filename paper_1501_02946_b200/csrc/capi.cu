@@ -495,6 +495,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
 
   CUDA_TRY(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
   if (const char* e = std::getenv("PATFFT_OVERLAP_CHUNKS")) P->overlap_chunks = std::max(1, std::min(4, std::atoi(e)));
+  if (const char* e = std::getenv("PATFFT_GRAPHS")) P->use_graphs = std::atoi(e) != 0;
   {
     int lo = 0, hi = 0;
     CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -778,12 +779,61 @@ static int execute_device_locked(patfft_nedner_plan* P, const float* samples, fl
 
 extern "C" {
 
+}  // extern "C"
+
+// Replay of a captured CUDA graph when the same (samples, image, frames)
+// buffers are executed again: the whole 6-7 kernel pipeline becomes one
+// graph launch (launch gaps dominate small reconstructions).  Profiling runs
+// and first calls go through the stream directly.
+static int execute_graphed(patfft_nedner_plan* P, int n_frames, const float* samples, float* image,
+                           cudaStream_t st) {
+  const size_t in_sz = (size_t)P->M * P->T, out_sz = (size_t)P->N0u * P->N1u * P->Tu;
+  auto enqueue = [&]() -> int {
+    for (int f = 0; f < n_frames; ++f) {
+      int rc = execute_device_locked(P, samples + f * in_sz, image + f * out_sz, st);
+      if (rc) return rc;
+    }
+    return PATFFT_OK;
+  };
+  if (P->profiling || !P->use_graphs) return enqueue();
+  if (P->graph_exec && P->g_in == samples && P->g_out == image && P->g_frames == n_frames) {
+    CUDA_TRY(cudaGraphLaunch(P->graph_exec, st));
+    return PATFFT_OK;
+  }
+  if (P->graph_exec) {
+    cudaGraphExecDestroy(P->graph_exec);
+    P->graph_exec = nullptr;
+  }
+  cudaGraph_t graph = nullptr;
+  CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const int rc = enqueue();
+  const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (ce != cudaSuccess) return fail(PATFFT_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+  const cudaError_t ie = cudaGraphInstantiate(&P->graph_exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    P->graph_exec = nullptr;
+    return fail(PATFFT_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+  }
+  P->g_in = samples;
+  P->g_out = image;
+  P->g_frames = n_frames;
+  CUDA_TRY(cudaGraphLaunch(P->graph_exec, st));
+  return PATFFT_OK;
+}
+
+extern "C" {
+
 int patfft_nedner_execute_device(patfft_nedner_plan* P, const float* samples, float* image, void* stream) {
   if (!P || !samples || !image) return fail(PATFFT_ERR_PARAMETER, "null argument");
   std::lock_guard<std::mutex> lk(P->mu);
   CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
-  return execute_device_locked(P, samples, image, st);
+  return execute_graphed(P, 1, samples, image, st);
 }
 
 int patfft_nedner_execute_frames_device(patfft_nedner_plan* P, int n_frames, const float* samples, float* images,
@@ -792,12 +842,7 @@ int patfft_nedner_execute_frames_device(patfft_nedner_plan* P, int n_frames, con
   std::lock_guard<std::mutex> lk(P->mu);
   CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
-  const size_t in_sz = (size_t)P->M * P->T, out_sz = (size_t)P->N0u * P->N1u * P->Tu;
-  for (int f = 0; f < n_frames; ++f) {
-    int rc = execute_device_locked(P, samples + f * in_sz, images + f * out_sz, st);
-    if (rc) return rc;
-  }
-  return PATFFT_OK;
+  return execute_graphed(P, n_frames, samples, images, st);
 }
 
 int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* image, double* imag_residual) {
@@ -813,7 +858,7 @@ int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* 
   cudaStream_t st = P->stream;
   CUDA_TRY(cudaMemcpyAsync(P->d_samples64, samples, in_n * sizeof(double), cudaMemcpyHostToDevice, st));
   CUDA_TRY(launch_f64_to_f32(P->d_samples64, P->d_samples, in_n, st));
-  if ((rc = execute_device_locked(P, P->d_samples, P->d_out, st))) return rc;
+  if ((rc = execute_graphed(P, 1, P->d_samples, P->d_out, st))) return rc;
   CUDA_TRY(launch_f32_to_f64(P->d_out, P->d_out64, out_n, st));
   CUDA_TRY(cudaMemcpyAsync(image, P->d_out64, out_n * sizeof(double), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -825,6 +870,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
   if (P->stream) cudaStreamSynchronize(P->stream);
+  if (P->graph_exec) cudaGraphExecDestroy(P->graph_exec);
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
   for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_gh,

@@ -114,6 +114,12 @@ struct patfft_nedner_plan {
   cudaStream_t stream2 = nullptr;  // lateral FFTs overlapped with the spread
   cudaEvent_t ev_chunk[4] = {}, ev_fork = nullptr, ev_join = nullptr;
   int overlap_chunks = 1;  // time chunks of the overlapped forward stages (1 = off)
+  // CUDA graph of the last executed (samples, image, frames) triple
+  bool use_graphs = true;
+  cudaGraphExec_t graph_exec = nullptr;
+  const float* g_in = nullptr;
+  float* g_out = nullptr;
+  int g_frames = 0;
   std::mutex mu;
 
   // sizes
