@@ -109,6 +109,23 @@ int patfft_nedner_execute_frames_device(patfft_nedner_plan* plan, int n_frames,
 
 void patfft_nedner_plan_destroy(patfft_nedner_plan* plan);
 
+/* ---- standalone NER NUFFT (the reference's NerPlan / nufft_ner, nufft.py:270-338) ----
+ * out[r, i] ~= sum_k u[r, k] exp(-2 pi i kappa[r, i] k / n); kappas are per row
+ * (rows x m) or shared (m) when `shared` != 0.  u/out complex (interleaved).
+ * The host call takes complex128 u/out and float64 kappas; the device call
+ * complex64 u/out (float2) and float64 kappas.  Range checks (finite, |kappa| <=
+ * kappa_max) are the caller's (nufft.py:305-308, done in the Python shim).   */
+typedef struct patfft_ner_plan patfft_ner_plan;
+int patfft_ner_plan_create(int n, double c, int K, double alpha_or_nan, double beta_or_nan, int device,
+                           patfft_ner_plan** out);
+/* info: n, n_over, 2K, tap polynomial degree */
+int patfft_ner_plan_info(const patfft_ner_plan* plan, int64_t info[4]);
+int patfft_ner_execute(patfft_ner_plan* plan, const double* u, const double* kappas, int rows, int m, int shared,
+                       double* out);
+int patfft_ner_execute_device(patfft_ner_plan* plan, const void* u, const double* kappas, int rows, int m,
+                              int shared, void* out, void* stream);
+void patfft_ner_plan_destroy(patfft_ner_plan* plan);
+
 /* ---- multi-GPU (one process per GPU; the caller runs the two exchanges) ----
  * A sharded plan splits one reconstruction over `world` ranks:
  *   forward  : NED spread + lateral FFT of the rank's time slice

@@ -18,6 +18,7 @@ from .recon import (
     reconstruct_interp_fft,
     reconstruct_nedner,
 )
+from .nufft import NerPlan, nufft_ner
 from .window import WindowSpec
 
 __version__ = "0.1.0"
@@ -29,10 +30,12 @@ __all__ = [
     "ParameterError",
     "EquispacedPlan",
     "NedNerPlan",
+    "NerPlan",
     "ScalarField",
     "SensorRecord",
     "WindowSpec",
     "amplitude_factor",
+    "nufft_ner",
     "kappa",
     "reconstruct_equispaced",
     "reconstruct_interp_fft",

@@ -58,6 +58,12 @@ _SIGS = {
     "patfft_nedner_shard_forward": (ctypes.c_int, [_P, _P, _P, _P]),
     "patfft_nedner_shard_ner": (ctypes.c_int, [_P, _P, _P, _P]),
     "patfft_nedner_shard_inverse": (ctypes.c_int, [_P, _P, _P, _P]),
+    "patfft_ner_plan_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                              ctypes.c_double, ctypes.c_int, ctypes.POINTER(_P)]),
+    "patfft_ner_plan_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
+    "patfft_ner_execute": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
+    "patfft_ner_execute_device": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P]),
+    "patfft_ner_plan_destroy": (None, [_P]),
     "patfft_nedner_set_profiling": (ctypes.c_int, [_P, ctypes.c_int]),
     "patfft_nedner_stage_times": (ctypes.c_int, [_P, _D, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
     "patfft_nedner_stage_name": (ctypes.c_char_p, [ctypes.c_int]),

@@ -33,6 +33,14 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+}  // namespace
+
+namespace patfft {
+int set_last_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace patfft
+
+namespace {
+
 #define CUDA_TRY(expr)                                                                   \
   do {                                                                                   \
     cudaError_t _e = (expr);                                                             \
@@ -133,7 +141,11 @@ std::vector<double> cheb_fit(F f, int D) {
 
 // NER tap polynomials: P_j(z) = psihat((z + K - 1/2 - j)/c)/psihat(0), z = f - 1/2.
 // Returns the max abs error on a fine grid.
-double fit_ner_poly(const Window& w, int D, NerParams* q) {
+double fit_ner_poly_into(const Window& w, int D, float (*poly)[kMaxPolyDegree + 1]) {
+  struct {
+    float (*poly)[kMaxPolyDegree + 1];
+  } qq{poly};
+  auto* q = &qq;
   const double norm = 1.0 / kb_psihat(w, 0.0);
   double worst = 0.0;
   for (int j = 0; j < kMaxTaps / 2; ++j)
@@ -156,6 +168,8 @@ double fit_ner_poly(const Window& w, int D, NerParams* q) {
   return worst;
 }
 
+double fit_ner_poly(const Window& w, int D, NerParams* q) { return fit_ner_poly_into(w, D, q->poly); }
+
 void free_dev(void* p) {
   if (p) cudaFree(p);
 }
@@ -164,6 +178,12 @@ void free_dev(void* p) {
 
 static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* gh, cudaStream_t st, bool overlap,
                            bool prof);
+
+namespace patfft {
+double fit_ner_poly_public(const Window& w, int D, float (*poly)[kMaxPolyDegree + 1]) {
+  return fit_ner_poly_into(w, D, poly);
+}
+}  // namespace patfft
 
 extern "C" {
 

@@ -1,0 +1,309 @@
+// Standalone non-equispaced-range NUFFT (the reference's NerPlan,
+// nufft.py:270-338): out[r, i] ~= sum_k u[r, k] exp(-2 pi i kappa[r, i] k / n).
+// One CTA per row: pre-window + rotation by -n/2 into shared memory (so the
+// FFT output already carries exp(i pi bin / c) and only one phase
+// exp(-i pi kappa) per target remains), radix-16 FFT of length n_over, and a
+// 2K-tap Kaiser-Bessel interpolation per target with polynomial tap weights.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fft_smem.cuh"
+#include "patfft_internal.h"
+
+namespace patfft {
+namespace {
+
+struct NerApiParams {
+  const float2* u;       // [rows][n]
+  const double* kap;     // [rows][m] or [m] (shared)
+  float2* out;           // [rows][m]
+  const float* iw;       // [n] psihat(0) * norm / psi(2 pi k/n - pi)
+  const float2* tw;      // exp(-2 pi i k / 2^14)
+  int n, n_over, L, rows, m, shared;
+  double c_eff;
+  float poly[kMaxTaps / 2][kMaxPolyDegree + 1];
+};
+
+__device__ __forceinline__ float2 cospi_sinpi_api(float r) {
+  const float q = rintf(2.f * r);
+  const float x = 3.14159265358979f * fmaf(-0.5f, q, r);
+  const float x2 = x * x;
+  const float s = x * fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, 2.7557319e-6f, -1.98412698e-4f), 8.33333333e-3f),
+                                    -0.166666667f), 1.f);
+  const float c = fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, -2.7557319e-7f, 2.48015873e-5f), -1.38888889e-3f),
+                                          4.16666667e-2f), -0.5f), 1.f);
+  switch (((int)q) & 3) {
+    case 0: return make_float2(c, s);
+    case 1: return make_float2(-s, c);
+    case 2: return make_float2(-c, -s);
+    default: return make_float2(s, -c);
+  }
+}
+
+template <int K2, int D>
+__global__ void __launch_bounds__(512) nerplan_kernel(const NerApiParams p) {
+  extern __shared__ float2 sbuf[];
+  constexpr int K = K2 / 2;
+  const int row = blockIdx.x;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int n = p.n, no = p.n_over, L = p.L;
+  const fft::SwzAddr ad = fft::SwzAddr::for_log(L);
+  const float2* __restrict__ u = p.u + (size_t)row * n;
+  fft::staged_copy<8, float2>(
+      no, tid, nth,
+      [&](int s) {
+        const int i = (s + n / 2) & (no - 1);  // sequence index stored at slot s
+        return i < n ? fft::cscale(__ldcs(&u[i]), __ldg(&p.iw[i])) : make_float2(0.f, 0.f);
+      },
+      [&](int s, float2 v) { sbuf[ad(fft::brev(s, L), 0)] = v; });
+  __syncthreads();
+  fft::fft_inplace<false, 4, true>(sbuf, L, 0, p.tw, tid, nth, ad);
+  const double* __restrict__ kap = p.shared ? p.kap : p.kap + (size_t)row * p.m;
+  float2* __restrict__ out = p.out + (size_t)row * p.m;
+  for (int i = tid; i < p.m; i += nth) {
+    const double kv = __ldg(&kap[i]);
+    const double xi = __dmul_rn(p.c_eff, kv);
+    const double k0d = floor(xi);
+    const int k0 = (int)k0d;
+    const float z = (float)(xi - k0d) - 0.5f;
+    const float z2 = z * z;
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      float e = p.poly[j][D], o = p.poly[j][D - 1];
+#pragma unroll
+      for (int d = D - 2; d >= 0; d -= 2) e = fmaf(e, z2, p.poly[j][d]);
+#pragma unroll
+      for (int d = D - 3; d >= 1; d -= 2) o = fmaf(o, z2, p.poly[j][d]);
+      const float wa = fmaf(z, o, e);
+      const float wb = fmaf(-z, o, e);
+      const float2 Fa = sbuf[ad((k0 + j - K + 1) & (no - 1), 0)];
+      const float2 Fb = sbuf[ad((k0 + K - j) & (no - 1), 0)];
+      acc.x = fmaf(wa, Fa.x, fmaf(wb, Fb.x, acc.x));
+      acc.y = fmaf(wa, Fa.y, fmaf(wb, Fb.y, acc.y));
+    }
+    const double red = kv - 2.0 * floor(0.5 * kv + 0.5);  // exp(-i pi kappa)
+    const float2 cs = cospi_sinpi_api((float)red);
+    out[i] = make_float2(acc.x * cs.x + acc.y * cs.y, acc.y * cs.x - acc.x * cs.y);
+  }
+}
+
+__global__ void c128_to_c64(const double2* __restrict__ s, float2* __restrict__ d, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    d[i] = make_float2((float)s[i].x, (float)s[i].y);
+}
+__global__ void c64_to_c128(const float2* __restrict__ s, double2* __restrict__ d, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    d[i] = make_double2(s[i].x, s[i].y);
+}
+
+}  // namespace
+int set_last_error(int code, const std::string& msg);  // capi.cu
+}  // namespace patfft
+
+using namespace patfft;
+
+struct patfft_ner_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  int n = 0, n_over = 0, K2 = 12, degree = 8;
+  Window win;
+  NerApiParams prm{};
+  float* d_iw = nullptr;
+  float2* d_tw = nullptr;
+  // host-path staging
+  size_t cap_u64 = 0, cap_u = 0, cap_k = 0, cap_o = 0, cap_o64 = 0;
+  double2* d_u64 = nullptr;
+  float2* d_u = nullptr;
+  double* d_k = nullptr;
+  float2* d_o = nullptr;
+  double2* d_o64 = nullptr;
+};
+
+namespace {
+int api_fail(int code, const std::string& m) { return set_last_error(code, m); }
+#define API_CUDA(expr)                                                                              \
+  do {                                                                                              \
+    cudaError_t _e = (expr);                                                                        \
+    if (_e != cudaSuccess) return api_fail(PATFFT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+unsigned gridn(size_t n) {
+  const size_t b = (n + 255) / 256;
+  return (unsigned)std::max<size_t>(1, std::min<size_t>(b, 148 * 32));
+}
+
+int launch_nerplan(patfft_ner_plan* P, const float2* u, const double* kap, int rows, int m, int shared, float2* out,
+                   cudaStream_t s) {
+  NerApiParams q = P->prm;
+  q.u = u;
+  q.kap = kap;
+  q.out = out;
+  q.rows = rows;
+  q.m = m;
+  q.shared = shared;
+  int threads = P->n_over / 16;
+  threads = std::max(64, std::min(512, threads));
+  const size_t smem = (size_t)P->n_over * sizeof(float2);
+  cudaError_t err = cudaSuccess;
+  auto go = [&](auto k) {
+    err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err == cudaSuccess && rows > 0) {
+      k<<<rows, threads, smem, s>>>(q);
+      err = cudaGetLastError();
+    }
+  };
+#define PATFFT_NERAPI_CASE(k2)                     \
+  case k2:                                         \
+    if (P->degree == 8) go(nerplan_kernel<k2, 8>); \
+    else go(nerplan_kernel<k2, 12>);               \
+    break;
+  switch (P->K2) {
+    PATFFT_NERAPI_CASE(2) PATFFT_NERAPI_CASE(4) PATFFT_NERAPI_CASE(6) PATFFT_NERAPI_CASE(8)
+    PATFFT_NERAPI_CASE(10) PATFFT_NERAPI_CASE(12) PATFFT_NERAPI_CASE(14) PATFFT_NERAPI_CASE(16)
+    default: return api_fail(PATFFT_ERR_PARAMETER, "unsupported K");
+  }
+#undef PATFFT_NERAPI_CASE
+  if (err != cudaSuccess) return api_fail(PATFFT_ERR_CUDA, cudaGetErrorString(err));
+  return PATFFT_OK;
+}
+
+template <typename T>
+int ensure(T** p, size_t* cap, size_t need) {
+  if (*cap >= need && *p) return PATFFT_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  API_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(1, need) * sizeof(T)));
+  *cap = need;
+  return PATFFT_OK;
+}
+}  // namespace
+
+// host-side helpers defined in capi.cu
+namespace patfft {
+double fit_ner_poly_public(const Window& w, int D, float (*poly)[kMaxPolyDegree + 1]);
+}
+
+extern "C" {
+
+int patfft_ner_plan_create(int n, double c, int K, double alpha, double beta, int device, patfft_ner_plan** out) {
+  if (!out) return api_fail(PATFFT_ERR_PARAMETER, "null argument");
+  *out = nullptr;
+  if (n < 2) return api_fail(PATFFT_ERR_PARAMETER, "input length must be >= 2");  // nufft.py:274-275
+  if (n % 2) return api_fail(PATFFT_ERR_UNSUPPORTED, "GPU NerPlan supports even lengths");
+  if (!(std::isfinite(c) && c > 1.0)) return api_fail(PATFFT_ERR_PARAMETER, "oversampling factor must exceed 1");
+  if (K < 1) return api_fail(PATFFT_ERR_PARAMETER, "interpolation half-width K must be an integer >= 1");
+  if (K > kMaxTaps / 2) return api_fail(PATFFT_ERR_UNSUPPORTED, "GPU path supports interpolation half-width K <= 8");
+  int64_t no = 1;
+  while (no < (int64_t)std::ceil(c * n)) no <<= 1;
+  if (no > 16384) return api_fail(PATFFT_ERR_UNSUPPORTED, "GPU NerPlan supports oversampled lengths up to 16384");
+  std::unique_ptr<patfft_ner_plan, void (*)(patfft_ner_plan*)> P(new patfft_ner_plan(), &patfft_ner_plan_destroy);
+  P->device = device;
+  API_CUDA(cudaSetDevice(device));
+  P->n = n;
+  P->n_over = (int)no;
+  P->K2 = 2 * K;
+  std::string err;
+  if (!resolve_window(c, K, alpha, beta, double(no) / n, &P->win, &err)) return api_fail(PATFFT_ERR_PARAMETER, err);
+  const int nref = even_fast_len(c * n);
+  if ((!std::isnan(alpha) || !std::isnan(beta)) && nref != no && no <= 8192) {
+    const double e = window_relative_error(P->win, n, (int)no);
+    if (!(e <= 1e-6))
+      return api_fail(PATFFT_ERR_UNSUPPORTED,
+                      "window loses accuracy at the GPU's power-of-two oversampled length (use default alpha/beta)");
+  }
+  const double s0 = kb_psihat(P->win, 0.0), norm = 1.0 / (2.0 * M_PI * P->win.c_eff);
+  std::vector<float> iw(n);
+  for (int k = 0; k < n; ++k) iw[k] = (float)(s0 * norm / kb_psi(P->win, 2.0 * M_PI * k / n - M_PI));
+  std::vector<float2> tw(1 << 14);
+  for (int k = 0; k < (1 << 14); ++k) {
+    const double a = -2.0 * M_PI * k / (1 << 14);
+    tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  P->degree = 8;
+  if (fit_ner_poly_public(P->win, 8, P->prm.poly) > 2e-8) {
+    P->degree = 12;
+    if (fit_ner_poly_public(P->win, 12, P->prm.poly) > 1e-6)
+      return api_fail(PATFFT_ERR_UNSUPPORTED, "window transform not representable by the tap polynomials");
+  }
+  API_CUDA(cudaMalloc(&P->d_iw, n * sizeof(float)));
+  API_CUDA(cudaMemcpy(P->d_iw, iw.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+  API_CUDA(cudaMalloc(&P->d_tw, tw.size() * sizeof(float2)));
+  API_CUDA(cudaMemcpy(P->d_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  API_CUDA(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  NerApiParams& q = P->prm;
+  q.iw = P->d_iw;
+  q.tw = P->d_tw;
+  q.n = n;
+  q.n_over = (int)no;
+  int L = 0;
+  while ((1 << L) < no) ++L;
+  q.L = L;
+  q.c_eff = P->win.c_eff;
+  *out = P.release();
+  return PATFFT_OK;
+}
+
+int patfft_ner_plan_info(const patfft_ner_plan* P, int64_t info[4]) {
+  if (!P || !info) return api_fail(PATFFT_ERR_PARAMETER, "null argument");
+  info[0] = P->n;
+  info[1] = P->n_over;
+  info[2] = P->K2;
+  info[3] = P->degree;
+  return PATFFT_OK;
+}
+
+int patfft_ner_execute_device(patfft_ner_plan* P, const void* u, const double* kappas, int rows, int m, int shared,
+                              void* out, void* stream) {
+  if (!P || (!u && rows) || (!kappas && m) || (!out && rows && m)) return api_fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  API_CUDA(cudaSetDevice(P->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+  if (rows == 0 || m == 0) return PATFFT_OK;
+  return launch_nerplan(P, static_cast<const float2*>(u), kappas, rows, m, shared, static_cast<float2*>(out), st);
+}
+
+int patfft_ner_execute(patfft_ner_plan* P, const double* u, const double* kappas, int rows, int m, int shared,
+                       double* out) {
+  if (!P) return api_fail(PATFFT_ERR_PARAMETER, "null plan");
+  if (rows == 0 || m == 0) return PATFFT_OK;
+  if (!u || !kappas || !out) return api_fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  API_CUDA(cudaSetDevice(P->device));
+  cudaStream_t st = P->stream;
+  const size_t nu = (size_t)rows * P->n, nk = shared ? (size_t)m : (size_t)rows * m, no = (size_t)rows * m;
+  int rc;
+  if ((rc = ensure(&P->d_u64, &P->cap_u64, nu))) return rc;
+  if ((rc = ensure(&P->d_u, &P->cap_u, nu))) return rc;
+  if ((rc = ensure(&P->d_k, &P->cap_k, nk))) return rc;
+  if ((rc = ensure(&P->d_o, &P->cap_o, no))) return rc;
+  if ((rc = ensure(&P->d_o64, &P->cap_o64, no))) return rc;
+  API_CUDA(cudaMemcpyAsync(P->d_u64, u, nu * sizeof(double2), cudaMemcpyHostToDevice, st));
+  API_CUDA(cudaMemcpyAsync(P->d_k, kappas, nk * sizeof(double), cudaMemcpyHostToDevice, st));
+  c128_to_c64<<<gridn(nu), 256, 0, st>>>(P->d_u64, P->d_u, nu);
+  if ((rc = launch_nerplan(P, P->d_u, P->d_k, rows, m, shared, P->d_o, st))) return rc;
+  c64_to_c128<<<gridn(no), 256, 0, st>>>(P->d_o, P->d_o64, no);
+  API_CUDA(cudaMemcpyAsync(out, P->d_o64, no * sizeof(double2), cudaMemcpyDeviceToHost, st));
+  API_CUDA(cudaStreamSynchronize(st));
+  return PATFFT_OK;
+}
+
+void patfft_ner_plan_destroy(patfft_ner_plan* P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  if (P->stream) cudaStreamSynchronize(P->stream);
+  for (void* p : {(void*)P->d_iw, (void*)P->d_tw, (void*)P->d_u64, (void*)P->d_u, (void*)P->d_k, (void*)P->d_o,
+                  (void*)P->d_o64})
+    if (p) cudaFree(p);
+  if (P->stream) cudaStreamDestroy(P->stream);
+  delete P;
+}
+
+}  // extern "C"

@@ -172,3 +172,36 @@ def test_gpu_equispaced_rejects_incomplete_grid():
     s = synth.make_3d(9, 16, 32, 20e-9, "jittered", 1)
     with pytest.raises(pb.ParameterError, match="complete sensor grid"):
         pb.reconstruct_equispaced(s.as_record())
+
+
+def test_gpu_nerplan_matches_reference_golden():
+    from conftest import GOLDEN
+
+    g = np.load(os.path.join(GOLDEN, "ner_rows.npz"))
+    plan = pb.NerPlan(g["u"].shape[-1])
+    out = plan.execute(g["u"], g["kappas"])
+    assert out.shape == g["out"].shape and out.dtype == np.complex128
+    e1 = rel_l2(out, g["out"])
+    e2 = rel_l2(plan.execute(g["u"], g["kappas_shared"]), g["out_shared"])
+    e3 = rel_l2(out, g["direct"])
+    print(f"NerPlan rows {e1:.2e} shared {e2:.2e} vs direct {e3:.2e}")
+    assert e1 <= 1e-5 and e2 <= 1e-5 and e3 <= 1e-5
+
+
+def test_gpu_nerplan_validation_and_larger_sizes():
+    rng = np.random.default_rng(3)
+    with pytest.raises(pb.ParameterError):
+        pb.NerPlan(1)
+    plan = pb.NerPlan(256)
+    with pytest.raises(pb.ParameterError):
+        plan.execute(np.zeros((2, 128)), np.zeros(3))
+    with pytest.raises(pb.ParameterError):
+        plan.execute(np.zeros((2, 256)), np.array([1e9]))
+    with pytest.raises(pb.ParameterError):
+        plan.execute(np.zeros((2, 256)), np.array([np.nan]))
+    u = rng.standard_normal((3, 4, 256)) + 1j * rng.standard_normal((3, 4, 256))
+    kap = rng.uniform(-256, 256, size=(3, 4, 50))
+    got = pb.nufft_ner(u, kap)
+    assert got.shape == (3, 4, 50)
+    want = O.ner_direct(u, kap)
+    assert rel_l2(got, want) <= 1e-5
