@@ -126,6 +126,17 @@ int patfft_ner_execute_device(patfft_ner_plan* plan, const void* u, const double
                               int shared, void* out, void* stream);
 void patfft_ner_plan_destroy(patfft_ner_plan* plan);
 
+/* ---- standalone NED NUFFT (the reference's NedPlan / nufft_ned, nufft.py:345-423) ----
+ * out[j, b] ~= sum_m values[m, b] exp(-2 pi i (j . x_m) / N), j on the centred
+ * grid out_dims (1 or 2 axes), x_m = grid_positions (n_points x n_lat, grid
+ * units).  values: n_points x n_values complex128 (interleaved) host; out:
+ * out_dims x n_values complex128 host, centred (centered != 0) or wrapped
+ * order (nufft.py:414-417).  The plan is tied to the positions.              */
+int patfft_ned_plan_create(int n_lat, const int32_t* out_dims, int n_values, double spec_c, int spec_K,
+                           double spec_alpha, double spec_beta, const double* grid_positions, int n_points,
+                           int device, patfft_nedner_plan** out);
+int patfft_ned_execute(patfft_nedner_plan* plan, const double* values, double* out, int centered);
+
 /* ---- multi-GPU (one process per GPU; the caller runs the two exchanges) ----
  * A sharded plan splits one reconstruction over `world` ranks:
  *   forward  : NED spread + lateral FFT of the rank's time slice

@@ -18,7 +18,7 @@ from .recon import (
     reconstruct_interp_fft,
     reconstruct_nedner,
 )
-from .nufft import NerPlan, nufft_ner
+from .nufft import NedPlan, NerPlan, nufft_ned, nufft_ner
 from .window import WindowSpec
 
 __version__ = "0.1.0"
@@ -30,11 +30,13 @@ __all__ = [
     "ParameterError",
     "EquispacedPlan",
     "NedNerPlan",
+    "NedPlan",
     "NerPlan",
     "ScalarField",
     "SensorRecord",
     "WindowSpec",
     "amplitude_factor",
+    "nufft_ned",
     "nufft_ner",
     "kappa",
     "reconstruct_equispaced",

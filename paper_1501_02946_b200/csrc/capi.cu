@@ -255,7 +255,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
       return fail(PATFFT_ERR_PARAMETER, err);
   }
   P->mode = mode;
-  if (mode != 0) {  // the full grid itself is the lateral FFT input: no oversampling, no window
+  if (mode == 1 || mode == 2) {  // the full grid itself is the lateral FFT input: no oversampling, no window
     for (int a = 0; a < d->n_lat; ++a)
       if (!is_pow2(d->out_dims[a]) || d->out_dims[a] < 4)
         return fail(PATFFT_ERR_UNSUPPORTED, "GPU equispaced path needs power-of-two lateral grids (>= 4)");
@@ -271,13 +271,15 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
 
   // ---- NER window (nufft.py:273-285), power-of-two oversampled length ----
   const int n_ext = 2 * P->T;  // NER always works on the full record length
-  // interp mode: plain length-2T FFT of the extension (recon.py:298)
-  const int64_t n_over_t = mode == 2 ? n_ext : next_pow2((int64_t)std::ceil(c * n_ext));
+  // interp mode: plain length-2T FFT of the extension (recon.py:298); NedPlan
+  // mode (3) has no NER at all
+  const int64_t n_over_t = mode == 3 ? 2 : (mode == 2 ? n_ext : next_pow2((int64_t)std::ceil(c * n_ext)));
   if (mode == 2 && !is_pow2(n_ext)) return fail(PATFFT_ERR_UNSUPPORTED, "GPU interp path needs a power-of-two N_t");
   if (n_over_t > 16384)
     return fail(PATFFT_ERR_UNSUPPORTED, "GPU NER supports oversampled depth lengths up to 16384 (N_t <= 4096 at c=2)");
   P->n_over_t = (int)n_over_t;
-  if (mode != 2 && !resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_t) / n_ext, &P->win_t, &err))
+  if (mode != 2 && mode != 3 &&
+      !resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_t) / n_ext, &P->win_t, &err))
     return fail(PATFFT_ERR_PARAMETER, err);
   P->fused_ifft = is_pow2(P->Tu) && P->Tu <= 16384;
 
@@ -286,12 +288,12 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // reference's (even 11-smooth length) the same (alpha, beta, K) can cover a
   // different part of the window.  Probe the accuracy at the GPU sizes and
   // refuse loudly instead of returning a silently different answer.
-  if (mode == 0 && (!std::isnan(d->spec_alpha) || !std::isnan(d->spec_beta))) {
+  if ((mode == 0 || mode == 3) && (!std::isnan(d->spec_alpha) || !std::isnan(d->spec_beta))) {
     struct Probe { const Window* w; int n, n_over, n_over_ref; };
     std::vector<Probe> probes;
     for (int a = 0; a < d->n_lat; ++a)
       probes.push_back({&P->win_lat[a], d->out_dims[a], n_over_lat[a], even_fast_len(c * d->out_dims[a])});
-    probes.push_back({&P->win_t, n_ext, P->n_over_t, even_fast_len(c * n_ext)});
+    if (mode != 3) probes.push_back({&P->win_t, n_ext, P->n_over_t, even_fast_len(c * n_ext)});
     for (const Probe& pr : probes) {
       if (pr.n_over == pr.n_over_ref || pr.n_over > 8192) continue;
       const double e = window_relative_error(*pr.w, pr.n, pr.n_over);
@@ -306,7 +308,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
       }
     }
   }
-  if (P->T > 8 * ner_threads(P->n_over_t))
+  if (mode != 3 && P->T > 8 * ner_threads(P->n_over_t))
     return fail(PATFFT_ERR_UNSUPPORTED, "depth too long for the NER CTA layout");
   P->custom_inverse = is_pow2(P->N0u) && is_pow2(P->N1u) && P->N0u <= 16384 && P->N1u <= 16384 && P->N1u >= 2;
 
@@ -336,7 +338,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   const int RECW = spread_record_words(K2);
   P->R = R;
   P->ngroups = (nrows + R - 1) / R;
-  const int Mrec = mode == 0 ? M : 0;  // the equispaced modes gather instead of spreading
+  const int Mrec = (mode == 0 || mode == 3) ? M : 0;  // the equispaced modes gather instead of spreading
   std::vector<int> ucol(M), urow(M);
   std::vector<double> wcolv((size_t)M * K2), wrowv((size_t)M * K2);
   for (int m = 0; m < Mrec; ++m) {
@@ -449,7 +451,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
       dp[jw] = (float)(s0 / (2.0 * M_PI * w.c_eff * kb_psi(w, 2.0 * M_PI * j / N)));
     }
   };
-  if (mode == 0) {
+  if (mode == 0 || mode == 3) {
     if (d->n_lat == 2) deapod(wrow, P->N0, dp0);
     deapod(wcol, P->N1, dp1);
   } else {
@@ -478,7 +480,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   }
   NerParams& q = P->ner;
   P->poly_degree = 8;
-  if (mode != 2 && fit_ner_poly(wt, 8, &q) > 2e-8) {
+  if (mode != 2 && mode != 3 && fit_ner_poly(wt, 8, &q) > 2e-8) {
     P->poly_degree = 12;
     if (fit_ner_poly(wt, 12, &q) > 1e-6)
       return fail(PATFFT_ERR_UNSUPPORTED, "window transform not representable by the tap polynomials");
@@ -487,7 +489,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // ---- device buffers -----------------------------------------------------
   int rc;
   if ((rc = upload(&P->d_recs, recbuf))) return rc;
-  if (mode != 0) {
+  if (mode == 1 || mode == 2) {
     std::vector<int> gi(M);
     std::vector<char> seen((size_t)M, 0);
     for (int m = 0; m < M; ++m) {
@@ -527,7 +529,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   CUDA_TRY(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
 
   // ---- cuFFT only for sizes the shared-memory kernels do not cover --------
-  if (!P->custom_inverse) {
+  if (!P->custom_inverse && mode != 3) {
     int n[2], inem[2], onem[2];
     const int rank = d->n_lat;
     if (rank == 2) {
@@ -540,7 +542,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     CUFFT_TRY(cufftPlanMany(&P->fft_c2r, rank, n, inem, P->Tu, 1, onem, P->Tu, 1, CUFFT_C2R, P->Tu));
     P->have_c2r = true;
   }
-  if (!P->fused_ifft) {
+  if (!P->fused_ifft && mode != 3) {
     int nl[1] = {P->Tu};
     CUFFT_TRY(cufftPlanMany(&P->fft_l, 1, nl, nl, 1, P->Tu, nl, 1, P->Tu, CUFFT_C2C, P->N0u * P->N1uh));
     P->have_l = true;
@@ -624,6 +626,69 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
 int patfft_nedner_plan_create(const patfft_nedner_desc* d, const double* gpos, const double* sscale, int device,
                               patfft_nedner_plan** out) {
   return create_plan(d, gpos, sscale, device, 0, 1, 0, nullptr, out);
+}
+
+int patfft_ned_plan_create(int n_lat, const int32_t* out_dims, int n_values, double spec_c, int spec_K,
+                           double spec_alpha, double spec_beta, const double* grid_positions, int n_points,
+                           int device, patfft_nedner_plan** out) {
+  if (!out_dims || !grid_positions || !out) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  if (n_values < 1) return fail(PATFFT_ERR_PARAMETER, "need at least one value column");
+  patfft_nedner_desc d{};
+  d.n_lat = n_lat;
+  d.out_dims[0] = out_dims[0];
+  d.out_dims[1] = n_lat == 2 ? out_dims[1] : 0;
+  d.n_time = 2 * n_values;  // real and imaginary parts as interleaved samples
+  d.upsample = 1;
+  d.n_sensors = n_points;
+  d.lat_ratio[0] = d.lat_ratio[1] = 1.0;
+  d.spec_c = spec_c;
+  d.spec_K = spec_K;
+  d.spec_alpha = spec_alpha;
+  d.spec_beta = spec_beta;
+  std::vector<double> ones(std::max(1, n_points), 1.0);
+  return create_plan(&d, grid_positions, ones.data(), device, 0, 1, 3, nullptr, out);
+}
+
+int patfft_ned_execute(patfft_nedner_plan* P, const double* values, double* out, int centered) {
+  if (!P || !values || !out) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  if (P->mode != 3) return fail(PATFFT_ERR_PARAMETER, "not a NedPlan plan");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  const int B = P->T / 2;
+  const size_t in_n = (size_t)P->M * P->T, out_c = (size_t)P->N0 * P->N1 * B;
+  int rc;
+  if (!P->d_samples && (rc = dalloc(&P->d_samples, in_n))) return rc;
+  if (!P->d_samples64 && (rc = dalloc(&P->d_samples64, in_n))) return rc;
+  if (!P->d_out64 && (rc = dalloc(&P->d_out64, 2 * out_c))) return rc;
+  cudaStream_t st = P->stream;
+  CUDA_TRY(cudaMemcpyAsync(P->d_samples64, values, in_n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_f64_to_f32(P->d_samples64, P->d_samples, in_n, st));
+  SpreadParams sp;
+  sp.samples = P->d_samples;
+  sp.recs = P->d_recs;
+  sp.blk = P->d_blk;
+  sp.blk_grp = P->d_blkgrp;
+  sp.grid = P->d_grid;
+  sp.T = P->T;
+  sp.ncols = P->ncols;
+  sp.nrows = P->nrows;
+  sp.t_begin = 0;
+  sp.t_end = P->T;
+  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
+  LateralParams L = P->lat;
+  L.cplx = 1;
+  L.centered = centered ? 1 : 0;
+  L.ny = P->N1;
+  L.t_begin = 0;
+  L.t_end = P->T;
+  CUDA_TRY(launch_lateral_col(L, st));
+  L.T = B;  // rowfft works on complex columns
+  L.t_end = B;
+  CUDA_TRY(launch_lateral_row(L, st));
+  CUDA_TRY(launch_f32_to_f64(reinterpret_cast<const float*>(P->d_gh), P->d_out64, 2 * out_c, st));
+  CUDA_TRY(cudaMemcpyAsync(out, P->d_out64, 2 * out_c * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PATFFT_OK;
 }
 
 int patfft_equispaced_plan_create(const patfft_nedner_desc* d, const int64_t* grid_index, int time_eval, int device,

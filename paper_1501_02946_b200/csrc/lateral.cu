@@ -53,6 +53,20 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
   __syncthreads();
   if constexpr (LC > 0) fft::fft_ct<false, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
   else fft::fft_inplace<false, 4, false>(sm, p.lcols, PLOG, p.tw, tid, nth, ad);
+  if (p.cplx) {
+    // complex values (NedPlan): the packed pair IS one complex sample; keep
+    // the full cropped spectrum j1 in [-N1/2, N1/2) in wrapped order
+    const int Tc = T / 2;
+    float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * Tc;
+    for (int i = tid; i < p.ny * P; i += nth) {
+      const int k = i >> PLOG, q = i & (P - 1);
+      const int t = t0 + 2 * q;
+      if (t >= p.t_end) continue;
+      const int j1 = k < p.N1 / 2 ? k : k - p.N1;
+      dst[(size_t)k * Tc + t / 2] = sm[ad(j1 & (n - 1), q)];
+    }
+    return;
+  }
   float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * T;
   for (int i = tid; i < p.ny * P; i += nth) {
     const int k = i >> PLOG, q = i & (P - 1);
@@ -86,9 +100,25 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
   __syncthreads();
   if constexpr (LC > 0) fft::fft_ct<false, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
   else fft::fft_inplace<false, 4, false>(sm, p.lrows, PLOG, p.tw, tid, nth, ad);
-  const bool nyq1 = (j1 == p.N1 / 2);
   const int N0 = p.N0, mask = nr - 1;
   const float dp1 = p.dp1[j1];
+  if (p.cplx) {
+    // NedPlan: full spectrum, centred-grid sign (-1)^(j0+j1), deapodise,
+    // centred or wrapped output order (nufft.py:406-417)
+    const int j1s = j1 < p.N1 / 2 ? j1 : j1 - p.N1;
+    for (int i = tid; i < N0 * P; i += nth) {
+      const int j0w = i >> PLOG, q = i & (P - 1);
+      const int t = t0 + q;
+      if (t >= p.t_end) continue;
+      const int a = (N0 > 1) ? (j0w < N0 / 2 ? j0w : j0w - N0) : 0;
+      const float sg = ((a + j1s) & 1) ? -1.f : 1.f;
+      const float2 v = fft::cscale(sm[ad(a & mask, q)], sg * p.dp0[j0w] * dp1);
+      const size_t o = p.centered ? (size_t)(a + N0 / 2) * p.ny + (j1s + p.N1 / 2) : (size_t)j0w * p.ny + j1;
+      p.gh[o * T + t] = v;
+    }
+    return;
+  }
+  const bool nyq1 = (j1 == p.N1 / 2);
   for (int i = tid; i < N0 * P; i += nth) {
     const int j0w = i >> PLOG, q = i & (P - 1);
     const int t = t0 + q;

@@ -61,6 +61,8 @@ struct LateralParams {
   const float* dp1;    // [N1]
   int T, nrows, lrows, ncols, lcols, ny, N0, N1;
   int t_begin, t_end;  // forward kernels: time range processed by this launch
+  int cplx;            // 1: NedPlan mode (complex values, full spectrum, no Hermitian fix-up)
+  int centered;        // NedPlan output order
   // inverse
   float2* z;           // [N0u][N1uh][Tu]
   float* out;          // [N0u][N1u][Tu]

@@ -205,3 +205,32 @@ def test_gpu_nerplan_validation_and_larger_sizes():
     assert got.shape == (3, 4, 50)
     want = O.ner_direct(u, kap)
     assert rel_l2(got, want) <= 1e-5
+
+
+def test_gpu_nedplan_matches_reference_golden():
+    from conftest import GOLDEN
+
+    g = np.load(os.path.join(GOLDEN, "ned_axes.npz"))
+    out1 = pb.NedPlan((32,)).execute(g["pos1"], g["v1"])
+    out2 = pb.NedPlan((16, 24)).execute(g["pos2"], g["v2"], order="wrapped")
+    e1, e1d = rel_l2(out1, g["out1"]), rel_l2(out1, g["direct1"])
+    e2 = rel_l2(out2, g["out2_wrapped"])
+    print(f"NedPlan 1-axis {e1:.2e} (direct {e1d:.2e}), 2-axis wrapped {e2:.2e}")
+    assert out1.shape == g["out1"].shape and out2.shape == g["out2_wrapped"].shape
+    assert e1 <= 1e-5 and e1d <= 1e-5 and e2 <= 1e-5
+
+
+def test_gpu_nedplan_centered_2d_vs_direct_and_validation():
+    rng = np.random.default_rng(5)
+    pos = np.stack([rng.uniform(-16, 16, 300), rng.uniform(-8, 8, 300)], axis=1)
+    vals = rng.standard_normal((300, 3)) + 1j * rng.standard_normal((300, 3))
+    got = pb.nufft_ned(pos, vals, (32, 16))
+    want = O.ned_direct(pos, vals, (32, 16))
+    assert got.shape == (32, 16, 3)
+    assert rel_l2(got, want) <= 1e-5
+    with pytest.raises(pb.ParameterError):
+        pb.NedPlan((32, 16)).execute(pos * 3, vals)
+    with pytest.raises(pb.ParameterError):
+        pb.NedPlan((32, 15))
+    with pytest.raises(pb.ParameterError):
+        pb.NedPlan((32, 16)).execute(pos, vals, order="sideways")
