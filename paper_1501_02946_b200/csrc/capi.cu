@@ -195,7 +195,7 @@ const char* patfft_version(void) { return "patfft-b200 0.2.0 (sm_100a)"; }
 // mode 2: equispaced grid + linear interpolation (reconstruct_interp_fft, recon.py:382-389)
 static int create_plan(const patfft_nedner_desc* d, const double* gpos, const double* sscale, int device, int rank,
                        int world, int mode, const int64_t* gidx, patfft_nedner_plan** out) {
-  if (!d || !out || (mode == 0 && (!gpos || !sscale)) || (mode != 0 && !gidx))
+  if (!d || !out || ((mode == 0 || mode == 3) && (!gpos || !sscale)) || ((mode == 1 || mode == 2) && !gidx))
     return fail(PATFFT_ERR_PARAMETER, "null argument");
   if (world < 1 || rank < 0 || rank >= world) return fail(PATFFT_ERR_PARAMETER, "invalid rank / world size");
   *out = nullptr;
