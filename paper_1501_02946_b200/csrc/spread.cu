@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "patfft_internal.h"
 
@@ -230,7 +231,15 @@ cudaError_t go(const SpreadParams& p, int nblk, cudaStream_t s) {
 
 }  // namespace
 
-int spread_rows_per_group(int n_lat, int K2) { return n_lat == 1 ? 1 : (K2 <= 12 ? 4 : 2); }
+int spread_rows_per_group(int n_lat, int K2) {
+  static const int forced = [] {
+    const char* e = std::getenv("PATFFT_SPREAD_ROWS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (n_lat == 1) return 1;
+  if ((forced == 2 || forced == 4) && (K2 <= 12 || forced == 2)) return forced;
+  return K2 <= 12 ? 4 : 2;
+}
 int spread_ring(int K2) { return K2 <= 12 ? 16 : 32; }
 int spread_record_words(int K2) { return 8 + spread_ring(K2); }
 int spread_time_chunks(int T) { return (T + kThreads - 1) / kThreads; }
@@ -247,6 +256,12 @@ cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaSt
     }
   } else if (R == 2) {
     switch (K2) {
+      case 2: return go<2, 2, 16>(p, nblk, s);
+      case 4: return go<4, 2, 16>(p, nblk, s);
+      case 6: return go<6, 2, 16>(p, nblk, s);
+      case 8: return go<8, 2, 16>(p, nblk, s);
+      case 10: return go<10, 2, 16>(p, nblk, s);
+      case 12: return go<12, 2, 16>(p, nblk, s);
       case 14: return go<14, 2, 32>(p, nblk, s);
       case 16: return go<16, 2, 32>(p, nblk, s);
     }
