@@ -181,7 +181,7 @@ def run_reference_arm(args):
     recs = make_workload(args.config)
     rec = recs[0]
     vox = _voxels(rec)
-    frac = args.cpu_frac
+    frac = args.cpu_frac or 1.0 / 16
     vals = []
     for i in range(args.warmup + args.steps):
         full, meas = cpu_sample_seconds(rec, frac)
@@ -458,9 +458,10 @@ def run_gpu_arm(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         os.environ.setdefault("PAT_THREADS", str(os.cpu_count() or 1))
-        full, meas = cpu_sample_seconds(rec, args.cpu_frac)
+        cfrac = args.cpu_frac or 0.25
+        full, meas = cpu_sample_seconds(rec, cfrac)
         cpu = {"value": _voxels(rec) / full, "unit": UNIT, "cores": int(os.environ["PAT_THREADS"]),
-               "kind": "port", "sample": _sample_desc(args.config, args.cpu_frac), "measured_s": meas}
+               "kind": "port", "sample": _sample_desc(args.config, cfrac), "measured_s": meas}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -491,7 +492,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-frac", type=float, default=1.0 / 16)
+    ap.add_argument("--cpu-frac", type=float, default=None,
+                    help="fraction of the workload the CPU sample runs (default: 1/4 for the cpu_baseline leg "
+                         "(~10-15 s), 1/16 per step for --impl reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the sharded multi-GPU path even at N=1")
     args = ap.parse_args()

@@ -14,7 +14,7 @@ import re
 from .errors import DataValidationError, DeviceError, ParameterError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpatfft_b200.so")
+LIB_PATH = os.environ.get("PATFFT_LIB") or os.path.join(HERE, "libpatfft_b200.so")  # PATFFT_LIB: experimental variant builds
 HEADER = os.path.join(os.path.dirname(HERE), "include", "patfft_b200.h")
 
 PATFFT_OK = 0

@@ -400,8 +400,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     std::memcpy(&o[0], &recs[i].ws, 4);
     std::memcpy(&o[1], &recs[i].m, 4);
     for (int r = 0; r < 4; ++r) o[4 + r] = recs[i].wr[r];
-    const int ring = RECW - 8;
-    for (int j = 0; j < K2; ++j) o[8 + (int)pmod(recs[i].ws + j, ring)] = (float)wcolv[(size_t)recs[i].m * K2 + j];
+    for (int j = 0; j < K2; ++j) o[8 + (int)pmod(recs[i].ws + j, K2)] = (float)wcolv[(size_t)recs[i].m * K2 + j];
   }
   std::vector<int64_t> gstart(P->ngroups + 1, 0);
   for (const Rec& r : recs) gstart[r.grp + 1]++;
@@ -414,7 +413,11 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   std::vector<int> blk_grp;
   {
     const int64_t tch = spread_time_chunks(T);
-    const int64_t target_blocks = 148LL * 16;  // ~4 resident CTAs/SM x 4 waves
+    static const int waves = [] {
+      const char* e = std::getenv("PATFFT_SPREAD_WAVES");
+      return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    const int64_t target_blocks = 148LL * spread_ctas_per_sm() * waves;
     const int64_t per_chunk = std::max<int64_t>(1, ceildiv(target_blocks, tch));
     const int64_t nrec_all = std::max<int64_t>(1, (int64_t)recs.size());
     const double rec_per_block = std::max(64.0, (double)nrec_all / (double)per_chunk);
@@ -440,6 +443,27 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
       }
     }
     P->nblk = (int)blk.size();
+    // longest-first launch order: the block scheduler then fills the tail of
+    // the grid with the short segments (LPT), instead of ending on a partial
+    // wave of full-size ones
+    static const bool lpt = [] {
+      const char* e = std::getenv("PATFFT_SPREAD_LPT");
+      return e ? std::atoi(e) != 0 : true;
+    }();
+    if (lpt) {
+      std::vector<int> order(blk.size());
+      for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+      auto cost = [&](int i) { return (int64_t)(blk[i].y - blk[i].x) * 8 + (blk[i].w - blk[i].z); };
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
+      std::vector<int4> b2(blk.size());
+      std::vector<int> g2(blk.size());
+      for (size_t i = 0; i < order.size(); ++i) {
+        b2[i] = blk[order[i]];
+        g2[i] = blk_grp[order[i]];
+      }
+      blk.swap(b2);
+      blk_grp.swap(g2);
+    }
   }
 
   // ---- deapodisation (nufft.py:367-371), normalised by psi_hat(0) --------

@@ -93,6 +93,7 @@ struct NerParams {
 cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaStream_t s);
 int spread_rows_per_group(int n_lat, int K2);
 int spread_record_words(int K2);
+int spread_ctas_per_sm();
 int spread_time_chunks(int T);
 cudaError_t launch_lateral_col(const LateralParams& p, cudaStream_t s);
 cudaError_t launch_lateral_row(const LateralParams& p, cudaStream_t s);

@@ -21,7 +21,13 @@ namespace patfft {
 namespace {
 
 constexpr int kThreads = 128;  // time samples per CTA
-constexpr int kChunk = 32;     // records staged per chunk
+#ifndef PATFFT_SPREAD_CHUNK
+#define PATFFT_SPREAD_CHUNK 32
+#endif
+constexpr int kChunk = PATFFT_SPREAD_CHUNK;  // records staged per chunk
+#ifndef PATFFT_SPREAD_MINB
+#define PATFFT_SPREAD_MINB 5
+#endif
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -48,51 +54,73 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return d;
 }
 
-template <int Q, int R, int RING>
-__device__ __forceinline__ void flush_q(float2 (&acc)[R][RING / 2], float* __restrict__ colp, size_t row_stride,
-                                        int T, int rows_valid, bool store) {
+// Accumulators: acc[slot][p] holds rows (2p, 2p+1) of ring column `slot`
+// (R = 1: only .x is used).  Flushing a column stores its R rows (coalesced
+// over time) and clears the slot.
+template <int Q, int R, int NS>
+__device__ __forceinline__ void flush_slot(float2 (&acc)[NS][(R + 1) / 2], float* __restrict__ colp,
+                                           size_t row_stride, int rows_valid, bool store) {
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
+  for (int p = 0; p < (R + 1) / 2; ++p) {
+    if (store && 2 * p < rows_valid) colp[(size_t)(2 * p) * row_stride] = acc[Q][p].x;
+    if (R > 1 && store && 2 * p + 1 < rows_valid) colp[(size_t)(2 * p + 1) * row_stride] = acc[Q][p].y;
+    acc[Q][p] = make_float2(0.f, 0.f);
+  }
+}
+
+// One record: acc[j][p] += (s*wr[2p], s*wr[2p+1]) * w_j for every ring slot j.
+template <int NS, int R>
+__device__ __forceinline__ void record_fma(float2 (&acc)[NS][(R + 1) / 2], const float* __restrict__ rec, float s) {
+  constexpr int RP = (R + 1) / 2;
+  const float4 wr4 = *reinterpret_cast<const float4*>(rec + 4);
+  float2 sv[RP];
+  if (R == 1) {
+    sv[0] = make_float2(s * wr4.x, 0.f);
+  } else {
+    sv[0] = make_float2(s * wr4.x, s * wr4.y);
+    if (RP > 1) sv[RP > 1 ? 1 : 0] = make_float2(s * wr4.z, s * wr4.w);
+  }
+  const float4* wq = reinterpret_cast<const float4*>(rec + 8);
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      if (store && r < rows_valid) {
-        colp[(size_t)r * row_stride + (size_t)(2 * c) * T] = acc[r][Q * 2 + c].x;
-        colp[(size_t)r * row_stride + (size_t)(2 * c + 1) * T] = acc[r][Q * 2 + c].y;
+  for (int j4 = 0; j4 < (NS + 3) / 4; ++j4) {
+    const float4 q = wq[j4];
+    const float wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j4 * 4 + u;
+      if (j < NS) {
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          if (R == 1) acc[j < NS ? j : 0][r].x = fmaf(sv[r].x, wv[u], acc[j < NS ? j : 0][r].x);
+          else acc[j < NS ? j : 0][r] = ffma2(sv[r], make_float2(wv[u], wv[u]), acc[j < NS ? j : 0][r]);
+        }
       }
-      acc[r][Q * 2 + c] = make_float2(0.f, 0.f);
     }
   }
 }
 
-template <int R, int RING>
-__device__ __forceinline__ void flush_group(float2 (&acc)[R][RING / 2], int g, float* __restrict__ base, size_t row_stride,
-                                            int T, int c0, int c1, int rows_valid, bool tvalid) {
-  const int col = g * 4;
-  const bool store = tvalid && col >= c0 && col < c1;
-  float* colp = base + (size_t)(store ? col : 0) * T;
-  switch (g & (RING / 4 - 1)) {
-#define PATFFT_FQ(q) \
-  case q:            \
-    if (q < RING / 4) flush_q<(q < RING / 4 ? q : 0), R, RING>(acc, colp, row_stride, T, rows_valid, store); \
-    break;
-    PATFFT_FQ(0) PATFFT_FQ(1) PATFFT_FQ(2) PATFFT_FQ(3) PATFFT_FQ(4) PATFFT_FQ(5) PATFFT_FQ(6) PATFFT_FQ(7)
-#undef PATFFT_FQ
-  }
-}
-
 // Record layout (float words): [0] ws (int bits), [1] sensor m (int bits),
-// [2..3] pad, [4..7] row weights (R <= 4), [8..8+RING) column weights
-// rotated into ring order: slot (ws + j) mod RING holds tap j, the other
-// RING - 2K slots are zero.  Every record then updates the whole ring with
-// compile-time register indices (no per-record branch on the rotation).
-template <int K2, int R, int RING, bool VEC16>
-__global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams p) {
-  static_assert(K2 + 3 <= RING, "ring too small for the window");
-  constexpr int RECW = 8 + RING;
-  constexpr int NG = RING / 4;
+// [2..3] pad, [4..7] row weights (R <= 4), [8..8+NS) column weights rotated
+// into ring order: slot (ws + j) mod NS holds tap j.  The ring is exactly
+// NS = 2K columns wide, so every FMA is useful in the column direction, and
+// each record updates the whole ring with compile-time register indices.
+// Rows are paired into FFMA2 lanes: acc[j][p] += (s*wr[2p], s*wr[2p+1]) *
+// w_j, with the column weight folded in as the broadcast operand.
+//
+// Column sweep as a state machine: state q means "the ring's oldest column
+// fg lives in slot q".  In state q the CTA applies every record starting at
+// fg, then flushes slot q (a compile-time register set: no indirect branch
+// per column) and moves to state q + 1 mod NS.  The state is dispatched
+// dynamically only when a staged chunk of records runs out.
+template <int K2, int R, bool VEC16>
+__global__ void __launch_bounds__(kThreads, PATFFT_SPREAD_MINB) spread_kernel(const SpreadParams p) {
+  constexpr int NS = K2;
+  constexpr int RP = (R + 1) / 2;
+  constexpr int RECW = 8 + (K2 + 3) / 4 * 4;
   constexpr int PIECE = VEC16 ? 4 : 2;                 // floats per cp.async
   constexpr int PIECES = kThreads / PIECE;             // per record
   constexpr int PER_THREAD = kChunk * PIECES / kThreads;
+  static_assert(NS <= 16, "ring states are generated for up to 16 slots");
   extern __shared__ float4 smem4[];
   float* rbuf = reinterpret_cast<float*>(smem4);             // [2][kChunk][RECW]
   float* sbuf = rbuf + 2 * kChunk * RECW;                    // [2][kChunk][kThreads]
@@ -148,81 +176,97 @@ __global__ void __launch_bounds__(kThreads, 4) spread_kernel(const SpreadParams 
     cp_commit();
   };
 
-  float2 acc[R][RING / 2];  // column pairs (2c, 2c+1)
+  float2 acc[NS][RP];
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+  for (int j = 0; j < NS; ++j)
 #pragma unroll
-    for (int c = 0; c < RING / 2; ++c) acc[r][c] = make_float2(0.f, 0.f);
+    for (int q = 0; q < RP; ++q) acc[j][q] = make_float2(0.f, 0.f);
 
   const size_t row_stride = (size_t)p.ncols * T;
   float* base = p.grid + (size_t)row0 * row_stride + (tvalid ? t : 0);
-  int fg = (c0 >> 2) - NG;  // ring holds column groups [fg, fg + NG)
+  // the ring holds columns [fg, fg + NS); start on a multiple of NS so the
+  // sweep enters in state 0 (the few extra columns before c0 are not stored)
+  int fg = (c0 - NS) >= 0 ? (c0 - NS) / NS * NS : -((NS - (c0 - NS) - 1) / NS) * NS;
+  int fs = 0;
 
   if (nchunks > 0) {
     load_m(0);
     stage(0, 0);
     load_m(1);
   }
-  for (int c = 0; c < nchunks; ++c) {
+  const int npass = max(nchunks, 1);
+  for (int c = 0; c < npass; ++c) {
     const int b = c & 1;
-    if (c + 1 < nchunks) {
-      stage(c + 1, b ^ 1);
-      load_m(c + 2);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
+    int ne = 0;
+    if (c < nchunks) {
+      if (c + 1 < nchunks) {
+        stage(c + 1, b ^ 1);
+        load_m(c + 2);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      __syncthreads();
+      ne = min(kChunk, nrec - c * kChunk);
     }
-    __syncthreads();
+    const bool last = c + 1 >= npass;
     const float* rb = rbuf + b * kChunk * RECW;
     const float* sb = sbuf + b * kChunk * kThreads + tid;
-    const int ne = min(kChunk, nrec - c * kChunk);
-    for (int e = 0; e < ne; ++e) {
-      const float* rec = rb + e * RECW;
-      const int ws = __float_as_int(rec[0]);
-      const int gs = ws >> 2;
-      while (fg < gs) {
-        flush_group<R, RING>(acc, fg, base, row_stride, T, c0, c1, rows_valid, tvalid);
-        ++fg;
-      }
-      const float s = sb[e * kThreads];
-      const float4 wr4 = *reinterpret_cast<const float4*>(rec + 4);
-      const float wrv[4] = {wr4.x, wr4.y, wr4.z, wr4.w};
-      float sv[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) sv[r] = s * wrv[r];
-      const float4* wq = reinterpret_cast<const float4*>(rec + 8);
-#pragma unroll
-      for (int j = 0; j < RING / 4; ++j) {
-        const float4 q = wq[j];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const float2 svv = make_float2(sv[r], sv[r]);
-          acc[r][2 * j + 0] = ffma2(make_float2(q.x, q.y), svv, acc[r][2 * j + 0]);
-          acc[r][2 * j + 1] = ffma2(make_float2(q.z, q.w), svv, acc[r][2 * j + 1]);
-        }
-      }
+    int e = 0;
+    switch (fs) {
+      case 0: goto st_0;   case 1: goto st_1;   case 2: goto st_2;   case 3: goto st_3;
+      case 4: goto st_4;   case 5: goto st_5;   case 6: goto st_6;   case 7: goto st_7;
+      case 8: goto st_8;   case 9: goto st_9;   case 10: goto st_10; case 11: goto st_11;
+      case 12: goto st_12; case 13: goto st_13; case 14: goto st_14; default: goto st_15;
     }
+#define PATFFT_STATE(q, qn)                                                                          \
+  st_##q:                                                                                            \
+    if (q < NS) {                                                                                    \
+      while (e < ne) {                                                                               \
+        const float* rec = rb + e * RECW;                                                            \
+        if (__float_as_int(rec[0]) != fg) break;                                                     \
+        record_fma<NS, R>(acc, rec, sb[e * kThreads]);                                               \
+        ++e;                                                                                         \
+      }                                                                                              \
+      if (e == ne) {                                                                                 \
+        if (!last) {                                                                                 \
+          fs = q;                                                                                    \
+          goto chunk_end;                                                                            \
+        }                                                                                            \
+        if (fg >= c1) goto all_done;                                                                 \
+      }                                                                                              \
+      {                                                                                              \
+        const bool store = tvalid && fg >= c0 && fg < c1;                                            \
+        flush_slot<(q < NS ? q : 0), R, NS>(acc, base + (size_t)(store ? fg : 0) * T, row_stride,    \
+                                            rows_valid, store);                                      \
+      }                                                                                              \
+      ++fg;                                                                                          \
+      if (q + 1 >= NS) goto st_0;                                                                    \
+      goto st_##qn;                                                                                  \
+    }
+    PATFFT_STATE(0, 1) PATFFT_STATE(1, 2) PATFFT_STATE(2, 3) PATFFT_STATE(3, 4)
+    PATFFT_STATE(4, 5) PATFFT_STATE(5, 6) PATFFT_STATE(6, 7) PATFFT_STATE(7, 8)
+    PATFFT_STATE(8, 9) PATFFT_STATE(9, 10) PATFFT_STATE(10, 11) PATFFT_STATE(11, 12)
+    PATFFT_STATE(12, 13) PATFFT_STATE(13, 14) PATFFT_STATE(14, 15) PATFFT_STATE(15, 0)
+#undef PATFFT_STATE
+  chunk_end:
     __syncthreads();
   }
-  const int gend = c1 >> 2;
-  while (fg < gend) {
-    flush_group<R, RING>(acc, fg, base, row_stride, T, c0, c1, rows_valid, tvalid);
-    ++fg;
-  }
+all_done:;
 }
 
-template <int K2, int R, int RING>
+template <int K2, int R>
 cudaError_t go(const SpreadParams& p, int nblk, cudaStream_t s) {
-  constexpr int RECW = 8 + RING;
+  constexpr int RECW = 8 + (K2 + 3) / 4 * 4;
   const size_t smem = sizeof(float) * 2 * kChunk * (RECW + kThreads);
   dim3 grid((unsigned)nblk, (unsigned)((p.t_end - p.t_begin + kThreads - 1) / kThreads));
   cudaError_t err;
   if (p.T % 4 == 0) {
-    auto k = spread_kernel<K2, R, RING, true>;
+    auto k = spread_kernel<K2, R, true>;
     if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return err;
     k<<<grid, kThreads, smem, s>>>(p);
   } else {
-    auto k = spread_kernel<K2, R, RING, false>;
+    auto k = spread_kernel<K2, R, false>;
     if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return err;
     k<<<grid, kThreads, smem, s>>>(p);
   }
@@ -236,47 +280,36 @@ int spread_rows_per_group(int n_lat, int K2) {
     const char* e = std::getenv("PATFFT_SPREAD_ROWS");
     return e ? std::atoi(e) : 0;
   }();
+  (void)K2;
   if (n_lat == 1) return 1;
-  if ((forced == 2 || forced == 4) && (K2 <= 12 || forced == 2)) return forced;
-  return K2 <= 12 ? 4 : 2;
+  if (forced == 2 || forced == 4) return forced;
+  return 4;
 }
-int spread_ring(int K2) { return K2 <= 12 ? 16 : 32; }
-int spread_record_words(int K2) { return 8 + spread_ring(K2); }
+int spread_ring(int K2) { return K2; }
+int spread_ctas_per_sm() { return PATFFT_SPREAD_MINB; }
+int spread_record_words(int K2) { return 8 + (K2 + 3) / 4 * 4; }
 int spread_time_chunks(int T) { return (T + kThreads - 1) / kThreads; }
 
 cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaStream_t s) {
-  if (R == 4) {
-    switch (K2) {
-      case 2: return go<2, 4, 16>(p, nblk, s);
-      case 4: return go<4, 4, 16>(p, nblk, s);
-      case 6: return go<6, 4, 16>(p, nblk, s);
-      case 8: return go<8, 4, 16>(p, nblk, s);
-      case 10: return go<10, 4, 16>(p, nblk, s);
-      case 12: return go<12, 4, 16>(p, nblk, s);
-    }
-  } else if (R == 2) {
-    switch (K2) {
-      case 2: return go<2, 2, 16>(p, nblk, s);
-      case 4: return go<4, 2, 16>(p, nblk, s);
-      case 6: return go<6, 2, 16>(p, nblk, s);
-      case 8: return go<8, 2, 16>(p, nblk, s);
-      case 10: return go<10, 2, 16>(p, nblk, s);
-      case 12: return go<12, 2, 16>(p, nblk, s);
-      case 14: return go<14, 2, 32>(p, nblk, s);
-      case 16: return go<16, 2, 32>(p, nblk, s);
-    }
-  } else if (R == 1) {
-    switch (K2) {
-      case 2: return go<2, 1, 16>(p, nblk, s);
-      case 4: return go<4, 1, 16>(p, nblk, s);
-      case 6: return go<6, 1, 16>(p, nblk, s);
-      case 8: return go<8, 1, 16>(p, nblk, s);
-      case 10: return go<10, 1, 16>(p, nblk, s);
-      case 12: return go<12, 1, 16>(p, nblk, s);
-      case 14: return go<14, 1, 32>(p, nblk, s);
-      case 16: return go<16, 1, 32>(p, nblk, s);
-    }
+#define PATFFT_SPREAD_K(RR)                         \
+  switch (K2) {                                     \
+    case 2: return go<2, RR>(p, nblk, s);           \
+    case 4: return go<4, RR>(p, nblk, s);           \
+    case 6: return go<6, RR>(p, nblk, s);           \
+    case 8: return go<8, RR>(p, nblk, s);           \
+    case 10: return go<10, RR>(p, nblk, s);         \
+    case 12: return go<12, RR>(p, nblk, s);         \
+    case 14: return go<14, RR>(p, nblk, s);         \
+    case 16: return go<16, RR>(p, nblk, s);         \
   }
+  if (R == 4) {
+    PATFFT_SPREAD_K(4)
+  } else if (R == 2) {
+    PATFFT_SPREAD_K(2)
+  } else if (R == 1) {
+    PATFFT_SPREAD_K(1)
+  }
+#undef PATFFT_SPREAD_K
   return cudaErrorInvalidValue;
 }
 
