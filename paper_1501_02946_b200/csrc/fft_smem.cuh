@@ -12,6 +12,7 @@
 // Twiddles come from one table tw[k] = exp(-2 pi i k / 2^LMAX); a length-2^L
 // transform reads it with stride 2^(LMAX-L).
 #pragma once
+#include <type_traits>
 
 #include <cuda_runtime.h>
 
@@ -168,6 +169,7 @@ __device__ __forceinline__ int brev(int i, int L) { return L ? (int)(__brev((uns
 // ---------------------------------------------------------------------------
 template <int L>
 struct SwzC {  // SwzAddr with a compile-time shift
+  static constexpr bool kXorLinear = true;  // addr(a ^ b) == addr(a) ^ addr(b)
   static constexpr int sh = L >= 8 ? L - 4 : 31;
   __device__ __forceinline__ int operator()(int i, int) const { return i ^ (((i >> 4) ^ (i >> sh)) & 15); }
 };
@@ -175,6 +177,15 @@ template <int PLOG>
 struct TileC {
   __device__ __forceinline__ int operator()(int i, int p) const { return (i << PLOG) + p; }
 };
+
+// Element address of base + m*H.  The pass's base never shares a bit with
+// m*H (base = k + multiples of H << R, k < H), so for an XOR-linear layout
+// the address is addr(base) ^ addr(m*H) with the second term a compile-time
+// constant: one LOP3 per access instead of the full swizzle.
+template <class Addr, class = void>
+struct XorLinear : std::false_type {};
+template <class Addr>
+struct XorLinear<Addr, std::void_t<decltype(Addr::kXorLinear)>> : std::bool_constant<Addr::kXorLinear> {};
 
 template <int R, bool INV, int L, int PLOG, int LOGH, int NTH, class Addr>
 __device__ __forceinline__ void dit_pass_ct(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
@@ -192,8 +203,13 @@ __device__ __forceinline__ void dit_pass_ct(float2* __restrict__ buf, const floa
     const int k = q & (H - 1);
     const int base = ((q >> LOGH) << (LOGH + R)) + k;
     float2 e[PR];
+    int ab = 0;
+    if constexpr (XorLinear<Addr>::value) ab = addr(base, p);
 #pragma unroll
-    for (int m = 0; m < PR; ++m) e[m] = buf[addr(base + m * H, p)];
+    for (int m = 0; m < PR; ++m) {
+      if constexpr (XorLinear<Addr>::value) e[m] = buf[ab ^ addr(m * H, 0)];
+      else e[m] = buf[addr(base + m * H, p)];
+    }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       float2 wi = __ldg(&tw[k << (kLogTwiddles - LOGH - i - 1)]);
@@ -211,7 +227,10 @@ __device__ __forceinline__ void dit_pass_ct(float2* __restrict__ buf, const floa
       }
     }
 #pragma unroll
-    for (int m = 0; m < PR; ++m) buf[addr(base + m * H, p)] = e[m];
+    for (int m = 0; m < PR; ++m) {
+      if constexpr (XorLinear<Addr>::value) buf[ab ^ addr(m * H, 0)] = e[m];
+      else buf[addr(base + m * H, p)] = e[m];
+    }
   }
 }
 

@@ -50,11 +50,17 @@ __device__ __forceinline__ float2 cospi_sinpi(float r) {
 // LOGT > 0: compile-time variant for T = 2^LOGT, n_over = 4T, upsample 1,
 // fused depth IFFT, NTH = T/4 threads (clamped to [64, 512]); LOGT = 0: all
 // sizes at run time.
+constexpr int ner_ct_threads(int logt) {
+  return logt <= 0 ? 512 : ((1 << logt) / 4 < 64 ? 64 : ((1 << logt) / 4 > 512 ? 512 : (1 << logt) / 4));
+}
+// keep <= 80 registers per thread (3 CTAs of 256 threads per SM at T = 1024)
+constexpr int ner_ct_minb(int logt) { return logt <= 0 ? 1 : (65536 / 80) / ner_ct_threads(logt); }
+
 template <int K2, int D, int LOGT>
-__global__ void __launch_bounds__(512) ner_kernel(const NerParams p) {
+__global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_kernel(const NerParams p) {
   constexpr bool CT = LOGT > 0;
   constexpr int CT_T = CT ? (1 << LOGT) : 1;
-  constexpr int CT_NTH = CT ? ((CT_T / 4) < 64 ? 64 : ((CT_T / 4) > 512 ? 512 : CT_T / 4)) : 1;
+  constexpr int CT_NTH = CT ? ner_ct_threads(LOGT) : 1;
   extern __shared__ float2 sbuf[];
   constexpr int K = K2 / 2;
   const int rl = blockIdx.x;         // local row of the input array
