@@ -28,6 +28,9 @@ namespace {
 using fft::SwzAddr;
 
 constexpr int kMaxTargetsPerThread = 8;
+#ifndef PATFFT_NER_INV_MAXR
+#define PATFFT_NER_INV_MAXR 4  // radix-16 depth IFFT passes: fewer shared-memory round trips beat idle threads
+#endif
 
 // (cos(pi r), sin(pi r)) for |r| <= 1, ~1e-8 absolute
 __device__ __forceinline__ float2 cospi_sinpi(float r) {
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_k
     }
     }
     __syncthreads();
-    if constexpr (CT) fft::fft_ct<true, LOGT, (CT_NTH * 4 >= CT_T ? 2 : 4), true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT>());
+    if constexpr (CT) fft::fft_ct<true, LOGT, PATFFT_NER_INV_MAXR, true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT>());
     else fft::fft_inplace<true, 4, true>(sbuf, Lu, 0, p.tw, tid, nth, iad);
     // output row d, depth i lives at z[((i / tco) * rows_out + d) * tco + i % tco]
     const int tco = p.out_tchunk;
