@@ -187,6 +187,32 @@ struct XorLinear : std::false_type {};
 template <class Addr>
 struct XorLinear<Addr, std::void_t<decltype(Addr::kXorLinear)>> : std::bool_constant<Addr::kXorLinear> {};
 
+// Radix-2^R DIT butterflies of one pass item (stages LOGH+1 .. LOGH+R),
+// item offset k within the current half-length 2^LOGH.
+template <int R, bool INV, int LOGH>
+__device__ __forceinline__ void pass_butterflies(float2 (&e)[1 << R], int k, const float2* __restrict__ tw) {
+  constexpr int PR = 1 << R;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    float2 wi = make_float2(1.f, 0.f);
+    if constexpr (LOGH > 0) {
+      wi = __ldg(&tw[k << (kLogTwiddles - LOGH - i - 1)]);  // W_{H 2^{i+1}}^k
+      if (INV) wi.y = -wi.y;
+    }
+#pragma unroll
+    for (int r = 0; r < (1 << i); ++r) {
+      const float2 t = (r == 0) ? wi : (LOGH > 0 ? cmul(wi, w32<INV>(r << (4 - i))) : w32<INV>(r << (4 - i)));
+#pragma unroll
+      for (int m0 = 0; m0 < PR; m0 += (2 << i)) {
+        const int m = m0 + r;
+        const float2 x = (LOGH == 0 && r == 0) ? e[m + (1 << i)] : cmul(e[m + (1 << i)], t);
+        e[m + (1 << i)] = csub(e[m], x);
+        e[m] = cadd(e[m], x);
+      }
+    }
+  }
+}
+
 template <int R, bool INV, int L, int PLOG, int LOGH, int NTH, class Addr>
 __device__ __forceinline__ void dit_pass_ct(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
                                             Addr addr) {
@@ -210,22 +236,7 @@ __device__ __forceinline__ void dit_pass_ct(float2* __restrict__ buf, const floa
       if constexpr (XorLinear<Addr>::value) e[m] = buf[ab ^ addr(m * H, 0)];
       else e[m] = buf[addr(base + m * H, p)];
     }
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      float2 wi = __ldg(&tw[k << (kLogTwiddles - LOGH - i - 1)]);
-      if (INV) wi.y = -wi.y;
-#pragma unroll
-      for (int r = 0; r < (1 << i); ++r) {
-        const float2 t = (r == 0) ? wi : cmul(wi, w32<INV>(r << (4 - i)));
-#pragma unroll
-        for (int m0 = 0; m0 < PR; m0 += (2 << i)) {
-          const int m = m0 + r;
-          const float2 x = cmul(e[m + (1 << i)], t);
-          e[m + (1 << i)] = csub(e[m], x);
-          e[m] = cadd(e[m], x);
-        }
-      }
-    }
+    pass_butterflies<R, INV, LOGH>(e, k, tw);
 #pragma unroll
     for (int m = 0; m < PR; ++m) {
       if constexpr (XorLinear<Addr>::value) buf[ab ^ addr(m * H, 0)] = e[m];
@@ -250,6 +261,49 @@ __device__ __forceinline__ void fft_ct(float2* __restrict__ buf, const float2* _
     __syncthreads();
     fft_ct<INV, L, MAXR, EVEN, PLOG, NTH, LOGH + R>(buf, tw, tid, addr);
   }
+}
+
+constexpr int brev_c(int x, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((x >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+
+// Full compile-time transform whose first pass reads its inputs straight
+// from `load(n, p)` (element n in natural order of transform p) instead of
+// from a bit-reversed shared-memory copy: saves one shared-memory round trip.
+// With a single transform (PLOG = 0) item q is given to thread brev(q), so a
+// warp's loads are consecutive natural indices.  Ends with __syncthreads.
+template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, class Addr, class Load>
+__device__ __forceinline__ void fft_ct_loaded(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
+                                              Addr addr, Load load) {
+  constexpr int R = PassRadix<L, MAXR, EVEN, 0>::value;
+  constexpr int PR = 1 << R;
+  constexpr int ITEMS = 1 << (L - R + PLOG);
+  constexpr int ITER = (ITEMS + NTH - 1) / NTH;
+#pragma unroll
+  for (int j = 0; j < ITER; ++j) {
+    const int it = tid + j * NTH;
+    if ((ITEMS % NTH) != 0 && it >= ITEMS) break;
+    const int p = it & ((1 << PLOG) - 1);
+    const int qi = it >> PLOG;
+    const int q = PLOG == 0 ? brev(qi, L - R) : qi;
+    const int nat0 = PLOG == 0 ? qi : brev(qi, L - R);  // natural index of element m = 0
+    float2 e[PR];
+#pragma unroll
+    for (int m = 0; m < PR; ++m) e[m] = load((brev_c(m, R) << (L - R)) + nat0, p);
+    pass_butterflies<R, INV, 0>(e, 0, tw);
+    const int base = q << R;
+    int ab = 0;
+    if constexpr (XorLinear<Addr>::value) ab = addr(base, p);
+#pragma unroll
+    for (int m = 0; m < PR; ++m) {
+      if constexpr (XorLinear<Addr>::value) buf[ab ^ addr(m, 0)] = e[m];
+      else buf[addr(base + m, p)] = e[m];
+    }
+  }
+  __syncthreads();
+  fft_ct<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
 }
 
 // staged_copy with compile-time sizes

@@ -42,17 +42,19 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
   const int T = p.T, n = p.ncols;
   const TileAddr ad{PLOG};
   const float* __restrict__ src = p.grid + (size_t)u0 * n * T;
-  fft::staged_copy<8, float2>(
-      n * P, tid, nth,
-      [&](int i) {
-        const int row = i >> PLOG, t = t0 + 2 * (i & (P - 1));
-        return (t < p.t_end) ? __ldcs(reinterpret_cast<const float2*>(src + (size_t)row * T + t))
-                             : make_float2(0.f, 0.f);
-      },
-      [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lcols), i & (P - 1))] = v; });
-  __syncthreads();
-  if constexpr (LC > 0) fft::fft_ct<false, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
-  else fft::fft_inplace<false, 4, false>(sm, p.lcols, PLOG, p.tw, tid, nth, ad);
+  auto ld = [&](int row, int q) {
+    const int t = t0 + 2 * q;
+    return (t < p.t_end) ? __ldcs(reinterpret_cast<const float2*>(src + (size_t)row * T + t)) : make_float2(0.f, 0.f);
+  };
+  if constexpr (LC > 0) {
+    fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
+  } else {
+    fft::staged_copy<8, float2>(
+        n * P, tid, nth, [&](int i) { return ld(i >> PLOG, i & (P - 1)); },
+        [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lcols), i & (P - 1))] = v; });
+    __syncthreads();
+    fft::fft_inplace<false, 4, false>(sm, p.lcols, PLOG, p.tw, tid, nth, ad);
+  }
   if (p.cplx) {
     // complex values (NedPlan): the packed pair IS one complex sample; keep
     // the full cropped spectrum j1 in [-N1/2, N1/2) in wrapped order
@@ -90,16 +92,19 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
   const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.T, nr = p.nrows;
   const TileAddr ad{PLOG};
-  fft::staged_copy<8, float2>(
-      nr * P, tid, nth,
-      [&](int i) {
-        const int row = i >> PLOG, t = t0 + (i & (P - 1));
-        return (t < p.t_end) ? __ldcs(p.Y + ((size_t)row * p.ny + j1) * T + t) : make_float2(0.f, 0.f);
-      },
-      [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lrows), i & (P - 1))] = v; });
-  __syncthreads();
-  if constexpr (LC > 0) fft::fft_ct<false, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
-  else fft::fft_inplace<false, 4, false>(sm, p.lrows, PLOG, p.tw, tid, nth, ad);
+  auto ld = [&](int row, int q) {
+    const int t = t0 + q;
+    return (t < p.t_end) ? __ldcs(p.Y + ((size_t)row * p.ny + j1) * T + t) : make_float2(0.f, 0.f);
+  };
+  if constexpr (LC > 0) {
+    fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
+  } else {
+    fft::staged_copy<8, float2>(
+        nr * P, tid, nth, [&](int i) { return ld(i >> PLOG, i & (P - 1)); },
+        [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.lrows), i & (P - 1))] = v; });
+    __syncthreads();
+    fft::fft_inplace<false, 4, false>(sm, p.lrows, PLOG, p.tw, tid, nth, ad);
+  }
   const int N0 = p.N0, mask = nr - 1;
   const float dp1 = p.dp1[j1];
   if (p.cplx) {
@@ -150,16 +155,19 @@ __global__ void __launch_bounds__(512, 2) inv_col_kernel(const LateralParams p) 
   const int T = p.Tu, n = p.N0u;
   const TileAddr ad{PLOG};
   float2* __restrict__ z = p.z;
-  fft::staged_copy<8, float2>(
-      n * P, tid, nth,
-      [&](int i) {
-        const int row = i >> PLOG, t = t0 + (i & (P - 1));
-        return (t < T) ? z[((size_t)row * p.N1uh + j1) * T + t] : make_float2(0.f, 0.f);
-      },
-      [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.l0u), i & (P - 1))] = v; });
-  __syncthreads();
-  if constexpr (LC > 0) fft::fft_ct<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
-  else fft::fft_inplace<true, 4, false>(sm, p.l0u, PLOG, p.tw, tid, nth, ad);
+  auto ld = [&](int row, int q) {
+    const int t = t0 + q;
+    return (t < T) ? z[((size_t)row * p.N1uh + j1) * T + t] : make_float2(0.f, 0.f);
+  };
+  if constexpr (LC > 0) {
+    fft::fft_ct_loaded<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
+  } else {
+    fft::staged_copy<8, float2>(
+        n * P, tid, nth, [&](int i) { return ld(i >> PLOG, i & (P - 1)); },
+        [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.l0u), i & (P - 1))] = v; });
+    __syncthreads();
+    fft::fft_inplace<true, 4, false>(sm, p.l0u, PLOG, p.tw, tid, nth, ad);
+  }
   for (int i = tid; i < n * P; i += nth) {
     const int row = i >> PLOG, q = i & (P - 1);
     const int t = t0 + q;

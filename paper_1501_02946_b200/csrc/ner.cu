@@ -100,9 +100,8 @@ __global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_k
   };
   auto store_brev = [&](int m, float2 v) { sbuf[ad(fft::brev(m, L), 0)] = v; };
   if constexpr (CT) {
-    fft::staged_copy_ct<8, 4 * CT_T, CT_NTH, float2>(tid, load_ext, store_brev);
-    __syncthreads();
-    fft::fft_ct<false, LOGT + 2, 4, true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT + 2>());
+    fft::fft_ct_loaded<false, LOGT + 2, 4, true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT + 2>(),
+                                                          [&](int m, int) { return load_ext(m); });
   } else {
     fft::staged_copy<8, float2>(n, tid, nth, load_ext, store_brev);
     __syncthreads();
