@@ -306,6 +306,92 @@ __device__ __forceinline__ void fft_ct_loaded(float2* __restrict__ buf, const fl
   fft_ct<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
 }
 
+// Last pass that hands its outputs (natural order) to `store(n, p, v)`
+// instead of writing them back to shared memory.  No trailing barrier.
+template <int R, bool INV, int L, int PLOG, int LOGH, int NTH, class Addr, class Store>
+__device__ __forceinline__ void dit_pass_ct_st(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
+                                               Addr addr, Store store) {
+  constexpr int PR = 1 << R;
+  constexpr int H = 1 << LOGH;
+  constexpr int ITEMS = 1 << (L - R + PLOG);
+  constexpr int ITER = (ITEMS + NTH - 1) / NTH;
+#pragma unroll
+  for (int j = 0; j < ITER; ++j) {
+    const int it = tid + j * NTH;
+    if ((ITEMS % NTH) != 0 && it >= ITEMS) break;
+    const int p = it & ((1 << PLOG) - 1);
+    const int q = it >> PLOG;
+    const int k = q & (H - 1);
+    const int base = ((q >> LOGH) << (LOGH + R)) + k;
+    float2 e[PR];
+    int ab = 0;
+    if constexpr (XorLinear<Addr>::value) ab = addr(base, p);
+#pragma unroll
+    for (int m = 0; m < PR; ++m) {
+      if constexpr (XorLinear<Addr>::value) e[m] = buf[ab ^ addr(m * H, 0)];
+      else e[m] = buf[addr(base + m * H, p)];
+    }
+    pass_butterflies<R, INV, LOGH>(e, k, tw);
+#pragma unroll
+    for (int m = 0; m < PR; ++m) store(base + m * H, p, e[m]);
+  }
+}
+
+// Passes LOGH.. of a compile-time transform, the last one storing through `store`.
+template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, int LOGH, class Addr, class Store>
+__device__ __forceinline__ void fft_ct_tail_store(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
+                                                  Addr addr, Store store) {
+  constexpr int R = PassRadix<L, MAXR, EVEN, LOGH>::value;
+  if constexpr (LOGH + R >= L) {
+    dit_pass_ct_st<R, INV, L, PLOG, LOGH, NTH>(buf, tw, tid, addr, store);
+  } else {
+    dit_pass_ct<R, INV, L, PLOG, LOGH, NTH>(buf, tw, tid, addr);
+    __syncthreads();
+    fft_ct_tail_store<INV, L, MAXR, EVEN, PLOG, NTH, LOGH + R>(buf, tw, tid, addr, store);
+  }
+}
+
+// Whole transform from shared memory (bit-reversed input) to `store`.
+template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, class Addr, class Store>
+__device__ __forceinline__ void fft_ct_stored(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
+                                              Addr addr, Store store) {
+  fft_ct_tail_store<INV, L, MAXR, EVEN, PLOG, NTH, 0>(buf, tw, tid, addr, store);
+}
+
+// Whole transform from `load` (natural order) to `store`; needs >= 2 passes.
+template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, class Addr, class Load, class Store>
+__device__ __forceinline__ void fft_ct_loaded_stored(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
+                                                     Addr addr, Load load, Store store) {
+  constexpr int R = PassRadix<L, MAXR, EVEN, 0>::value;
+  static_assert(R < L, "single-pass transform: use fft_ct_loaded");
+  constexpr int PR = 1 << R;
+  constexpr int ITEMS = 1 << (L - R + PLOG);
+  constexpr int ITER = (ITEMS + NTH - 1) / NTH;
+#pragma unroll
+  for (int j = 0; j < ITER; ++j) {
+    const int it = tid + j * NTH;
+    if ((ITEMS % NTH) != 0 && it >= ITEMS) break;
+    const int p = it & ((1 << PLOG) - 1);
+    const int qi = it >> PLOG;
+    const int q = PLOG == 0 ? brev(qi, L - R) : qi;
+    const int nat0 = PLOG == 0 ? qi : brev(qi, L - R);
+    float2 e[PR];
+#pragma unroll
+    for (int m = 0; m < PR; ++m) e[m] = load((brev_c(m, R) << (L - R)) + nat0, p);
+    pass_butterflies<R, INV, 0>(e, 0, tw);
+    const int base = q << R;
+    int ab = 0;
+    if constexpr (XorLinear<Addr>::value) ab = addr(base, p);
+#pragma unroll
+    for (int m = 0; m < PR; ++m) {
+      if constexpr (XorLinear<Addr>::value) buf[ab ^ addr(m, 0)] = e[m];
+      else buf[addr(base + m, p)] = e[m];
+    }
+  }
+  __syncthreads();
+  fft_ct_tail_store<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr, store);
+}
+
 // staged_copy with compile-time sizes
 template <int B, int TOTAL, int NTH, class V, class Load, class Store>
 __device__ __forceinline__ void staged_copy_ct(int tid, Load load, Store store) {

@@ -25,6 +25,13 @@ namespace {
 
 using fft::TileAddr;
 
+#ifndef PATFFT_C2R_LOADED
+#define PATFFT_C2R_LOADED 1
+#endif
+#ifndef PATFFT_INVCOL_STORED
+#define PATFFT_INVCOL_STORED 1
+#endif
+
 constexpr int nth_for(int L, int PLOG) {
   return ((L >= 4 ? (1 << (L - 4)) : 1) << PLOG) < 64 ? 64
          : (((L >= 4 ? (1 << (L - 4)) : 1) << PLOG) > 512 ? 512 : ((L >= 4 ? (1 << (L - 4)) : 1) << PLOG));
@@ -159,19 +166,23 @@ __global__ void __launch_bounds__(512, 2) inv_col_kernel(const LateralParams p) 
     const int t = t0 + q;
     return (t < T) ? z[((size_t)row * p.N1uh + j1) * T + t] : make_float2(0.f, 0.f);
   };
-  if constexpr (LC > 0) {
+  auto st = [&](int row, int q, float2 v) {
+    const int t = t0 + q;
+    if (t < T) z[((size_t)row * p.N1uh + j1) * T + t] = v;
+  };
+  if constexpr (LC > 4 && PATFFT_INVCOL_STORED) {
+    fft::fft_ct_loaded_stored<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld, st);
+  } else if constexpr (LC > 0) {
     fft::fft_ct_loaded<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
+    for (int i = tid; i < n * P; i += nth) st(i >> PLOG, i & (P - 1), sm[ad(i >> PLOG, i & (P - 1))]);
   } else {
     fft::staged_copy<8, float2>(
         n * P, tid, nth, [&](int i) { return ld(i >> PLOG, i & (P - 1)); },
         [&](int i, float2 v) { sm[ad(fft::brev(i >> PLOG, p.l0u), i & (P - 1))] = v; });
     __syncthreads();
-    fft::fft_inplace<true, 4, false>(sm, p.l0u, PLOG, p.tw, tid, nth, ad);
-  }
-  for (int i = tid; i < n * P; i += nth) {
-    const int row = i >> PLOG, q = i & (P - 1);
-    const int t = t0 + q;
-    if (t < T) z[((size_t)row * p.N1uh + j1) * T + t] = sm[ad(row, q)];
+    if constexpr (LC > 0) fft::fft_ct<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
+    else fft::fft_inplace<true, 4, false>(sm, p.l0u, PLOG, p.tw, tid, nth, ad);
+    for (int i = tid; i < n * P; i += nth) st(i >> PLOG, i & (P - 1), sm[ad(i >> PLOG, i & (P - 1))]);
   }
 }
 
@@ -186,6 +197,32 @@ __global__ void __launch_bounds__(512, 2) inv_c2r_kernel(const LateralParams p) 
   const int T = p.Tu, n = p.N1u, half = n / 2;
   const TileAddr ad{PLOG};
   const float2* __restrict__ z = p.z + (size_t)n0 * p.N1uh * T;
+  float* __restrict__ out = p.out + (size_t)n0 * n * T;
+  auto st = [&](int row, int q, float2 v) {
+    const int t = t0 + 2 * q;
+    if (t < T) *reinterpret_cast<float2*>(out + (size_t)row * T + t) = v;
+  };
+  if constexpr (LC > 4 && PATFFT_C2R_LOADED) {
+    // element r of the packed transform Z = Xa + i Xb (Xa, Xb: the half
+    // spectra of time samples t, t+1): r <= n/2 from bin r, else from the
+    // conjugate of bin n - r (Z[n-k] = conj(Xa) + i conj(Xb)); each bin is
+    // read twice, the second time from L1
+    auto ld = [&](int r, int q) {
+      const int t = t0 + 2 * q;
+      const bool lo = r <= half;
+      const int k = lo ? r : n - r;
+      // unconditional (clamped) load so the compiler issues all of an item's loads back to back
+      float4 v = __ldg(reinterpret_cast<const float4*>(z + (size_t)k * T + min(t, T - 2)));
+      if (k == 0 || k == half) {  // C2R semantics: self-conjugate bins are real
+        v.y = 0.f;
+        v.w = 0.f;
+      }
+      const float2 o = lo ? make_float2(v.x - v.w, v.y + v.z) : make_float2(v.x + v.w, v.z - v.y);
+      return t < T ? o : make_float2(0.f, 0.f);
+    };
+    fft::fft_ct_loaded_stored<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld, st);
+    return;
+  }
   fft::staged_copy<8, float4>(
       (half + 1) * P, tid, nth,
       [&](int i) {
@@ -206,12 +243,7 @@ __global__ void __launch_bounds__(512, 2) inv_c2r_kernel(const LateralParams p) 
   __syncthreads();
   if constexpr (LC > 0) fft::fft_ct<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>());
   else fft::fft_inplace<true, 4, false>(sm, p.l1u, PLOG, p.tw, tid, nth, ad);
-  float* __restrict__ out = p.out + (size_t)n0 * n * T;
-  for (int i = tid; i < n * P; i += nth) {
-    const int row = i >> PLOG, q = i & (P - 1);
-    const int t = t0 + 2 * q;
-    if (t < T) *reinterpret_cast<float2*>(out + (size_t)row * T + t) = sm[ad(row, q)];
-  }
+  for (int i = tid; i < n * P; i += nth) st(i >> PLOG, i & (P - 1), sm[ad(i >> PLOG, i & (P - 1))]);
 }
 
 int tile_bytes() {

@@ -28,6 +28,9 @@ namespace {
 using fft::SwzAddr;
 
 constexpr int kMaxTargetsPerThread = 8;
+#ifndef PATFFT_NER_STORED
+#define PATFFT_NER_STORED 1
+#endif
 #ifndef PATFFT_NER_INV_MAXR
 #define PATFFT_NER_INV_MAXR 4  // radix-16 depth IFFT passes: fewer shared-memory round trips beat idle threads
 #endif
@@ -271,19 +274,24 @@ __global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_k
     }
     }
     __syncthreads();
-    if constexpr (CT) fft::fft_ct<true, LOGT, PATFFT_NER_INV_MAXR, true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT>());
-    else fft::fft_inplace<true, 4, true>(sbuf, Lu, 0, p.tw, tid, nth, iad);
     // output row d, depth i lives at z[((i / tco) * rows_out + d) * tco + i % tco]
     const int tco = p.out_tchunk;
     const size_t zstride = (size_t)p.rows_out * tco;
     float2* __restrict__ z0 = p.z + (size_t)(drow0 - p.out_row0) * tco;
     float2* __restrict__ z1 = p.z + (size_t)((drow1 >= 0 ? drow1 : drow0) - p.out_row0) * tco;
-#pragma unroll 4
-    for (int i = tid; i < Tu; i += nth) {
-      const float2 v = sbuf[iad(i, 0)];
+    auto st = [&](int i, int, float2 v) {
       const size_t o = (i >> p.out_tshift) * zstride + (i & p.out_tmask);
       z0[o] = v;
       if (drow1 >= 0) z1[o] = v;
+    };
+    if constexpr (CT && PATFFT_NER_STORED) {
+      // the last IFFT pass writes the z row straight to global memory
+      fft::fft_ct_stored<true, LOGT, PATFFT_NER_INV_MAXR, true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT>(), st);
+    } else {
+      if constexpr (CT) fft::fft_ct<true, LOGT, PATFFT_NER_INV_MAXR, true, 0, CT_NTH>(sbuf, p.tw, tid, fft::SwzC<LOGT>());
+      else fft::fft_inplace<true, 4, true>(sbuf, Lu, 0, p.tw, tid, nth, iad);
+#pragma unroll 4
+      for (int i = tid; i < Tu; i += nth) st(i, 0, sbuf[iad(i, 0)]);
     }
   } else {
     // spectrum only; z was zero-filled and a batched cuFFT does the depth IFFT
