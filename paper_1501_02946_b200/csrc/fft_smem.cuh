@@ -269,12 +269,54 @@ constexpr int brev_c(int x, int bits) {
   return r;
 }
 
+// log2(half-length) at which the last pass of the schedule starts
+template <int L, int MAXR, bool EVEN, int LOGH = 0>
+struct LastPassLogh {
+  static constexpr int R = PassRadix<L, MAXR, EVEN, LOGH>::value;
+  static constexpr int value = (LOGH + R >= L) ? LOGH : LastPassLogh<L, MAXR, EVEN, (LOGH + R >= L ? L : LOGH + R)>::value;
+};
+template <int L, int MAXR, bool EVEN>
+struct LastPassLogh<L, MAXR, EVEN, L> {
+  static constexpr int value = L;
+};
+
+// Passes LOGH.. of the schedule except the last one (each followed by a barrier).
+template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, int LOGH, class Addr>
+__device__ __forceinline__ void fft_ct_but_last(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
+                                                Addr addr) {
+  constexpr int R = PassRadix<L, MAXR, EVEN, LOGH>::value;
+  if constexpr (LOGH + R < L) {
+    dit_pass_ct<R, INV, L, PLOG, LOGH, NTH>(buf, tw, tid, addr);
+    __syncthreads();
+    fft_ct_but_last<INV, L, MAXR, EVEN, PLOG, NTH, LOGH + R>(buf, tw, tid, addr);
+  }
+}
+
+// Output `idx` (natural order) of a transform whose last radix-2^RL pass
+// (half-length H = 2^(L-RL)) has not been run: the pass's inputs are the
+// H-point DFTs D_r of the decimated sequences x[r + 2^RL s], stored in block
+// brev(r) of the buffer, and Z[idx] = sum_r W_{2^L}^{idx r} D_r[idx mod H].
+template <bool INV, int L, int RL, class Addr>
+__device__ __forceinline__ float2 last_pass_output(const float2* __restrict__ buf, const float2* __restrict__ tw,
+                                                   Addr addr, int idx, int p) {
+  constexpr int H = 1 << (L - RL);
+  const int s = idx & (H - 1);
+  float2 acc = buf[addr(s, p)];
+#pragma unroll
+  for (int r = 1; r < (1 << RL); ++r) {
+    float2 w = __ldg(&tw[((idx * r) & ((1 << L) - 1)) << (kLogTwiddles - L)]);
+    if (INV) w.y = -w.y;
+    acc = cadd(acc, cmul(buf[addr(brev_c(r, RL) * H + s, p)], w));
+  }
+  return acc;
+}
+
 // Full compile-time transform whose first pass reads its inputs straight
 // from `load(n, p)` (element n in natural order of transform p) instead of
 // from a bit-reversed shared-memory copy: saves one shared-memory round trip.
 // With a single transform (PLOG = 0) item q is given to thread brev(q), so a
 // warp's loads are consecutive natural indices.  Ends with __syncthreads.
-template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, class Addr, class Load>
+template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, bool SKIP_LAST = false, class Addr, class Load>
 __device__ __forceinline__ void fft_ct_loaded(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
                                               Addr addr, Load load) {
   constexpr int R = PassRadix<L, MAXR, EVEN, 0>::value;
@@ -303,7 +345,8 @@ __device__ __forceinline__ void fft_ct_loaded(float2* __restrict__ buf, const fl
     }
   }
   __syncthreads();
-  fft_ct<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
+  if constexpr (SKIP_LAST) fft_ct_but_last<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
+  else fft_ct<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
 }
 
 // Last pass that hands its outputs (natural order) to `store(n, p, v)`

@@ -28,6 +28,12 @@ using fft::TileAddr;
 #ifndef PATFFT_C2R_LOADED
 #define PATFFT_C2R_LOADED 1
 #endif
+#ifndef PATFFT_LAT_FUSED
+#define PATFFT_LAT_FUSED 1  // colfft/rowfft: last FFT pass evaluated inside the crop/unpack epilogue
+#endif
+#ifndef PATFFT_ROW_FUSED
+#define PATFFT_ROW_FUSED 0  // measured slower for rowfft (half the outputs are cropped away anyway)
+#endif
 #ifndef PATFFT_INVCOL_STORED
 #define PATFFT_INVCOL_STORED 1
 #endif
@@ -53,8 +59,10 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
     const int t = t0 + 2 * q;
     return (t < p.t_end) ? __ldcs(reinterpret_cast<const float2*>(src + (size_t)row * T + t)) : make_float2(0.f, 0.f);
   };
+  constexpr int LLAST = LC > 0 ? fft::LastPassLogh<(LC > 0 ? LC : 1), 4, false>::value : 0;
+  constexpr bool FUSED = PATFFT_LAT_FUSED && LC > 0 && LLAST > 0;
   if constexpr (LC > 0) {
-    fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
+    fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
   } else {
     fft::staged_copy<8, float2>(
         n * P, tid, nth, [&](int i) { return ld(i >> PLOG, i & (P - 1)); },
@@ -62,6 +70,12 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
     __syncthreads();
     fft::fft_inplace<false, 4, false>(sm, p.lcols, PLOG, p.tw, tid, nth, ad);
   }
+  // spectrum value at column frequency k (the last pass folded in when FUSED)
+  auto zat = [&](int k, int q) {
+    if constexpr (FUSED) return fft::last_pass_output<false, (LC > 0 ? LC : 1), (LC > 0 ? LC : 1) - LLAST>(
+        sm, p.tw, fft::TileC<PLOG>(), k, q);
+    else return sm[ad(k, q)];
+  };
   if (p.cplx) {
     // complex values (NedPlan): the packed pair IS one complex sample; keep
     // the full cropped spectrum j1 in [-N1/2, N1/2) in wrapped order
@@ -72,7 +86,7 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
       const int t = t0 + 2 * q;
       if (t >= p.t_end) continue;
       const int j1 = k < p.N1 / 2 ? k : k - p.N1;
-      dst[(size_t)k * Tc + t / 2] = sm[ad(j1 & (n - 1), q)];
+      dst[(size_t)k * Tc + t / 2] = zat(j1 & (n - 1), q);
     }
     return;
   }
@@ -81,8 +95,8 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
     const int k = i >> PLOG, q = i & (P - 1);
     const int t = t0 + 2 * q;
     if (t >= p.t_end) continue;
-    const float2 zk = sm[ad(k, q)];
-    const float2 zm = fft::conjf2(sm[ad((n - k) & (n - 1), q)]);
+    const float2 zk = zat(k, q);
+    const float2 zm = fft::conjf2(zat((n - k) & (n - 1), q));
     const float2 d = fft::csub(zk, zm);
     const float4 o = make_float4(0.5f * (zk.x + zm.x), 0.5f * (zk.y + zm.y), 0.5f * d.y, -0.5f * d.x);
     *reinterpret_cast<float4*>(dst + (size_t)k * T + t) = o;
@@ -103,8 +117,10 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
     const int t = t0 + q;
     return (t < p.t_end) ? __ldcs(p.Y + ((size_t)row * p.ny + j1) * T + t) : make_float2(0.f, 0.f);
   };
+  constexpr int LLAST = LC > 0 ? fft::LastPassLogh<(LC > 0 ? LC : 1), 4, false>::value : 0;
+  constexpr bool FUSED = PATFFT_ROW_FUSED && LC > 0 && LLAST > 0;
   if constexpr (LC > 0) {
-    fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
+    fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
   } else {
     fft::staged_copy<8, float2>(
         nr * P, tid, nth, [&](int i) { return ld(i >> PLOG, i & (P - 1)); },
@@ -112,6 +128,11 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
     __syncthreads();
     fft::fft_inplace<false, 4, false>(sm, p.lrows, PLOG, p.tw, tid, nth, ad);
   }
+  auto zat = [&](int k, int q) {
+    if constexpr (FUSED) return fft::last_pass_output<false, (LC > 0 ? LC : 1), (LC > 0 ? LC : 1) - LLAST>(
+        sm, p.tw, fft::TileC<PLOG>(), k, q);
+    else return sm[ad(k, q)];
+  };
   const int N0 = p.N0, mask = nr - 1;
   const float dp1 = p.dp1[j1];
   if (p.cplx) {
@@ -124,7 +145,7 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
       if (t >= p.t_end) continue;
       const int a = (N0 > 1) ? (j0w < N0 / 2 ? j0w : j0w - N0) : 0;
       const float sg = ((a + j1s) & 1) ? -1.f : 1.f;
-      const float2 v = fft::cscale(sm[ad(a & mask, q)], sg * p.dp0[j0w] * dp1);
+      const float2 v = fft::cscale(zat(a & mask, q), sg * p.dp0[j0w] * dp1);
       const size_t o = p.centered ? (size_t)(a + N0 / 2) * p.ny + (j1s + p.N1 / 2) : (size_t)j0w * p.ny + j1;
       p.gh[o * T + t] = v;
     }
@@ -139,13 +160,13 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
     const bool nyq0 = (N0 > 1) && (a == -(N0 / 2));
     float2 v;
     if (nyq1) {  // stored j1 = N1/2 is signed -N1/2: X(a,-N1/2) = conj X(-a,+N1/2)
-      const float2 v1 = fft::conjf2(sm[ad((-a) & mask, q)]);
-      const float2 v2 = sm[ad((nyq0 ? -a : a) & mask, q)];
+      const float2 v1 = fft::conjf2(zat((-a) & mask, q));
+      const float2 v2 = zat((nyq0 ? -a : a) & mask, q);
       v = fft::cscale(fft::cadd(v1, v2), 0.5f);
     } else if (nyq0) {
-      v = fft::cscale(fft::cadd(sm[ad(a & mask, q)], sm[ad((-a) & mask, q)]), 0.5f);
+      v = fft::cscale(fft::cadd(zat(a & mask, q), zat((-a) & mask, q)), 0.5f);
     } else {
-      v = sm[ad(a & mask, q)];
+      v = zat(a & mask, q);
     }
     p.gh[((size_t)j0w * p.ny + j1) * T + t] = fft::cscale(v, p.dp0[j0w] * dp1);
   }
