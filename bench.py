@@ -430,7 +430,7 @@ def run_gpu_arm(args):
             e2e_s = float(t.item())
         e2e = {"value": vox * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * nsamp,
                "d2h_bytes_per_step": 8 * nout, "ms_per_step": 1e3 * e2e_s,
-               "path": "patfft_nedner_execute (C ABI): pinned f64 host -> device -> pinned f64 host"}
+               "path": "patfft_nedner_execute (C ABI): pinned f64 host -> device (8 time chunks, H2D overlapped with spread + lateral FFTs) -> pinned f64 host"}
         lib.patfft_host_free(hin)
         lib.patfft_host_free(hout)
 

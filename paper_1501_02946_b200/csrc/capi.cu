@@ -542,6 +542,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   CUDA_TRY(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
   if (const char* e = std::getenv("PATFFT_OVERLAP_CHUNKS")) P->overlap_chunks = std::max(1, std::min(4, std::atoi(e)));
   if (const char* e = std::getenv("PATFFT_GRAPHS")) P->use_graphs = std::atoi(e) != 0;
+  if (const char* e = std::getenv("PATFFT_H2D_CHUNKS")) P->h2d_chunks = std::max(1, std::atoi(e));
   {
     int lo = 0, hi = 0;
     CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -958,6 +959,7 @@ int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* 
   if (!P || !samples || !image) return fail(PATFFT_ERR_PARAMETER, "null argument");
   std::lock_guard<std::mutex> lk(P->mu);
   CUDA_TRY(cudaSetDevice(P->device));
+  if (P->world != 1) return fail(PATFFT_ERR_PARAMETER, "sharded plan: use the patfft_nedner_shard_* stages");
   const size_t in_n = (size_t)P->M * P->T, out_n = (size_t)P->N0u * P->N1u * P->Tu;
   int rc;
   if (!P->d_samples && (rc = dalloc(&P->d_samples, in_n))) return rc;
@@ -965,9 +967,74 @@ int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* 
   if (!P->d_out && (rc = dalloc(&P->d_out, out_n))) return rc;
   if (!P->d_out64 && (rc = dalloc(&P->d_out64, out_n))) return rc;
   cudaStream_t st = P->stream;
-  CUDA_TRY(cudaMemcpyAsync(P->d_samples64, samples, in_n * sizeof(double), cudaMemcpyHostToDevice, st));
-  CUDA_TRY(launch_f64_to_f32(P->d_samples64, P->d_samples, in_n, st));
-  if ((rc = execute_graphed(P, 1, P->d_samples, P->d_out, st))) return rc;
+  // Time-chunked upload: the H2D of chunk k+1 (copy engine, second stream)
+  // overlaps the conversion, spread and lateral FFTs of chunk k, which only
+  // need the samples of their own time range.  The NER and the inverse need
+  // every time sample and follow the last chunk.
+  const int T = P->T;
+  int nc = (P->mode == 0 && !P->profiling) ? std::max(1, std::min(P->h2d_chunks, T / 128)) : 1;
+  nc = std::min(nc, (int)patfft_nedner_plan::kMaxH2dChunks);
+  if (nc > 1 && !P->copy_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : P->ev_h2d) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (nc == 1) {
+    CUDA_TRY(cudaMemcpyAsync(P->d_samples64, samples, in_n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(launch_f64_to_f32(P->d_samples64, P->d_samples, in_n, st));
+    if ((rc = execute_graphed(P, 1, P->d_samples, P->d_out, st))) return rc;
+  } else {
+    const int chunk = ((T + nc - 1) / nc + 127) / 128 * 128;
+    CUDA_TRY(cudaEventRecord(P->ev_fork, st));  // the device buffers are free (previous call finished on st)
+    CUDA_TRY(cudaStreamWaitEvent(P->copy_stream, P->ev_fork, 0));
+    int used = 0;
+    for (int k = 0; k < nc; ++k) {
+      const int tb = k * chunk, te = std::min(T, tb + chunk);
+      if (tb >= te) break;
+      CUDA_TRY(cudaMemcpy2DAsync(P->d_samples64 + tb, (size_t)T * sizeof(double), samples + tb,
+                                 (size_t)T * sizeof(double), (size_t)(te - tb) * sizeof(double), (size_t)P->M,
+                                 cudaMemcpyHostToDevice, P->copy_stream));
+      CUDA_TRY(cudaEventRecord(P->ev_h2d[k], P->copy_stream));
+      used = k + 1;
+    }
+    SpreadParams sp;
+    sp.samples = P->d_samples;
+    sp.recs = P->d_recs;
+    sp.blk = P->d_blk;
+    sp.blk_grp = P->d_blkgrp;
+    sp.grid = P->d_grid;
+    sp.T = T;
+    sp.ncols = P->ncols;
+    sp.nrows = P->nrows;
+    LateralParams L = P->lat;
+    L.gh = P->d_gh;
+    for (int k = 0; k < used; ++k) {
+      const int tb = k * chunk, te = std::min(T, tb + chunk);
+      CUDA_TRY(cudaStreamWaitEvent(st, P->ev_h2d[k], 0));
+      CUDA_TRY(launch_f64_to_f32_cols(P->d_samples64, P->d_samples, P->M, T, tb, te, st));
+      sp.t_begin = L.t_begin = tb;
+      sp.t_end = L.t_end = te;
+      CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
+      CUDA_TRY(launch_lateral_col(L, st));
+      CUDA_TRY(launch_lateral_row(L, st));
+    }
+    L.t_begin = 0;
+    L.t_end = T;
+    L.out = P->d_out;
+    if (P->up > 1 || !P->fused_ifft)
+      CUDA_TRY(cudaMemsetAsync(P->d_z, 0, sizeof(float2) * (size_t)P->N0u * P->N1uh * P->Tu, st));
+    CUDA_TRY(launch_ner(P->ner, P->K2, P->poly_degree, st));
+    if (!P->fused_ifft) {
+      CUFFT_TRY(cufftSetStream(P->fft_l, st));
+      CUFFT_TRY(cufftExecC2C(P->fft_l, reinterpret_cast<cufftComplex*>(P->d_z), reinterpret_cast<cufftComplex*>(P->d_z),
+                             CUFFT_INVERSE));
+    }
+    if (P->custom_inverse) {
+      CUDA_TRY(launch_lateral_inverse(L, st));
+    } else {
+      CUFFT_TRY(cufftSetStream(P->fft_c2r, st));
+      CUFFT_TRY(cufftExecC2R(P->fft_c2r, reinterpret_cast<cufftComplex*>(P->d_z), P->d_out));
+    }
+  }
   CUDA_TRY(launch_f32_to_f64(P->d_out, P->d_out64, out_n, st));
   CUDA_TRY(cudaMemcpyAsync(image, P->d_out64, out_n * sizeof(double), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -994,6 +1061,12 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
     if (e) cudaEventDestroy(e);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_join) cudaEventDestroy(P->ev_join);
+  if (P->copy_stream) {
+    cudaStreamSynchronize(P->copy_stream);
+    for (auto& e : P->ev_h2d)
+      if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(P->copy_stream);
+  }
   if (P->stream2) cudaStreamDestroy(P->stream2);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;

@@ -102,6 +102,7 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s);
 size_t ner_smem_bytes(int n_over, int Tu);
 int ner_threads(int n_over);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);
+cudaError_t launch_f64_to_f32_cols(const double* src, float* dst, int M, int T, int tb, int te, cudaStream_t s);
 cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s);
 cudaError_t launch_fill(float* dst, size_t n, float v, cudaStream_t s);
 cudaError_t launch_gather_rows(const float* samples, const int* gidx, float* grid, int M, int T, cudaStream_t s);
@@ -116,6 +117,11 @@ struct patfft_nedner_plan {
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // lateral FFTs overlapped with the spread
   cudaEvent_t ev_chunk[4] = {}, ev_fork = nullptr, ev_join = nullptr;
+  // host-buffer path: H2D of time chunk k on copy_stream, compute waits ev_h2d[k]
+  static constexpr int kMaxH2dChunks = 16;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_h2d[kMaxH2dChunks] = {};
+  int h2d_chunks = 8;
   int overlap_chunks = 1;  // time chunks of the overlapped forward stages (1 = off)
   // CUDA graph of the last executed (samples, image, frames) triple
   bool use_graphs = true;

@@ -14,6 +14,17 @@ __global__ void f32_to_f64_kernel(const float* __restrict__ s, double* __restric
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     d[i] = (double)s[i];
 }
+// columns [tb, te) of an M x T row-major array
+__global__ void f64_to_f32_cols_kernel(const double* __restrict__ s, float* __restrict__ d, int M, int T, int tb,
+                                       int te) {
+  const int w = te - tb;
+  const size_t n = (size_t)M * w;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / w);
+    const size_t o = (size_t)m * T + tb + (int)(i - (size_t)m * w);
+    d[o] = (float)__ldcs(&s[o]);
+  }
+}
 __global__ void fill_kernel(float* __restrict__ d, size_t n, float v) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     d[i] = v;
@@ -34,6 +45,11 @@ unsigned grid_for(size_t n) {
   return (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 }  // namespace
+
+cudaError_t launch_f64_to_f32_cols(const double* src, float* dst, int M, int T, int tb, int te, cudaStream_t s) {
+  f64_to_f32_cols_kernel<<<grid_for((size_t)M * (te - tb)), 256, 0, s>>>(src, dst, M, T, tb, te);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s) {
   f64_to_f32_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n);
