@@ -987,15 +987,18 @@ int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* 
     CUDA_TRY(cudaEventRecord(P->ev_fork, st));  // the device buffers are free (previous call finished on st)
     CUDA_TRY(cudaStreamWaitEvent(P->copy_stream, P->ev_fork, 0));
     int used = 0;
-    for (int k = 0; k < nc; ++k) {
+    while (used < nc && used * chunk < T) ++used;
+    // (issued one chunk ahead of the compute: with pageable host memory the
+    // copy call itself blocks, and the GPU still works on the previous chunk)
+    auto upload = [&](int k) -> int {
       const int tb = k * chunk, te = std::min(T, tb + chunk);
-      if (tb >= te) break;
       CUDA_TRY(cudaMemcpy2DAsync(P->d_samples64 + tb, (size_t)T * sizeof(double), samples + tb,
                                  (size_t)T * sizeof(double), (size_t)(te - tb) * sizeof(double), (size_t)P->M,
                                  cudaMemcpyHostToDevice, P->copy_stream));
       CUDA_TRY(cudaEventRecord(P->ev_h2d[k], P->copy_stream));
-      used = k + 1;
-    }
+      return PATFFT_OK;
+    };
+    if ((rc = upload(0))) return rc;
     SpreadParams sp;
     sp.samples = P->d_samples;
     sp.recs = P->d_recs;
@@ -1009,6 +1012,7 @@ int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* 
     L.gh = P->d_gh;
     for (int k = 0; k < used; ++k) {
       const int tb = k * chunk, te = std::min(T, tb + chunk);
+      if (k + 1 < used && (rc = upload(k + 1))) return rc;
       CUDA_TRY(cudaStreamWaitEvent(st, P->ev_h2d[k], 0));
       CUDA_TRY(launch_f64_to_f32_cols(P->d_samples64, P->d_samples, P->M, T, tb, te, st));
       sp.t_begin = L.t_begin = tb;

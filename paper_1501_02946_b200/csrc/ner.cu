@@ -129,22 +129,21 @@ __global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_k
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       // tap j (dk = j-K+1) and its mirror K2-1-j share one polynomial:
-      // w_j = E(z^2) + z O(z^2), w_mirror = E(z^2) - z O(z^2)
-      float e = p.poly[j][D], o = p.poly[j][D - 1];
-      if (D % 2) {
-        e = p.poly[j][D - 1];
-        o = p.poly[j][D];
-      }
+      // w_j = E(z^2) + z O(z^2), w_mirror = E(z^2) - z O(z^2); the E and O
+      // Horner chains run side by side in packed FP32 lanes
+      constexpr int DE = D % 2 ? D - 1 : D;  // top even / odd degrees
+      constexpr int DO = D % 2 ? D : D - 1;
+      float2 eo = make_float2(p.poly[j][DE], p.poly[j][DO]);
 #pragma unroll
-      for (int d = (D % 2 ? D - 3 : D - 2); d >= 0; d -= 2) e = fmaf(e, z2, p.poly[j][d]);
+      for (int s2 = 1; s2 <= DO / 2; ++s2)
+        eo = fft::f2fma(eo, make_float2(z2, z2), make_float2(p.poly[j][DE - 2 * s2], p.poly[j][DO - 2 * s2]));
 #pragma unroll
-      for (int d = (D % 2 ? D - 2 : D - 3); d >= 1; d -= 2) o = fmaf(o, z2, p.poly[j][d]);
-      const float wa = fmaf(z, o, e);
-      const float wb = fmaf(-z, o, e);
+      for (int d = DE - 2 * (DO / 2) - 2; d >= 0; d -= 2) eo.x = fmaf(eo.x, z2, p.poly[j][d]);
+      const float wa = fmaf(z, eo.y, eo.x);
+      const float wb = fmaf(-z, eo.y, eo.x);
       const float2 Fa = sbuf[gad((k0 + j - K + 1) & (n - 1), 0)];
       const float2 Fb = sbuf[gad((k0 + K - j) & (n - 1), 0)];
-      acc.x = fmaf(wa, Fa.x, fmaf(wb, Fb.x, acc.x));
-      acc.y = fmaf(wa, Fa.y, fmaf(wb, Fb.y, acc.y));
+      acc = fft::f2fma(Fa, make_float2(wa, wa), fft::f2fma(Fb, make_float2(wb, wb), acc));
     }
     return acc;
   };
