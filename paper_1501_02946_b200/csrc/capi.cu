@@ -335,7 +335,8 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   const int M = P->M, K2 = P->K2, nrows = P->nrows, ncols = P->ncols, T = P->Tr;
   const int Tfull = P->T;
   const int R = spread_rows_per_group(d->n_lat, K2);
-  const int RECW = spread_record_words(K2);
+  const int RECW = spread_record_words(K2, R);
+  const bool tpair = spread_time_pairs(R);
   P->R = R;
   P->ngroups = (nrows + R - 1) / R;
   const int Mrec = (mode == 0 || mode == 3) ? M : 0;  // the equispaced modes gather instead of spreading
@@ -353,7 +354,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   }
   struct Rec {
     int grp, ws, m;
-    float wr[4];
+    double wr[4];
   };
   std::vector<Rec> recs;
   recs.reserve((size_t)M * ((d->n_lat == 2 ? (K2 + R - 1) / R + 1 : 1)) + 64);
@@ -385,7 +386,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
           rc.grp = g.first;
           rc.ws = (int)(ws0 + s * ncols);
           rc.m = m;
-          for (int r = 0; r < 4; ++r) rc.wr[r] = (float)g.second[r];
+          for (int r = 0; r < 4; ++r) rc.wr[r] = g.second[r];
           recs.push_back(rc);
         }
     }
@@ -399,8 +400,16 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     float* o = &recbuf[i * RECW];
     std::memcpy(&o[0], &recs[i].ws, 4);
     std::memcpy(&o[1], &recs[i].m, 4);
-    for (int r = 0; r < 4; ++r) o[4 + r] = recs[i].wr[r];
-    for (int j = 0; j < K2; ++j) o[8 + (int)pmod(recs[i].ws + j, K2)] = (float)wcolv[(size_t)recs[i].m * K2 + j];
+    if (tpair) {  // [4 + slot*R + r] = wr[r] * wc[tap]
+      for (int j = 0; j < K2; ++j) {
+        const int slot = (int)pmod(recs[i].ws + j, K2);
+        const double wc = wcolv[(size_t)recs[i].m * K2 + j];
+        for (int r = 0; r < R; ++r) o[4 + slot * R + r] = (float)(recs[i].wr[r] * wc);
+      }
+    } else {
+      for (int r = 0; r < 4; ++r) o[4 + r] = (float)recs[i].wr[r];
+      for (int j = 0; j < K2; ++j) o[8 + (int)pmod(recs[i].ws + j, K2)] = (float)wcolv[(size_t)recs[i].m * K2 + j];
+    }
   }
   std::vector<int64_t> gstart(P->ngroups + 1, 0);
   for (const Rec& r : recs) gstart[r.grp + 1]++;
@@ -412,12 +421,12 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   std::vector<int4> blk;   // {lo, hi, c0, c1}
   std::vector<int> blk_grp;
   {
-    const int64_t tch = spread_time_chunks(T);
+    const int64_t tch = spread_time_chunks(T, R);
     static const int waves = [] {
       const char* e = std::getenv("PATFFT_SPREAD_WAVES");
-      return e ? std::max(1, std::atoi(e)) : 4;
+      return e ? std::max(1, std::atoi(e)) : 2;
     }();
-    const int64_t target_blocks = 148LL * spread_ctas_per_sm() * waves;
+    const int64_t target_blocks = 148LL * spread_ctas_per_sm(R) * waves;
     const int64_t per_chunk = std::max<int64_t>(1, ceildiv(target_blocks, tch));
     const int64_t nrec_all = std::max<int64_t>(1, (int64_t)recs.size());
     const double rec_per_block = std::max(64.0, (double)nrec_all / (double)per_chunk);

@@ -92,9 +92,10 @@ struct NerParams {
 // Kernel launchers
 cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaStream_t s);
 int spread_rows_per_group(int n_lat, int K2);
-int spread_record_words(int K2);
-int spread_ctas_per_sm();
-int spread_time_chunks(int T);
+int spread_record_words(int K2, int R);
+int spread_ctas_per_sm(int R);
+bool spread_time_pairs(int R);
+int spread_time_chunks(int T, int R);
 cudaError_t launch_lateral_col(const LateralParams& p, cudaStream_t s);
 cudaError_t launch_lateral_row(const LateralParams& p, cudaStream_t s);
 cudaError_t launch_lateral_inverse(const LateralParams& p, cudaStream_t s);

@@ -37,6 +37,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -255,6 +259,221 @@ __global__ void __launch_bounds__(kThreads, PATFFT_SPREAD_MINB) spread_kernel(co
 all_done:;
 }
 
+// ---------------------------------------------------------------------------
+// Time-pair variant (default for 2-D sensor planes): R = 2 grid rows per
+// group and TWO consecutive time samples per thread.  FFMA2 lanes are the
+// time pair, the broadcast operand is the precomputed weight product
+// wr[r] * wc[j], so one record costs 2K*R FFMA2 with no per-record FMUL and a
+// single LDS.64 for the samples; the thinner row groups waste fewer FMAs on
+// rows outside a sensor's window ((2K+1)/2K vs (2K+3)/2K for R = 4).
+// Record layout (float words): [0] ws, [1] m, [2..3] pad, [4 + j*R + r]
+// weight of ring slot j (column (ws + tap) mod NS = j) and group row r.
+// ---------------------------------------------------------------------------
+#ifndef PATFFT_SPREAD_TP_MINB
+#define PATFFT_SPREAD_TP_MINB 5
+#endif
+#ifndef PATFFT_SPREAD_TP_CHUNK
+#define PATFFT_SPREAD_TP_CHUNK 16
+#endif
+constexpr int kChunkTP = PATFFT_SPREAD_TP_CHUNK;
+constexpr int kTimeTP = 2 * kThreads;  // time samples per CTA
+
+template <int NS, int R>
+__device__ __forceinline__ void record_fma_tp(float2 (&acc)[NS][R], const float* __restrict__ rec, float2 s2) {
+  const float4* wq = reinterpret_cast<const float4*>(rec + 4);
+#pragma unroll
+  for (int j4 = 0; j4 < (NS * R + 3) / 4; ++j4) {
+    const float4 q = wq[j4];
+    const float wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = j4 * 4 + u;
+      if (idx < NS * R) {
+        const int j = idx < NS * R ? idx / R : 0, r = idx < NS * R ? idx % R : 0;
+        acc[j][r] = ffma2(s2, make_float2(wv[u], wv[u]), acc[j][r]);
+      }
+    }
+  }
+}
+
+template <int Q, int R, int NS, bool TEVEN>
+__device__ __forceinline__ void flush_slot_tp(float2 (&acc)[NS][R], float* __restrict__ colp, size_t row_stride,
+                                              int rows_valid, bool store, bool t1valid) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (store && r < rows_valid) {
+      float* d = colp + (size_t)r * row_stride;
+      if (TEVEN) {
+        *reinterpret_cast<float2*>(d) = acc[Q][r];
+      } else {
+        d[0] = acc[Q][r].x;
+        if (t1valid) d[1] = acc[Q][r].y;
+      }
+    }
+    acc[Q][r] = make_float2(0.f, 0.f);
+  }
+}
+
+template <int K2, int R, int PIECE>
+__global__ void __launch_bounds__(kThreads, PATFFT_SPREAD_TP_MINB) spread_tp_kernel(const SpreadParams p) {
+  constexpr int NS = K2;
+  constexpr int RECW = 4 + (NS * R + 3) / 4 * 4;
+  constexpr int CH = kChunkTP;
+  constexpr int PIECES = kTimeTP / PIECE;  // cp.async pieces per record
+  constexpr int PER_THREAD = CH * PIECES / kThreads;
+  constexpr bool TEVEN = PIECE >= 2;       // T even: aligned float2 samples and stores
+  static_assert(NS <= 16, "ring states are generated for up to 16 slots");
+  static_assert((CH * PIECES) % kThreads == 0, "staging split");
+  extern __shared__ float4 smem4[];
+  float* rbuf = reinterpret_cast<float*>(smem4);  // [2][CH][RECW]
+  float* sbuf = rbuf + 2 * CH * RECW;             // [2][CH][kTimeTP]
+
+  const int4 bk = p.blk[blockIdx.x];
+  const int grp = p.blk_grp[blockIdx.x];
+  const int c0 = bk.z;
+  const int c1 = bk.w;
+  const int T = p.T;
+  const int t0 = p.t_begin + blockIdx.y * kTimeTP;
+  const int tid = threadIdx.x;
+  const int t = t0 + 2 * tid;
+  const bool tvalid = t < p.t_end;
+  const bool t1valid = t + 1 < p.t_end;
+  const int nrec = bk.y - bk.x;
+  const int nchunks = (nrec + CH - 1) / CH;
+  const int row0 = grp * R;
+  const int rows_valid = min(R, p.nrows - row0);
+
+  int mnext[PER_THREAD];  // sensor of each (record, piece) this thread stages
+  auto load_m = [&](int c) {
+#pragma unroll
+    for (int i = 0; i < PER_THREAD; ++i) {
+      const int flat = tid + i * kThreads;  // (record, piece) pair index within the chunk
+      const int e = c * CH + flat / PIECES;
+      mnext[i] = (e < nrec) ? __ldg(reinterpret_cast<const int*>(p.recs) + (size_t)(bk.x + e) * RECW + 1) : -1;
+    }
+  };
+  auto stage = [&](int c, int b) {
+    const int e0 = c * CH;
+    const int ne = min(CH, nrec - e0);
+    const float4* srcr = reinterpret_cast<const float4*>(p.recs + (size_t)(bk.x + e0) * RECW);
+    float4* dstr = reinterpret_cast<float4*>(rbuf + b * CH * RECW);
+    for (int i = tid; i < ne * RECW / 4; i += kThreads) cp_async16(dstr + i, srcr + i, 16);
+    float* sb = sbuf + b * CH * kTimeTP;
+#pragma unroll
+    for (int i = 0; i < PER_THREAD; ++i) {
+      const int flat = tid + i * kThreads;
+      const int e = flat / PIECES, pc = flat % PIECES;
+      const int m = mnext[i];
+      if (m >= 0) {
+        const int tp = t0 + pc * PIECE;
+        const int nb = max(0, min(PIECE, p.t_end - tp)) * 4;
+        float* dst = sb + e * kTimeTP + pc * PIECE;
+        const float* src = p.samples + (size_t)m * T + (nb > 0 ? tp : 0);
+        if (PIECE == 4) cp_async16(dst, src, nb);
+        else if (PIECE == 2) cp_async8(dst, src, nb);
+        else cp_async4(dst, src, nb);
+      }
+    }
+    cp_commit();
+  };
+
+  float2 acc[NS][R];
+#pragma unroll
+  for (int j = 0; j < NS; ++j)
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[j][r] = make_float2(0.f, 0.f);
+
+  const size_t row_stride = (size_t)p.ncols * T;
+  float* base = p.grid + (size_t)row0 * row_stride + (tvalid ? t : 0);
+  int fg = (c0 - NS) >= 0 ? (c0 - NS) / NS * NS : -((NS - (c0 - NS) - 1) / NS) * NS;
+  int fs = 0;
+
+  if (nchunks > 0) {
+    load_m(0);
+    stage(0, 0);
+    load_m(1);
+  }
+  const int npass = max(nchunks, 1);
+  for (int c = 0; c < npass; ++c) {
+    const int b = c & 1;
+    int ne = 0;
+    if (c < nchunks) {
+      if (c + 1 < nchunks) {
+        stage(c + 1, b ^ 1);
+        load_m(c + 2);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      __syncthreads();
+      ne = min(CH, nrec - c * CH);
+    }
+    const bool last = c + 1 >= npass;
+    const float* rb = rbuf + b * CH * RECW;
+    const float* sb = sbuf + b * CH * kTimeTP + 2 * tid;
+    int e = 0;
+    switch (fs) {
+      case 0: goto st_0;   case 1: goto st_1;   case 2: goto st_2;   case 3: goto st_3;
+      case 4: goto st_4;   case 5: goto st_5;   case 6: goto st_6;   case 7: goto st_7;
+      case 8: goto st_8;   case 9: goto st_9;   case 10: goto st_10; case 11: goto st_11;
+      case 12: goto st_12; case 13: goto st_13; case 14: goto st_14; default: goto st_15;
+    }
+#define PATFFT_STATE_TP(q, qn)                                                                       \
+  st_##q:                                                                                            \
+    if (q < NS) {                                                                                    \
+      while (e < ne) {                                                                               \
+        const float* rec = rb + e * RECW;                                                            \
+        if (__float_as_int(rec[0]) != fg) break;                                                     \
+        float2 s2;                                                                                   \
+        if (TEVEN) s2 = *reinterpret_cast<const float2*>(sb + e * kTimeTP);                          \
+        else s2 = make_float2(sb[e * kTimeTP], sb[e * kTimeTP + 1]);                                 \
+        record_fma_tp<NS, R>(acc, rec, s2);                                                          \
+        ++e;                                                                                         \
+      }                                                                                              \
+      if (e == ne) {                                                                                 \
+        if (!last) {                                                                                 \
+          fs = q;                                                                                    \
+          goto chunk_end;                                                                            \
+        }                                                                                            \
+        if (fg >= c1) goto all_done;                                                                 \
+      }                                                                                              \
+      {                                                                                              \
+        const bool store = tvalid && fg >= c0 && fg < c1;                                            \
+        flush_slot_tp<(q < NS ? q : 0), R, NS, TEVEN>(acc, base + (size_t)(store ? fg : 0) * T,      \
+                                                      row_stride, rows_valid, store, t1valid);       \
+      }                                                                                              \
+      ++fg;                                                                                          \
+      if (q + 1 >= NS) goto st_0;                                                                    \
+      goto st_##qn;                                                                                  \
+    }
+    PATFFT_STATE_TP(0, 1) PATFFT_STATE_TP(1, 2) PATFFT_STATE_TP(2, 3) PATFFT_STATE_TP(3, 4)
+    PATFFT_STATE_TP(4, 5) PATFFT_STATE_TP(5, 6) PATFFT_STATE_TP(6, 7) PATFFT_STATE_TP(7, 8)
+    PATFFT_STATE_TP(8, 9) PATFFT_STATE_TP(9, 10) PATFFT_STATE_TP(10, 11) PATFFT_STATE_TP(11, 12)
+    PATFFT_STATE_TP(12, 13) PATFFT_STATE_TP(13, 14) PATFFT_STATE_TP(14, 15) PATFFT_STATE_TP(15, 0)
+#undef PATFFT_STATE_TP
+  chunk_end:
+    __syncthreads();
+  }
+all_done:;
+}
+
+template <int K2, int R>
+cudaError_t go_tp(const SpreadParams& p, int nblk, cudaStream_t s) {
+  constexpr int RECW = 4 + (K2 * R + 3) / 4 * 4;
+  const size_t smem = sizeof(float) * 2 * kChunkTP * (RECW + kTimeTP);
+  dim3 grid((unsigned)nblk, (unsigned)((p.t_end - p.t_begin + kTimeTP - 1) / kTimeTP));
+  cudaError_t err;
+  auto run = [&](auto k) {
+    if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return;
+    k<<<grid, kThreads, smem, s>>>(p);
+    err = cudaGetLastError();
+  };
+  if (p.T % 4 == 0) run(spread_tp_kernel<K2, R, 4>);
+  else if (p.T % 2 == 0) run(spread_tp_kernel<K2, R, 2>);
+  else run(spread_tp_kernel<K2, R, 1>);
+  return err;
+}
+
 template <int K2, int R>
 cudaError_t go(const SpreadParams& p, int nblk, cudaStream_t s) {
   constexpr int RECW = 8 + (K2 + 3) / 4 * 4;
@@ -282,15 +501,48 @@ int spread_rows_per_group(int n_lat, int K2) {
   }();
   (void)K2;
   if (n_lat == 1) return 1;
-  if (forced == 2 || forced == 4) return forced;
-  return 4;
+  if (forced == 1 || forced == 2 || forced == 4) return forced;
+  return 2;
+}
+// R <= 2: the time-pair kernel (set PATFFT_SPREAD_TP=0 for the one-sample kernel)
+bool spread_time_pairs(int R) {
+  static const bool on = [] {
+    const char* e = std::getenv("PATFFT_SPREAD_TP");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on && R <= 2;
 }
 int spread_ring(int K2) { return K2; }
-int spread_ctas_per_sm() { return PATFFT_SPREAD_MINB; }
-int spread_record_words(int K2) { return 8 + (K2 + 3) / 4 * 4; }
-int spread_time_chunks(int T) { return (T + kThreads - 1) / kThreads; }
+int spread_ctas_per_sm(int R) { return spread_time_pairs(R) ? PATFFT_SPREAD_TP_MINB : PATFFT_SPREAD_MINB; }
+int spread_record_words(int K2, int R) {
+  return spread_time_pairs(R) ? 4 + (K2 * R + 3) / 4 * 4 : 8 + (K2 + 3) / 4 * 4;
+}
+int spread_time_chunks(int T, int R) {
+  const int tb = spread_time_pairs(R) ? kTimeTP : kThreads;
+  return (T + tb - 1) / tb;
+}
 
 cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaStream_t s) {
+  if (spread_time_pairs(R)) {
+#define PATFFT_SPREAD_TPK(RR)                       \
+    switch (K2) {                                   \
+      case 2: return go_tp<2, RR>(p, nblk, s);      \
+      case 4: return go_tp<4, RR>(p, nblk, s);      \
+      case 6: return go_tp<6, RR>(p, nblk, s);      \
+      case 8: return go_tp<8, RR>(p, nblk, s);      \
+      case 10: return go_tp<10, RR>(p, nblk, s);    \
+      case 12: return go_tp<12, RR>(p, nblk, s);    \
+      case 14: return go_tp<14, RR>(p, nblk, s);    \
+      case 16: return go_tp<16, RR>(p, nblk, s);    \
+    }
+    if (R == 2) {
+      PATFFT_SPREAD_TPK(2)
+    } else {
+      PATFFT_SPREAD_TPK(1)
+    }
+#undef PATFFT_SPREAD_TPK
+    return cudaErrorInvalidValue;
+  }
 #define PATFFT_SPREAD_K(RR)                         \
   switch (K2) {                                     \
     case 2: return go<2, RR>(p, nblk, s);           \
