@@ -41,6 +41,31 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
 }
+// --- bulk (TMA) copies completing on an mbarrier -------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra WAIT;\n"
+      "DONE:\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -272,6 +297,9 @@ all_done:;
 #ifndef PATFFT_SPREAD_TP_MINB
 #define PATFFT_SPREAD_TP_MINB 5
 #endif
+#ifndef PATFFT_SPREAD_BULK
+#define PATFFT_SPREAD_BULK 1
+#endif
 #ifndef PATFFT_SPREAD_TP_CHUNK
 #define PATFFT_SPREAD_TP_CHUNK 16
 #endif
@@ -322,11 +350,18 @@ __global__ void __launch_bounds__(kThreads, PATFFT_SPREAD_TP_MINB) spread_tp_ker
   constexpr int PIECES = kTimeTP / PIECE;  // cp.async pieces per record
   constexpr int PER_THREAD = CH * PIECES / kThreads;
   constexpr bool TEVEN = PIECE >= 2;       // T even: aligned float2 samples and stores
+  // T % 4 == 0: records and each record's sample row arrive as bulk (TMA)
+  // copies issued by one warp and completing on mbarriers -- no per-thread
+  // cp.async address work
+  constexpr bool BULK = PIECE == 4 && PATFFT_SPREAD_BULK;
+  constexpr int NRB = BULK ? 3 : 2;        // record buffers (bulk: two chunks ahead)
   static_assert(NS <= 16, "ring states are generated for up to 16 slots");
   static_assert((CH * PIECES) % kThreads == 0, "staging split");
+  static_assert(CH <= 32, "one lane per record in the bulk issue");
   extern __shared__ float4 smem4[];
-  float* rbuf = reinterpret_cast<float*>(smem4);  // [2][CH][RECW]
-  float* sbuf = rbuf + 2 * CH * RECW;             // [2][CH][kTimeTP]
+  float* rbuf = reinterpret_cast<float*>(smem4);  // [NRB][CH][RECW]
+  float* sbuf = rbuf + NRB * CH * RECW;           // [2][CH][kTimeTP]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sbuf + 2 * CH * kTimeTP);  // [NRB] records, [2] samples
 
   const int4 bk = p.blk[blockIdx.x];
   const int grp = p.blk_grp[blockIdx.x];
@@ -388,7 +423,40 @@ __global__ void __launch_bounds__(kThreads, PATFFT_SPREAD_TP_MINB) spread_tp_ker
   int fg = (c0 - NS) >= 0 ? (c0 - NS) / NS * NS : -((NS - (c0 - NS) - 1) / NS) * NS;
   int fs = 0;
 
-  if (nchunks > 0) {
+  const int nvalid = min(kTimeTP, p.t_end - t0);  // time samples of this block
+  // bulk issue (warp 0): records of chunk cc into record buffer cc % NRB
+  auto issue_recs = [&](int cc) {
+    const int ne = min(CH, nrec - cc * CH);
+    uint64_t* bar = mbar + (cc % NRB);
+    mbar_expect_tx(bar, (unsigned)(ne * RECW * 4));
+    bulk_g2s(rbuf + (cc % NRB) * CH * RECW, p.recs + (size_t)(bk.x + cc * CH) * RECW, (unsigned)(ne * RECW * 4), bar);
+  };
+  // samples of chunk cc (its records must have landed): lane e copies record e's row
+  auto issue_smp = [&](int cc, int lane) {
+    const int ne = min(CH, nrec - cc * CH);
+    uint64_t* bar = mbar + NRB + (cc & 1);
+    if (lane == 0) mbar_expect_tx(bar, (unsigned)(ne * nvalid * 4));
+    __syncwarp();
+    if (lane < ne) {
+      const int m = __float_as_int(rbuf[((cc % NRB) * CH + lane) * RECW + 1]);
+      bulk_g2s(sbuf + ((cc & 1) * CH + lane) * kTimeTP, p.samples + (size_t)m * T + t0, (unsigned)(nvalid * 4), bar);
+    }
+  };
+  if constexpr (BULK) {
+    if (tid == 0) {
+      for (int i = 0; i < NRB + 2; ++i) mbar_init(mbar + i, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (tid < 32 && nchunks > 0) {
+      if (tid == 0) {
+        issue_recs(0);
+        if (nchunks > 1) issue_recs(1);
+      }
+      mbar_wait(mbar + 0, 0);
+      issue_smp(0, tid);
+    }
+  } else if (nchunks > 0) {
     load_m(0);
     stage(0, 0);
     load_m(1);
@@ -398,18 +466,30 @@ __global__ void __launch_bounds__(kThreads, PATFFT_SPREAD_TP_MINB) spread_tp_ker
     const int b = c & 1;
     int ne = 0;
     if (c < nchunks) {
-      if (c + 1 < nchunks) {
-        stage(c + 1, b ^ 1);
-        load_m(c + 2);
-        cp_wait<1>();
+      if constexpr (BULK) {
+        if (tid < 32) {
+          if (tid == 0 && c + 2 < nchunks) issue_recs(c + 2);
+          if (c + 1 < nchunks) {
+            mbar_wait(mbar + (c + 1) % NRB, (unsigned)(((c + 1) / NRB) & 1));
+            issue_smp(c + 1, tid);
+          }
+        }
+        mbar_wait(mbar + c % NRB, (unsigned)((c / NRB) & 1));
+        mbar_wait(mbar + NRB + b, (unsigned)((c >> 1) & 1));
       } else {
-        cp_wait<0>();
+        if (c + 1 < nchunks) {
+          stage(c + 1, b ^ 1);
+          load_m(c + 2);
+          cp_wait<1>();
+        } else {
+          cp_wait<0>();
+        }
+        __syncthreads();
       }
-      __syncthreads();
       ne = min(CH, nrec - c * CH);
     }
     const bool last = c + 1 >= npass;
-    const float* rb = rbuf + b * CH * RECW;
+    const float* rb = rbuf + (BULK ? c % NRB : b) * CH * RECW;
     const float* sb = sbuf + b * CH * kTimeTP + 2 * tid;
     int e = 0;
     switch (fs) {
@@ -460,7 +540,7 @@ all_done:;
 template <int K2, int R>
 cudaError_t go_tp(const SpreadParams& p, int nblk, cudaStream_t s) {
   constexpr int RECW = 4 + (K2 * R + 3) / 4 * 4;
-  const size_t smem = sizeof(float) * 2 * kChunkTP * (RECW + kTimeTP);
+  const size_t smem = sizeof(float) * (3 * kChunkTP * RECW + 2 * kChunkTP * kTimeTP) + 8 * sizeof(uint64_t);
   dim3 grid((unsigned)nblk, (unsigned)((p.t_end - p.t_begin + kTimeTP - 1) / kTimeTP));
   cudaError_t err;
   auto run = [&](auto k) {
