@@ -822,7 +822,8 @@ static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* 
   sp.nrows = P->nrows;
   LateralParams L = P->lat;
   L.gh = gh;
-  const int nc = (overlap && P->mode == 0) ? std::max(1, std::min(P->overlap_chunks, T / 128)) : 1;
+  const int tgran = (1 << 20) / spread_time_chunks(1 << 20, P->R);  // spread CTA time block
+  const int nc = (overlap && P->mode == 0) ? std::max(1, std::min(P->overlap_chunks, T / tgran)) : 1;
   if (nc == 1) {
     sp.t_begin = L.t_begin = 0;
     sp.t_end = L.t_end = T;
@@ -835,7 +836,7 @@ static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* 
     if (prof) CUDA_TRY(cudaEventRecord(P->ev[3], st));
     return PATFFT_OK;
   }
-  const int chunk = ((T + nc - 1) / nc + 127) / 128 * 128;
+  const int chunk = ((T + nc - 1) / nc + tgran - 1) / tgran * tgran;
   CUDA_TRY(cudaEventRecord(P->ev_fork, st));
   CUDA_TRY(cudaStreamWaitEvent(P->stream2, P->ev_fork, 0));
   int used = 0;
@@ -981,7 +982,9 @@ int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* 
   // need the samples of their own time range.  The NER and the inverse need
   // every time sample and follow the last chunk.
   const int T = P->T;
-  int nc = (P->mode == 0 && !P->profiling) ? std::max(1, std::min(P->h2d_chunks, T / 128)) : 1;
+  // chunks are whole spread CTA time blocks (256 samples for the time-pair kernel)
+  const int tgran = (1 << 20) / spread_time_chunks(1 << 20, P->R);
+  int nc = (P->mode == 0 && !P->profiling) ? std::max(1, std::min(P->h2d_chunks, T / tgran)) : 1;
   nc = std::min(nc, (int)patfft_nedner_plan::kMaxH2dChunks);
   if (nc > 1 && !P->copy_stream) {
     CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
@@ -992,7 +995,7 @@ int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* 
     CUDA_TRY(launch_f64_to_f32(P->d_samples64, P->d_samples, in_n, st));
     if ((rc = execute_graphed(P, 1, P->d_samples, P->d_out, st))) return rc;
   } else {
-    const int chunk = ((T + nc - 1) / nc + 127) / 128 * 128;
+    const int chunk = ((T + nc - 1) / nc + tgran - 1) / tgran * tgran;
     CUDA_TRY(cudaEventRecord(P->ev_fork, st));  // the device buffers are free (previous call finished on st)
     CUDA_TRY(cudaStreamWaitEvent(P->copy_stream, P->ev_fork, 0));
     int used = 0;
