@@ -429,12 +429,13 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     const int64_t target_blocks = 148LL * spread_ctas_per_sm(R) * waves;
     const int64_t per_chunk = std::max<int64_t>(1, ceildiv(target_blocks, tch));
     const int64_t nrec_all = std::max<int64_t>(1, (int64_t)recs.size());
-    const double rec_per_block = std::max(64.0, (double)nrec_all / (double)per_chunk);
+    // (2-D: a single row group, so the column segments are all the parallelism there is)
+    const double rec_per_block = std::max(d->n_lat == 1 ? 8.0 : 64.0, (double)nrec_all / (double)per_chunk);
     for (int g = 0; g < P->ngroups; ++g) {
       auto b = recs.begin() + gstart[g], e = recs.begin() + gstart[g + 1];
       const int64_t ng = e - b;
       int nseg = (int)std::max<int64_t>(1, std::llround(ng / rec_per_block));
-      nseg = std::min(nseg, std::max(1, ncols / 16));
+      nseg = std::min(nseg, std::max(1, ncols / (d->n_lat == 1 ? 8 : 16)));
       std::vector<int> cuts{0};
       for (int s = 1; s < nseg; ++s) {
         const int64_t idx = ng * s / nseg;

@@ -584,13 +584,15 @@ int spread_rows_per_group(int n_lat, int K2) {
   if (forced == 1 || forced == 2 || forced == 4) return forced;
   return 2;
 }
-// R <= 2: the time-pair kernel (set PATFFT_SPREAD_TP=0 for the one-sample kernel)
+// R == 2: the time-pair kernel (set PATFFT_SPREAD_TP=0 for the one-sample
+// kernel).  2-D sensor lines (R = 1) keep the one-sample kernel: their grids
+// are small and need the finer time blocks for parallelism.
 bool spread_time_pairs(int R) {
   static const bool on = [] {
     const char* e = std::getenv("PATFFT_SPREAD_TP");
     return e ? std::atoi(e) != 0 : true;
   }();
-  return on && R <= 2;
+  return on && R == 2;
 }
 int spread_ring(int K2) { return K2; }
 int spread_ctas_per_sm(int R) { return spread_time_pairs(R) ? PATFFT_SPREAD_TP_MINB : PATFFT_SPREAD_MINB; }
