@@ -159,6 +159,31 @@ int patfft_nedner_shard_forward(patfft_nedner_plan* plan, const float* samples_s
 int patfft_nedner_shard_ner(patfft_nedner_plan* plan, const void* gh_recv, void* z_send, void* stream);
 int patfft_nedner_shard_inverse(patfft_nedner_plan* plan, const void* z_recv, float* image_slice, void* stream);
 
+/* ---- forward model: the reference's forward_fourier (forward.py:105-166) --
+ * Full-grid sensor traces of an initial pressure field on an
+ * (N0, N1, N_t) or (N, N_t) grid (time/depth fastest, dt = dz / c):
+ * lateral FFT of the field (cuFFT R2C), per lateral frequency row the NER
+ * transform at +-ky = +-sqrt(w^2 - |j|^2) on the doubled window with the
+ * w/(2 ky) Jacobian and the propagating mask (sm_100a kernel, depth inverse
+ * FFT in shared memory), lateral inverse (cuFFT C2R).  The ifftshift of the
+ * field and the fftshift of the traces (forward.py:124,157) cancel for even
+ * sizes and are both omitted.
+ *   n_lateral : n_lat lateral sizes, even (forward.py:118-119)
+ *   n_time    : N_t, a power of two <= 4096 on the GPU
+ *   j2        : N0*N1 float64, _lateral_freq_sq(n_lateral, ratios) on the
+ *               wrapped grid (recon.py:200-215, forward.py:141-143)
+ *   c, K, alpha, beta : WindowSpec of the NerPlan(N_t, spec) (forward.py:151) */
+typedef struct patfft_forward_plan patfft_forward_plan;
+int patfft_forward_plan_create(int n_lat, const int32_t* n_lateral, int n_time, const double* j2, double c, int K,
+                               double alpha, double beta, int device, patfft_forward_plan** out);
+/* field: N0*N1*N_t float64 host; traces: N0*N1*N_t float64 host, one row of
+ * N_t samples per grid node in C order (forward.py:158-166). */
+int patfft_forward_execute(patfft_forward_plan* plan, const double* field, double* traces);
+/* Device-resident float32 variant; field and traces may alias.  Enqueues on
+ * `stream` (NULL = the plan's stream) without synchronising. */
+int patfft_forward_execute_device(patfft_forward_plan* plan, const float* field_dev, float* traces_dev, void* stream);
+void patfft_forward_plan_destroy(patfft_forward_plan* plan);
+
 /* Per-stage device timing (CUDA events on the plan's stream).  When enabled
  * every execute records one event per stage boundary; patfft_nedner_stage_times
  * returns the accumulated milliseconds per stage and the launch count per

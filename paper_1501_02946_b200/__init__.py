@@ -19,6 +19,7 @@ from .recon import (
     reconstruct_nedner,
 )
 from .nufft import NedPlan, NerPlan, nufft_ned, nufft_ner
+from .forward import ForwardPlan, forward_fourier
 from .window import WindowSpec
 
 __version__ = "0.1.0"
@@ -29,6 +30,7 @@ __all__ = [
     "NumericalError",
     "ParameterError",
     "EquispacedPlan",
+    "ForwardPlan",
     "NedNerPlan",
     "NedPlan",
     "NerPlan",
@@ -36,6 +38,7 @@ __all__ = [
     "SensorRecord",
     "WindowSpec",
     "amplitude_factor",
+    "forward_fourier",
     "nufft_ned",
     "nufft_ner",
     "kappa",

@@ -68,6 +68,12 @@ _SIGS = {
                                               ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_double, _D,
                                               ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
     "patfft_ned_execute": (ctypes.c_int, [_P, _P, _P, ctypes.c_int]),
+    "patfft_forward_plan_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_int, _D,
+                                                  ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                                  ctypes.c_int, ctypes.POINTER(_P)]),
+    "patfft_forward_execute": (ctypes.c_int, [_P, _P, _P]),
+    "patfft_forward_execute_device": (ctypes.c_int, [_P, _P, _P, _P]),
+    "patfft_forward_plan_destroy": (None, [_P]),
     "patfft_nedner_set_profiling": (ctypes.c_int, [_P, ctypes.c_int]),
     "patfft_nedner_stage_times": (ctypes.c_int, [_P, _D, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
     "patfft_nedner_stage_name": (ctypes.c_char_p, [ctypes.c_int]),

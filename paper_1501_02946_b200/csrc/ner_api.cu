@@ -103,6 +103,95 @@ __global__ void c64_to_c128(const float2* __restrict__ s, double2* __restrict__ 
     d[i] = make_double2(s[i].x, s[i].y);
 }
 
+
+// ---------------------------------------------------------------------------
+// Forward model (the reference's forward_fourier, forward.py:105-166): per
+// lateral half-spectrum row j, the detected depth spectrum
+//   ghat(j, w) = w / (2 ky) * [fh(j, +ky) + fh(j, -ky)],  ky = sqrt(w^2 - |j|^2)
+// on the doubled window (2 N_t frequencies w = k/2), zero where |w| <= |j|
+// (forward.py:138-153), followed by the depth inverse FFT truncated to the
+// first N_t samples (forward.py:155).  fh(j, kappa) is the NER transform of
+// the laterally transformed field row; ghat is even in w, so only the
+// N_t + 1 values |w| = k/2, k = 0..N_t are evaluated and mirrored.  One CTA
+// per row: forward FFT (length n_over) and inverse FFT (length 2 N_t <=
+// n_over) both in shared memory, the row overwritten in place.
+// ---------------------------------------------------------------------------
+struct FwdParams {
+  NerApiParams q;       // u/out = the [rows][T] spectrum (in place)
+  const double* j2;     // [N0][N1] squared lateral frequency, wrapped (recon.py:200-215)
+  int N1, N1h, T, LT;   // LT = log2(2 T)
+  float scale;          // 1 / (2 T N0 N1): scipy ifft / ifftn normalisation
+};
+
+template <int K2, int D>
+__device__ __forceinline__ float2 ner_tap_sum(const NerApiParams& p, const float2* sbuf, fft::SwzAddr ad, double kv) {
+  constexpr int K = K2 / 2;
+  const int no = p.n_over;
+  const double xi = __dmul_rn(p.c_eff, kv);
+  const double k0d = floor(xi);
+  const int k0 = (int)k0d;
+  const float z = (float)(xi - k0d) - 0.5f;
+  const float z2 = z * z;
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    float e = p.poly[j][D], o = p.poly[j][D - 1];
+#pragma unroll
+    for (int d = D - 2; d >= 0; d -= 2) e = fmaf(e, z2, p.poly[j][d]);
+#pragma unroll
+    for (int d = D - 3; d >= 1; d -= 2) o = fmaf(o, z2, p.poly[j][d]);
+    const float wa = fmaf(z, o, e);
+    const float wb = fmaf(-z, o, e);
+    const float2 Fa = sbuf[ad((k0 + j - K + 1) & (no - 1), 0)];
+    const float2 Fb = sbuf[ad((k0 + K - j) & (no - 1), 0)];
+    acc.x = fmaf(wa, Fa.x, fmaf(wb, Fb.x, acc.x));
+    acc.y = fmaf(wa, Fa.y, fmaf(wb, Fb.y, acc.y));
+  }
+  const double red = kv - 2.0 * floor(0.5 * kv + 0.5);  // exp(-i pi kappa)
+  const float2 cs = cospi_sinpi_api((float)red);
+  return make_float2(acc.x * cs.x + acc.y * cs.y, acc.y * cs.x - acc.x * cs.y);
+}
+
+template <int K2, int D>
+__global__ void __launch_bounds__(512) forward_kernel(const FwdParams f) {
+  extern __shared__ float2 sbuf[];
+  const NerApiParams& p = f.q;
+  const int row = blockIdx.x;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int n = p.n, no = p.n_over, L = p.L, T = f.T, LT = f.LT;
+  const fft::SwzAddr ad = fft::SwzAddr::for_log(L);
+  const fft::SwzAddr adg = fft::SwzAddr::for_log(LT);
+  float2* gbuf = sbuf + no;
+  float2* __restrict__ u = p.out + (size_t)row * n;
+  fft::staged_copy<8, float2>(
+      no, tid, nth,
+      [&](int s) {
+        const int i = (s + n / 2) & (no - 1);
+        return i < n ? fft::cscale(u[i], __ldg(&p.iw[i])) : make_float2(0.f, 0.f);
+      },
+      [&](int s, float2 v) { sbuf[ad(fft::brev(s, L), 0)] = v; });
+  __syncthreads();
+  fft::fft_inplace<false, 4, true>(sbuf, L, 0, p.tw, tid, nth, ad);
+  const int j0 = row / f.N1h, j1 = row - j0 * f.N1h;
+  const double j2 = __ldg(&f.j2[(size_t)j0 * f.N1 + j1]);
+  for (int k = tid; k <= T; k += nth) {
+    const double w = 0.5 * k, w2 = w * w;
+    float2 g = make_float2(0.f, 0.f);
+    if (j2 < w2) {  // propagating (strict, forward.py:145)
+      const double ky = sqrt(w2 - j2);
+      const float2 a = ner_tap_sum<K2, D>(p, sbuf, ad, ky);
+      const float2 b = ner_tap_sum<K2, D>(p, sbuf, ad, -ky);
+      const float s = (float)(w / (2.0 * ky)) * f.scale;  // forward.py:148
+      g = make_float2((a.x + b.x) * s, (a.y + b.y) * s);
+    }
+    gbuf[adg(fft::brev(k, LT), 0)] = g;
+    if (k > 0 && k < T) gbuf[adg(fft::brev(2 * T - k, LT), 0)] = g;
+  }
+  __syncthreads();
+  fft::fft_inplace<true, 4, true>(gbuf, LT, 0, p.tw, tid, nth, adg);
+  for (int t = tid; t < T; t += nth) u[t] = gbuf[adg(t, 0)];
+}
+
 }  // namespace
 int set_last_error(int code, const std::string& msg);  // capi.cu
 }  // namespace patfft
@@ -182,6 +271,73 @@ int ensure(T** p, size_t* cap, size_t need) {
   *p = nullptr;
   API_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(1, need) * sizeof(T)));
   *cap = need;
+  return PATFFT_OK;
+}
+}  // namespace
+
+struct patfft_forward_plan {
+  int device = 0;
+  std::mutex mu;
+  patfft_ner_plan* ner = nullptr;  // NerPlan(N_t, spec) tables (forward.py:151)
+  int n_lat = 1, N0 = 1, N1 = 0, N1h = 0, T = 0;
+  size_t L = 0, Lh = 0;
+  double* d_j2 = nullptr;          // [N0][N1]
+  float* d_field = nullptr;        // host path staging [N0][N1][T] f32
+  double* d_f64 = nullptr;         // host path staging f64 (field in, traces out)
+  float2* d_spec = nullptr;        // [N0][N1h][T]
+  cufftHandle r2c = 0, c2r = 0;
+  bool have_r2c = false, have_c2r = false;
+};
+
+namespace {
+#define API_CUFFT(expr)                                                                    \
+  do {                                                                                     \
+    cufftResult _r = (expr);                                                               \
+    if (_r != CUFFT_SUCCESS)                                                               \
+      return api_fail(PATFFT_ERR_CUDA, std::string(#expr) + " failed (" + std::to_string((int)_r) + ")"); \
+  } while (0)
+
+int launch_forward(patfft_forward_plan* F, const float* field, float* traces, cudaStream_t s) {
+  patfft_ner_plan* P = F->ner;
+  API_CUFFT(cufftSetStream(F->r2c, s));
+  API_CUFFT(cufftSetStream(F->c2r, s));
+  API_CUFFT(cufftExecR2C(F->r2c, const_cast<float*>(field), reinterpret_cast<cufftComplex*>(F->d_spec)));
+  FwdParams f{};
+  f.q = P->prm;
+  f.q.u = F->d_spec;
+  f.q.out = F->d_spec;
+  f.q.rows = (int)F->Lh;
+  f.j2 = F->d_j2;
+  f.N1 = F->N1;
+  f.N1h = F->N1h;
+  f.T = F->T;
+  int LT = 0;
+  while ((1 << LT) < 2 * F->T) ++LT;
+  f.LT = LT;
+  f.scale = (float)(1.0 / (2.0 * F->T * (double)F->L));
+  const int threads = std::max(64, std::min(512, P->n_over / 16));
+  const size_t smem = (size_t)(P->n_over + 2 * F->T) * sizeof(float2);
+  cudaError_t err = cudaSuccess;
+  auto go = [&](auto k) {
+    err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err == cudaSuccess) {
+      k<<<(unsigned)F->Lh, threads, smem, s>>>(f);
+      err = cudaGetLastError();
+    }
+  };
+#define PATFFT_FWD_CASE(k2)                        \
+  case k2:                                         \
+    if (P->degree == 8) go(forward_kernel<k2, 8>); \
+    else go(forward_kernel<k2, 12>);               \
+    break;
+  switch (P->K2) {
+    PATFFT_FWD_CASE(2) PATFFT_FWD_CASE(4) PATFFT_FWD_CASE(6) PATFFT_FWD_CASE(8)
+    PATFFT_FWD_CASE(10) PATFFT_FWD_CASE(12) PATFFT_FWD_CASE(14) PATFFT_FWD_CASE(16)
+    default: return api_fail(PATFFT_ERR_PARAMETER, "unsupported K");
+  }
+#undef PATFFT_FWD_CASE
+  if (err != cudaSuccess) return api_fail(PATFFT_ERR_CUDA, cudaGetErrorString(err));
+  API_CUFFT(cufftExecC2R(F->c2r, reinterpret_cast<cufftComplex*>(F->d_spec), traces));
   return PATFFT_OK;
 }
 }  // namespace
@@ -304,6 +460,84 @@ void patfft_ner_plan_destroy(patfft_ner_plan* P) {
     if (p) cudaFree(p);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
+}
+
+int patfft_forward_plan_create(int n_lat, const int32_t* n_lateral, int n_time, const double* j2, double c, int K,
+                               double alpha, double beta, int device, patfft_forward_plan** out) {
+  if (!out || !n_lateral || !j2) return api_fail(PATFFT_ERR_PARAMETER, "null argument");
+  *out = nullptr;
+  if (n_lat != 1 && n_lat != 2) return api_fail(PATFFT_ERR_PARAMETER, "forward operator supports 2D and 3D fields");
+  const int N0 = n_lat == 2 ? n_lateral[0] : 1, N1 = n_lateral[n_lat - 1];
+  if (n_time < 2 || n_time % 2 || N1 < 2 || N1 % 2 || (n_lat == 2 && (N0 < 2 || N0 % 2)))
+    return api_fail(PATFFT_ERR_PARAMETER, "grid sizes must be even");  // forward.py:118-119
+  if (n_time & (n_time - 1)) return api_fail(PATFFT_ERR_UNSUPPORTED, "GPU forward model needs a power-of-two N_t");
+  if (2 * (int64_t)n_time > 8192) return api_fail(PATFFT_ERR_UNSUPPORTED, "GPU forward model supports N_t <= 4096");
+  std::unique_ptr<patfft_forward_plan, void (*)(patfft_forward_plan*)> F(new patfft_forward_plan(),
+                                                                          &patfft_forward_plan_destroy);
+  F->device = device;
+  int rc = patfft_ner_plan_create(n_time, c, K, alpha, beta, device, &F->ner);
+  if (rc) return rc;
+  if (F->ner->n_over < 2 * n_time)
+    return api_fail(PATFFT_ERR_UNSUPPORTED, "GPU forward model needs an oversampling factor >= 2");
+  F->n_lat = n_lat;
+  F->N0 = N0;
+  F->N1 = N1;
+  F->N1h = N1 / 2 + 1;
+  F->T = n_time;
+  F->L = (size_t)N0 * N1;
+  F->Lh = (size_t)N0 * F->N1h;
+  API_CUDA(cudaSetDevice(device));
+  API_CUDA(cudaMalloc(&F->d_j2, F->L * sizeof(double)));
+  API_CUDA(cudaMemcpy(F->d_j2, j2, F->L * sizeof(double), cudaMemcpyHostToDevice));
+  API_CUDA(cudaMalloc(&F->d_spec, F->Lh * n_time * sizeof(float2)));
+  // lateral transforms of the [N0][N1][T] volume, time fastest: T interleaved batches
+  int nr[2] = {N0, N1}, nc[2] = {N0, F->N1h};
+  int* dims = n_lat == 2 ? nr : nr + 1;
+  int* cdims = n_lat == 2 ? nc : nc + 1;
+  API_CUFFT(cufftPlanMany(&F->r2c, n_lat, dims, dims, n_time, 1, cdims, n_time, 1, CUFFT_R2C, n_time));
+  F->have_r2c = true;
+  API_CUFFT(cufftPlanMany(&F->c2r, n_lat, dims, cdims, n_time, 1, dims, n_time, 1, CUFFT_C2R, n_time));
+  F->have_c2r = true;
+  *out = F.release();
+  return PATFFT_OK;
+}
+
+int patfft_forward_execute_device(patfft_forward_plan* F, const float* field, float* traces, void* stream) {
+  if (!F || !field || !traces) return api_fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(F->mu);
+  API_CUDA(cudaSetDevice(F->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : F->ner->stream;
+  return launch_forward(F, field, traces, st);
+}
+
+int patfft_forward_execute(patfft_forward_plan* F, const double* field, double* traces) {
+  if (!F || !field || !traces) return api_fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(F->mu);
+  API_CUDA(cudaSetDevice(F->device));
+  cudaStream_t st = F->ner->stream;
+  const size_t vol = F->L * F->T;
+  if (!F->d_field) API_CUDA(cudaMalloc(&F->d_field, vol * sizeof(float)));
+  if (!F->d_f64) API_CUDA(cudaMalloc(&F->d_f64, vol * sizeof(double)));
+  API_CUDA(cudaMemcpyAsync(F->d_f64, field, vol * sizeof(double), cudaMemcpyHostToDevice, st));
+  API_CUDA(launch_f64_to_f32(F->d_f64, F->d_field, vol, st));
+  int rc = launch_forward(F, F->d_field, F->d_field, st);
+  if (rc) return rc;
+  API_CUDA(launch_f32_to_f64(F->d_field, F->d_f64, vol, st));
+  API_CUDA(cudaMemcpyAsync(traces, F->d_f64, vol * sizeof(double), cudaMemcpyDeviceToHost, st));
+  API_CUDA(cudaStreamSynchronize(st));
+  return PATFFT_OK;
+}
+
+void patfft_forward_plan_destroy(patfft_forward_plan* F) {
+  if (!F) return;
+  cudaSetDevice(F->device);
+  if (F->ner && F->ner->stream) cudaStreamSynchronize(F->ner->stream);
+  if (F->have_r2c) cufftDestroy(F->r2c);
+  if (F->have_c2r) cufftDestroy(F->c2r);
+  for (void* p : {(void*)F->d_j2, (void*)F->d_field, (void*)F->d_f64, (void*)F->d_spec})
+    if (p) cudaFree(p);
+  patfft_ner_plan_destroy(F->ner);
+  delete F;
 }
 
 }  // extern "C"

@@ -25,6 +25,7 @@ sys.dont_write_bytecode = True
 sys.path.insert(0, REF)
 sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
 
+from patfft import forward as rforward  # noqa: E402  (reference)
 from patfft import nufft as rnufft  # noqa: E402  (reference)
 from patfft import recon as rrecon  # noqa: E402  (reference)
 
@@ -149,6 +150,26 @@ def main():
     ned2 = rnufft.NedPlan((16, 24)).execute(pos2, v2, order="wrapped")
     _save("ned_axes", pos1=pos1, v1=v1, out1=ned1, direct1=rnufft.nudft_ned_direct(pos1, v1, (32,)),
           pos2=pos2, v2=v2, out2_wrapped=ned2)
+
+    # forward model (forward.py:105-166) on phantoms rasterised by the reference
+    def forward_case(name, dims, spacing, balls, spec=None, sound_speed=synth.SOUND_SPEED):
+        ph = rforward.PhantomSpec(dims=dims, spacing=spacing, balls=[rforward.Ball(*b) for b in balls])
+        f = ph.rasterize()
+        wspec = None if spec is None else rnufft.WindowSpec(**spec)
+        rec = rforward.forward_fourier(f, sound_speed, wspec)
+        spec = spec or {}
+        _save(name, field=f.values, spacing=np.asarray(f.spacing), sound_speed=sound_speed,
+              spec_c=spec.get("c", 2.0), spec_K=spec.get("K", 6),
+              samples=rec.samples, positions=rec.positions, weights=rec.weights, dt=rec.dt, dx=rec.dx,
+              n_lateral=np.asarray(rec.n_lateral))
+
+    p = synth.PITCH
+    forward_case("forward_3d_16x16x64", (16, 16, 64), (p, p, 30e-6),
+                 [((0.3e-3, -0.2e-3, 0.9e-3), 0.35e-3, 1.0), ((-0.5e-3, 0.4e-3, 1.3e-3), 0.25e-3, 0.6)])
+    forward_case("forward_3d_rect8x16x32", (8, 16, 32), (1.5 * p, p, 30e-6),
+                 [((0.1e-3, 0.2e-3, 0.5e-3), 0.3e-3, 0.8)], spec={"c": 2.0, "K": 4})
+    forward_case("forward_2d_64x128", (64, 128), (p, 20e-6),
+                 [((0.4e-3, 1.0e-3), 0.3e-3, 1.0), ((-1.5e-3, 1.8e-3), 0.5e-3, 0.5)])
 
     # window pair and warp known answers
     spec = rnufft.WindowSpec().resolved(2.0)

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import paper_1501_02946_b200 as pb
-from conftest import golden_recon_files, golden_spec, rel_l2
+from conftest import GOLDEN, golden_recon_files, golden_spec, rel_l2
 from oracle import nedner_oracle as O
 from paper_1501_02946_b200 import synth
 
@@ -234,3 +234,45 @@ def test_gpu_nedplan_centered_2d_vs_direct_and_validation():
         pb.NedPlan((32, 15))
     with pytest.raises(pb.ParameterError):
         pb.NedPlan((32, 16)).execute(pos, vals, order="sideways")
+
+
+FORWARD_GOLDENS = ["forward_3d_16x16x64", "forward_3d_rect8x16x32", "forward_2d_64x128"]
+
+
+@pytest.mark.parametrize("name", FORWARD_GOLDENS)
+def test_gpu_forward_fourier_matches_reference_golden(name):
+    g = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    f = pb.ScalarField(g["field"], tuple(g["spacing"]))
+    rec = pb.forward_fourier(f, float(g["sound_speed"]), pb.WindowSpec(c=float(g["spec_c"]), K=int(g["spec_K"])))
+    assert rec.samples.shape == g["samples"].shape and rec.samples.dtype == np.float64
+    np.testing.assert_array_equal(rec.positions, g["positions"])
+    np.testing.assert_array_equal(rec.weights, g["weights"])
+    assert rec.dt == float(g["dt"]) and rec.n_lateral == tuple(int(n) for n in g["n_lateral"])
+    err = rel_l2(rec.samples, g["samples"])
+    print(f"{name}: rel-L2 {err:.3e}")
+    assert err <= TOL
+
+
+def test_gpu_forward_fourier_larger_vs_oracle_and_validation():
+    from oracle import forward_oracle as F
+
+    rng = np.random.default_rng(5)
+    vals = np.zeros((64, 64, 256))
+    vals[20:30, 35:44, 60:75] = 1.0
+    vals += 0.05 * rng.standard_normal(vals.shape)
+    sp = (0.2e-3, 0.2e-3, 30e-6)
+    rec = pb.forward_fourier(pb.ScalarField(vals, sp), 1500.0)
+    want, _, _, _ = F.forward_fourier(vals, sp, 1500.0)
+    err = rel_l2(rec.samples, want)
+    print(f"forward 64x64x256: rel-L2 {err:.3e}")
+    assert err <= TOL
+    # linearity and zero field
+    rec2 = pb.forward_fourier(pb.ScalarField(2.0 * vals, sp), 1500.0)
+    assert rel_l2(rec2.samples, 2.0 * rec.samples) <= 1e-6
+    assert not np.any(pb.forward_fourier(pb.ScalarField(np.zeros((8, 8, 16)), sp), 1500.0).samples)
+    with pytest.raises(pb.ParameterError, match="sound speed"):
+        pb.forward_fourier(pb.ScalarField(vals, sp), 0.0)
+    with pytest.raises(pb.ParameterError, match="even"):
+        pb.forward_fourier(pb.ScalarField(np.zeros((8, 9, 16)), sp), 1500.0)
+    with pytest.raises(pb.ParameterError, match="2D and 3D"):
+        pb.forward_fourier(pb.ScalarField(np.zeros((4, 4, 4, 4)), (1, 1, 1, 1)), 1500.0)
