@@ -20,6 +20,7 @@ from .recon import (
 )
 from .nufft import NedPlan, NerPlan, nufft_ned, nufft_ner
 from .forward import ForwardPlan, forward_fourier
+from .arrayfile import open_array, read_array, reconstruct_frames_file, write_array
 from .window import WindowSpec
 
 __version__ = "0.1.0"
@@ -39,6 +40,10 @@ __all__ = [
     "WindowSpec",
     "amplitude_factor",
     "forward_fourier",
+    "open_array",
+    "read_array",
+    "reconstruct_frames_file",
+    "write_array",
     "nufft_ned",
     "nufft_ner",
     "kappa",

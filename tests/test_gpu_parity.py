@@ -276,3 +276,27 @@ def test_gpu_forward_fourier_larger_vs_oracle_and_validation():
         pb.forward_fourier(pb.ScalarField(np.zeros((8, 9, 16)), sp), 1500.0)
     with pytest.raises(pb.ParameterError, match="2D and 3D"):
         pb.forward_fourier(pb.ScalarField(np.zeros((4, 4, 4, 4)), (1, 1, 1, 1)), 1500.0)
+
+
+def test_gpu_frames_file_stream_matches_per_frame_reconstruction(tmp_path):
+    # config-5 style frames (one sensor layout) streamed from a PATARR01 file
+    s = synth.make_3d(31, 16, 32, 20e-9, "jittered", 2)
+    rng = np.random.default_rng(31)
+    frames = np.stack([s.samples * rng.uniform(0.5, 1.5) + 0.01 * rng.standard_normal(s.samples.shape)
+                       for _ in range(3)])
+    src, dst = tmp_path / "frames.patarr", tmp_path / "volumes.patarr"
+    pb.write_array(src, frames, spacing=(1.0, 1.0, s.dt), axes=("frame", "sensor", "t"))
+    plan = pb.NedNerPlan(s.positions, s.weights, 32, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    h = pb.reconstruct_frames_file(plan, src, dst)
+    vols, hr = pb.read_array(dst)
+    assert hr.dims == h.dims == (3,) + plan.out_shape
+    assert hr.meta["frames"] == [0, 1, 2]
+    for k in range(3):
+        rec = pb.SensorRecord(s.positions, s.weights, frames[k], s.dt, s.sound_speed, s.dx, s.n_lateral)
+        want = pb.reconstruct_nedner(rec).values
+        np.testing.assert_array_equal(vols[k], want)   # same plan arithmetic, bit-identical
+        oracle, _ = O.reconstruct_nedner(s.positions, s.weights, frames[k], s.dt, s.sound_speed, s.dx, s.n_lateral)
+        assert rel_l2(vols[k], oracle) <= TOL
+    with pytest.raises(pb.ParameterError):
+        pb.reconstruct_frames_file(pb.NedNerPlan(s.positions, s.weights, 64, s.dt, s.sound_speed, s.dx,
+                                                 s.n_lateral), src, dst)
