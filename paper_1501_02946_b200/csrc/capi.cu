@@ -103,6 +103,13 @@ double jterm(int kw, int n, double ratio) {
   return v * v;
 }
 
+void set_tc(const patfft_nedner_plan* P, SpreadParams& sp) {
+  sp.tc_recs = P->d_tc_recs;
+  sp.tc_tiles = P->d_tc_tiles;
+  sp.tc_ntiles = P->tc_ntiles;
+  sp.tc_n = P->tc_n;
+}
+
 // Interpolating polynomial of degree D through Chebyshev nodes on
 // [-1/2, 1/2] (monomial coefficients in z), fp64 Gaussian elimination.
 template <class F>
@@ -476,6 +483,82 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     }
   }
 
+  // ---- tensor-core gridding records (spread_tc.cu) --------------------------
+  // One record per (tile of 8 rows x 16 columns, sensor meeting it): the
+  // sensor's row weights (times h_m/dx^(d-1)) on the tile's 8 rows and its
+  // column weights on the tile's 16 columns (zero outside its window, wrapped
+  // taps summed), padded per tile to whole 16-sensor stages.  Tiles are
+  // launched longest first.
+  std::vector<float> tcrec;
+  std::vector<int4> tctiles;
+  static const bool tc_on = [] {
+    const char* e = std::getenv("PATFFT_SPREAD_TC");
+    return e ? std::atoi(e) != 0 : false;
+  }();
+  if (tc_on && mode == 0 && spread_tc_supported(d->n_lat, nrows, ncols, T)) {
+    const int trs = nrows / 8, tcs = ncols / 16, ntiles = trs * tcs;
+    std::vector<int64_t> cnt(ntiles, 0);
+    struct Pair {
+      int tile, m;
+      float wr[8], wc[16];
+    };
+    std::vector<Pair> pairs;
+    pairs.reserve((size_t)M * 5);
+    for (int m = 0; m < M; ++m) {
+      std::vector<std::pair<int, std::array<float, 8>>> rt;
+      std::vector<std::pair<int, std::array<float, 16>>> ct;
+      for (int a = 0; a < K2; ++a) {
+        const int row = (int)pmod(urow[m] + a, nrows), ti = row / 8;
+        auto it = std::find_if(rt.begin(), rt.end(), [&](const auto& x) { return x.first == ti; });
+        if (it == rt.end()) {
+          rt.push_back({ti, {}});
+          it = rt.end() - 1;
+          it->second.fill(0.f);
+        }
+        it->second[row % 8] = (float)((double)it->second[row % 8] + wrowv[(size_t)m * K2 + a] * sscale[m]);
+        const int col = (int)pmod(ucol[m] + a, ncols), tj = col / 16;
+        auto jt = std::find_if(ct.begin(), ct.end(), [&](const auto& x) { return x.first == tj; });
+        if (jt == ct.end()) {
+          ct.push_back({tj, {}});
+          jt = ct.end() - 1;
+          jt->second.fill(0.f);
+        }
+        jt->second[col % 16] = (float)((double)jt->second[col % 16] + wcolv[(size_t)m * K2 + a]);
+      }
+      for (const auto& r : rt)
+        for (const auto& c : ct) {
+          Pair q;
+          q.tile = r.first * tcs + c.first;
+          q.m = m;
+          std::copy(r.second.begin(), r.second.end(), q.wr);
+          std::copy(c.second.begin(), c.second.end(), q.wc);
+          pairs.push_back(q);
+          cnt[q.tile]++;
+        }
+    }
+    std::vector<int64_t> padded(ntiles), start(ntiles + 1, 0);
+    for (int t = 0; t < ntiles; ++t) {
+      padded[t] = (cnt[t] + 15) / 16 * 16;
+      start[t + 1] = start[t] + padded[t];
+    }
+    if (start[ntiles] > (int64_t)INT32_MAX / 32) return fail(PATFFT_ERR_UNSUPPORTED, "too many gridding records");
+    tcrec.assign((size_t)start[ntiles] * 32, 0.f);
+    std::vector<int64_t> fill(start.begin(), start.end() - 1);
+    for (const Pair& q : pairs) {
+      float* o = &tcrec[(size_t)fill[q.tile]++ * 32];
+      std::memcpy(&o[0], &q.m, 4);
+      std::copy(q.wr, q.wr + 8, o + 8);
+      std::copy(q.wc, q.wc + 16, o + 16);
+    }
+    std::vector<int> order(ntiles);
+    for (int t = 0; t < ntiles; ++t) order[t] = t;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return padded[a] > padded[b]; });
+    for (int t : order) tctiles.push_back(make_int4((int)start[t], (int)padded[t], (t / tcs) * 8, (t % tcs) * 16));
+    P->tc_ntiles = ntiles;
+    P->tc_n = spread_tc_block(T);
+    P->tc_records = start[ntiles];
+  }
+
   // ---- deapodisation (nufft.py:367-371), normalised by psi_hat(0) --------
   std::vector<float> dp0(P->N0, 1.0f), dp1(P->N1);
   auto deapod = [](const Window& w, int N, std::vector<float>& dp) {
@@ -523,6 +606,10 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // ---- device buffers -----------------------------------------------------
   int rc;
   if ((rc = upload(&P->d_recs, recbuf))) return rc;
+  if (P->tc_ntiles) {
+    if ((rc = upload(&P->d_tc_recs, tcrec))) return rc;
+    if ((rc = upload(&P->d_tc_tiles, tctiles))) return rc;
+  }
   if (mode == 1 || mode == 2) {
     std::vector<int> gi(M);
     std::vector<char> seen((size_t)M, 0);
@@ -703,6 +790,7 @@ int patfft_ned_execute(patfft_nedner_plan* P, const double* values, double* out,
   sp.recs = P->d_recs;
   sp.blk = P->d_blk;
   sp.blk_grp = P->d_blkgrp;
+  set_tc(P, sp);
   sp.grid = P->d_grid;
   sp.T = P->T;
   sp.ncols = P->ncols;
@@ -817,6 +905,7 @@ static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* 
   sp.recs = P->d_recs;
   sp.blk = P->d_blk;
   sp.blk_grp = P->d_blkgrp;
+  set_tc(P, sp);
   sp.grid = P->d_grid;
   sp.T = T;
   sp.ncols = P->ncols;
@@ -1017,6 +1106,7 @@ int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* 
     sp.recs = P->d_recs;
     sp.blk = P->d_blk;
     sp.blk_grp = P->d_blkgrp;
+    set_tc(P, sp);
     sp.grid = P->d_grid;
     sp.T = T;
     sp.ncols = P->ncols;
@@ -1067,7 +1157,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
   for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_gh,
-                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
+                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_tc_recs, (void*)P->d_tc_tiles, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_tw, (void*)P->d_jt0,
                   (void*)P->d_jt1})
     free_dev(p);

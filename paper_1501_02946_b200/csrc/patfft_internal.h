@@ -49,6 +49,10 @@ struct SpreadParams {
   float* grid;            // [nrows][ncols][T] centred oversampled grid
   int T, ncols, nrows;
   int t_begin, t_end;     // time range processed by this launch (multiples of 128)
+  // tensor-core gridding (spread_tc.cu); tc_tiles == nullptr selects the SIMT kernels
+  const float* tc_recs = nullptr;   // [records][32]: sensor id, 8 row weights at [8], 16 column weights at [16]
+  const int4* tc_tiles = nullptr;   // per tile (launch order): {first record, records (multiple of 16), row0, col0}
+  int tc_ntiles = 0, tc_n = 0, tc_tblocks = 0;  // tiles, time samples per CTA, time blocks per launch
 };
 
 struct LateralParams {
@@ -91,6 +95,9 @@ struct NerParams {
 
 // Kernel launchers
 cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaStream_t s);
+cudaError_t launch_spread_tc(const SpreadParams& p, cudaStream_t s);
+bool spread_tc_supported(int n_lat, int nrows, int ncols, int T);
+int spread_tc_block(int T);
 int spread_rows_per_group(int n_lat, int K2);
 int spread_record_words(int K2, int R);
 int spread_ctas_per_sm(int R);
@@ -155,6 +162,10 @@ struct patfft_nedner_plan {
   float* d_out = nullptr;       // [N0u][N1u][Tu] f32 (host path staging)
   double* d_out64 = nullptr;
   float* d_recs = nullptr;
+  float* d_tc_recs = nullptr;   // tensor-core gridding records (spread_tc.cu)
+  int4* d_tc_tiles = nullptr;
+  int tc_ntiles = 0, tc_n = 0;
+  int64_t tc_records = 0;
   int* d_gidx = nullptr;      // equispaced modes: grid row of each sensor
   int4* d_blk = nullptr;
   int* d_blkgrp = nullptr;

@@ -605,6 +605,7 @@ int spread_time_chunks(int T, int R) {
 }
 
 cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaStream_t s) {
+  if (p.tc_tiles) return launch_spread_tc(p, s);
   if (spread_time_pairs(R)) {
 #define PATFFT_SPREAD_TPK(RR)                       \
     switch (K2) {                                   \
