@@ -493,7 +493,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   std::vector<int4> tctiles;
   static const bool tc_on = [] {
     const char* e = std::getenv("PATFFT_SPREAD_TC");
-    return e ? std::atoi(e) != 0 : false;
+    return e ? std::atoi(e) != 0 : true;
   }();
   if (tc_on && mode == 0 && spread_tc_supported(d->n_lat, nrows, ncols, T)) {
     const int trs = nrows / 8, tcs = ncols / 16, ntiles = trs * tcs;

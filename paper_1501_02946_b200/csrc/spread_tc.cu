@@ -35,8 +35,9 @@ namespace {
 
 constexpr int kTR = 8, kTC = 16, kTM = kTR * kTC;  // tile rows, cols, points (UMMA M)
 constexpr int kKC = 16;                              // sensors per stage
-constexpr int kThreadsTC = 128;
+constexpr int kThreadsTC = 256;
 constexpr int kStages = 2;
+constexpr int kRecSlots = 3;  // record ring (bulk copies two stages ahead)
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -79,33 +80,35 @@ __device__ __forceinline__ void umma_tf32(uint32_t dt, uint64_t ad, uint64_t bd,
       "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
 }
 
-__device__ __forceinline__ float tf32_hi(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-__device__ __forceinline__ float4 split_hi(float4 v) {
-  return make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-}
-__device__ __forceinline__ float4 sub4(float4 a, float4 b) {
-  return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+// x = hi + lo with hi = x rounded to tf32 (10 explicit mantissa bits, ties
+// away) and lo = x - hi exact in fp32; the tensor core truncates lo to tf32.
+__device__ __forceinline__ void split_tf32(float4 v, float4& h, float4& l) {
+  h.x = __uint_as_float((__float_as_uint(v.x) + 0x1000u) & 0xFFFFE000u);
+  h.y = __uint_as_float((__float_as_uint(v.y) + 0x1000u) & 0xFFFFE000u);
+  h.z = __uint_as_float((__float_as_uint(v.z) + 0x1000u) & 0xFFFFE000u);
+  h.w = __uint_as_float((__float_as_uint(v.w) + 0x1000u) & 0xFFFFE000u);
+  l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
 }
 
 template <int N>
-__global__ void __launch_bounds__(kThreadsTC) spread_tc_kernel(const SpreadParams p) {
+__global__ void __launch_bounds__(kThreadsTC, 2) spread_tc_kernel(const SpreadParams p) {
   constexpr int A_BYTES = kTM * kKC * 4;          // 8 KB: [kKC/4][128][4]
   constexpr int B_BYTES = kKC * N * 4;            // [kKC/4][N][4]
   constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  constexpr uint32_t A_LBO = kTM * 16, A_SBO = 128;       // K step of 4 / 8-row group
-  constexpr uint32_t B_LBO = N * 16, B_SBO = 128;         // K step of 4 / 8-sample group
+  constexpr uint32_t A_LBO = kTM * 16, A_SBO = 128;  // K step of 4 / 8-row group
+  constexpr uint32_t B_LBO = N * 16, B_SBO = 128;    // K step of 4 / 8-sample group
   constexpr uint32_t TCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
   constexpr uint32_t IDESC = umma_idesc_tf32(N);
+  constexpr uint32_t REC_BYTES = kKC * 32 * 4;  // one stage of records (2 KB)
+  constexpr int NI = (N + kThreadsTC - 1) / kThreadsTC;
 
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mma_bar[kStages];
+  __shared__ uint64_t rec_bar[kRecSlots];
+  __shared__ __align__(16) float recbuf[kRecSlots * kKC * 32];
   __shared__ uint32_t tmem_base_s;
 
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int4 tile = p.tc_tiles[blockIdx.x / p.tc_tblocks];  // {first record, records, row0, col0}
   const int tb = blockIdx.x % p.tc_tblocks;
   const int t0 = p.t_begin + tb * N;
@@ -118,6 +121,7 @@ __global__ void __launch_bounds__(kThreadsTC) spread_tc_kernel(const SpreadParam
   }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init_tc(&mma_bar[s], 1);
+    for (int s = 0; s < kRecSlots; ++s) mbar_init_tc(&rec_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -125,9 +129,37 @@ __global__ void __launch_bounds__(kThreadsTC) spread_tc_kernel(const SpreadParam
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
 
-  // this thread's grid point (A rows) and its B-producer coordinates
-  const int pr = tid / kTC, pc = tid % kTC;
+  // A producer: grid point pa (row pr, column pc), k-quads ga0, ga0 + 1
+  const int pa = tid & (kTM - 1), pr = pa / kTC, pc = pa % kTC, ga0 = (tid >> 7) * 2;
   const float* __restrict__ recs = p.tc_recs + (size_t)tile.x * 32;
+  // records: 3-slot ring filled by bulk (TMA) copies two stages ahead
+  auto fetch_recs = [&](int c) {
+    const int r = c % kRecSlots;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rec_bar[r])), "r"(REC_BYTES)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(recbuf + r * kKC * 32)),
+                 "l"(recs + (size_t)c * kKC * 32), "r"(REC_BYTES), "r"(su32(&rec_bar[r]))
+                 : "memory");
+  };
+  if (tid == 0)
+    for (int c = 0; c < nch && c < kRecSlots - 1; ++c) fetch_recs(c);
+  // B producer: samples of the next stage prefetched into registers,
+  // sv[i][k] = S[sensor k][t0 + tid + 256 i]
+  float sv[NI][kKC];
+  auto load_samples = [&](int c) {
+    const int r = c % kRecSlots;
+    mbar_wait_tc(&rec_bar[r], (c / kRecSlots) & 1);
+    const float* rb = recbuf + r * kKC * 32;
+#pragma unroll
+    for (int k = 0; k < kKC; ++k) {
+      const float* __restrict__ srow = p.samples + (size_t)__float_as_int(rb[k * 32]) * p.T + t0;
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (tid + i * kThreadsTC < N) sv[i][k] = __ldg(srow + tid + i * kThreadsTC);
+    }
+  };
+  if (nch > 0) load_samples(0);
 
   for (int c = 0; c < nch; ++c) {
     const int s = c & 1;
@@ -137,36 +169,32 @@ __global__ void __launch_bounds__(kThreadsTC) spread_tc_kernel(const SpreadParam
     float* Alo = reinterpret_cast<float*>(st + A_BYTES);
     float* Bhi = reinterpret_cast<float*>(st + 2 * A_BYTES);
     float* Blo = reinterpret_cast<float*>(st + 2 * A_BYTES + B_BYTES);
-    const float* rc = recs + (size_t)c * kKC * 32;
-    // ---- A: W[p][k] = wrow[k][pr] * wcol[k][pc], k-quads of 16 bytes
+    const float* rb = recbuf + (c % kRecSlots) * kKC * 32;
+    // ---- A: W[p][k] = wrow[k][pr] * wcol[k][pc], K-major [k/4][p][4]
 #pragma unroll
-    for (int g = 0; g < kKC / 4; ++g) {
-      float w[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float* r = rc + (g * 4 + j) * 32;
-        w[j] = __ldg(r + 8 + pr) * __ldg(r + 16 + pc);
-      }
-      const float4 v = make_float4(w[0], w[1], w[2], w[3]);
-      const float4 h = split_hi(v);
-      *reinterpret_cast<float4*>(Ahi + g * (A_LBO / 4) + tid * 4) = h;
-      *reinterpret_cast<float4*>(Alo + g * (A_LBO / 4) + tid * 4) = sub4(v, h);
+    for (int g = ga0; g < ga0 + 2; ++g) {
+      const float4 v = make_float4(rb[(g * 4 + 0) * 32 + 8 + pr] * rb[(g * 4 + 0) * 32 + 16 + pc],
+                                   rb[(g * 4 + 1) * 32 + 8 + pr] * rb[(g * 4 + 1) * 32 + 16 + pc],
+                                   rb[(g * 4 + 2) * 32 + 8 + pr] * rb[(g * 4 + 2) * 32 + 16 + pc],
+                                   rb[(g * 4 + 3) * 32 + 8 + pr] * rb[(g * 4 + 3) * 32 + 16 + pc]);
+      float4 h, l;
+      split_tf32(v, h, l);
+      *reinterpret_cast<float4*>(Ahi + g * (A_LBO / 4) + pa * 4) = h;
+      *reinterpret_cast<float4*>(Alo + g * (A_LBO / 4) + pa * 4) = l;
     }
-    // ---- B: gathered sample rows, K-major [k/4][n][4] (thread = time sample,
-    // 4 sensors per 16-byte store; every load instruction is one 128-byte run)
+    // ---- B: K-major [k/4][n][4], thread = time sample, 4 sensors per 16-byte store
 #pragma unroll
-    for (int kq = 0; kq < kKC / 4; ++kq) {
-      const float* __restrict__ s0 = p.samples + (size_t)__float_as_int(__ldg(rc + (kq * 4 + 0) * 32)) * p.T + t0;
-      const float* __restrict__ s1 = p.samples + (size_t)__float_as_int(__ldg(rc + (kq * 4 + 1) * 32)) * p.T + t0;
-      const float* __restrict__ s2 = p.samples + (size_t)__float_as_int(__ldg(rc + (kq * 4 + 2) * 32)) * p.T + t0;
-      const float* __restrict__ s3 = p.samples + (size_t)__float_as_int(__ldg(rc + (kq * 4 + 3) * 32)) * p.T + t0;
+    for (int i = 0; i < NI; ++i) {
+      const int n = tid + i * kThreadsTC;
+      if (n < N) {
 #pragma unroll
-      for (int n = tid; n < N; n += kThreadsTC) {
-        const float4 v = make_float4(__ldg(s0 + n), __ldg(s1 + n), __ldg(s2 + n), __ldg(s3 + n));
-        const float4 h = split_hi(v);
-        const int off = kq * (B_LBO / 4) + n * 4;
-        *reinterpret_cast<float4*>(Bhi + off) = h;
-        *reinterpret_cast<float4*>(Blo + off) = sub4(v, h);
+        for (int kq = 0; kq < kKC / 4; ++kq) {
+          float4 h, l;
+          split_tf32(make_float4(sv[i][4 * kq], sv[i][4 * kq + 1], sv[i][4 * kq + 2], sv[i][4 * kq + 3]), h, l);
+          const int off = kq * (B_LBO / 4) + n * 4;
+          *reinterpret_cast<float4*>(Bhi + off) = h;
+          *reinterpret_cast<float4*>(Blo + off) = l;
+        }
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -187,20 +215,28 @@ __global__ void __launch_bounds__(kThreadsTC) spread_tc_kernel(const SpreadParam
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        su32(&mma_bar[s]))
                    : "memory");
+      // slot (c + 2) % 3 was last read in iteration c - 1 (before this iteration's barrier)
+      if (c + kRecSlots - 1 < nch) fetch_recs(c + kRecSlots - 1);
     }
+    if (c + 1 < nch) load_samples(c + 1);
   }
 
-  // ---- epilogue: TMEM -> registers -> grid (thread = grid point)
-  float* __restrict__ out =
-      p.grid + ((size_t)(tile.z + pr) * p.ncols + (tile.w + pc)) * p.T + t0;
+  // ---- epilogue: TMEM -> registers -> shared (per-warp transpose) -> grid.
+  // Warp w reads TMEM lanes 32 (w % 4) .. +31 (grid points) and the 32-sample
+  // column blocks j = w / 4, w / 4 + 2, ...; each store instruction then
+  // writes four points x 128 contiguous bytes.
+  const int q4 = warp & 3;
+  float* stg = reinterpret_cast<float*>(smem) + warp * 32 * 36;
   if (nch > 0) {
     const int cl = nch - 1;
     mbar_wait_tc(&mma_bar[cl & 1], (cl >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
 #pragma unroll 1
-    for (int j = 0; j < N / 32; ++j) {
-      uint32_t r[32];
-      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(j * 32);
+  for (int j = warp >> 2; j < N / 32; j += kThreadsTC / 128) {
+    uint32_t r[32];
+    if (nch > 0) {
+      const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(j * 32);
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
           "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
@@ -210,15 +246,22 @@ __global__ void __launch_bounds__(kThreadsTC) spread_tc_kernel(const SpreadParam
             "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
           : "r"(ta));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      float4* o4 = reinterpret_cast<float4*>(out + j * 32);
+    } else {
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        o4[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
-                            __uint_as_float(r[4 * q + 3]));
+      for (int q = 0; q < 32; ++q) r[q] = 0u;
     }
-  } else {
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j = 0; j < N / 4; ++j) reinterpret_cast<float4*>(out)[j] = z;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<uint4*>(stg + lane * 36 + 4 * q) = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int pl = q * 4 + (lane >> 3), pt = q4 * 32 + pl;  // point within the tile
+      const float4 v = *reinterpret_cast<const float4*>(stg + pl * 36 + (lane & 7) * 4);
+      float* o = p.grid + ((size_t)(tile.z + pt / kTC) * p.ncols + (tile.w + pt % kTC)) * p.T + t0 + j * 32;
+      *reinterpret_cast<float4*>(o + (lane & 7) * 4) = v;
+    }
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
