@@ -107,6 +107,8 @@ void set_tc(const patfft_nedner_plan* P, SpreadParams& sp) {
   sp.tc_recs = P->d_tc_recs;
   sp.tc_tiles = P->d_tc_tiles;
   sp.tc_ntiles = P->tc_ntiles;
+  sp.tc_nonempty = P->tc_nonempty;
+  sp.tc_counter = P->d_tc_counter;
   sp.tc_n = P->tc_n;
 }
 
@@ -555,6 +557,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return padded[a] > padded[b]; });
     for (int t : order) tctiles.push_back(make_int4((int)start[t], (int)padded[t], (t / tcs) * 8, (t % tcs) * 16));
     P->tc_ntiles = ntiles;
+    P->tc_nonempty = (int)std::count_if(padded.begin(), padded.end(), [](int64_t v) { return v > 0; });
     P->tc_n = spread_tc_block(T);
     P->tc_records = start[ntiles];
   }
@@ -609,6 +612,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   if (P->tc_ntiles) {
     if ((rc = upload(&P->d_tc_recs, tcrec))) return rc;
     if ((rc = upload(&P->d_tc_tiles, tctiles))) return rc;
+    if ((rc = dalloc(&P->d_tc_counter, 1))) return rc;
   }
   if (mode == 1 || mode == 2) {
     std::vector<int> gi(M);
@@ -1157,7 +1161,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
   for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_gh,
-                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_tc_recs, (void*)P->d_tc_tiles, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
+                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_tc_recs, (void*)P->d_tc_tiles, (void*)P->d_tc_counter, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_tw, (void*)P->d_jt0,
                   (void*)P->d_jt1})
     free_dev(p);

@@ -52,7 +52,9 @@ struct SpreadParams {
   // tensor-core gridding (spread_tc.cu); tc_tiles == nullptr selects the SIMT kernels
   const float* tc_recs = nullptr;   // [records][32]: sensor id, 8 row weights at [8], 16 column weights at [16]
   const int4* tc_tiles = nullptr;   // per tile (launch order): {first record, records (multiple of 16), row0, col0}
-  int tc_ntiles = 0, tc_n = 0, tc_tblocks = 0;  // tiles, time samples per CTA, time blocks per launch
+  int tc_ntiles = 0, tc_nonempty = 0;  // tiles (the non-empty ones first, longest first)
+  int tc_n = 0, tc_tblocks = 0;       // time samples per block, time blocks per launch
+  int* tc_counter = nullptr;          // work-item counter (zeroed before each launch)
 };
 
 struct LateralParams {
@@ -164,7 +166,8 @@ struct patfft_nedner_plan {
   float* d_recs = nullptr;
   float* d_tc_recs = nullptr;   // tensor-core gridding records (spread_tc.cu)
   int4* d_tc_tiles = nullptr;
-  int tc_ntiles = 0, tc_n = 0;
+  int* d_tc_counter = nullptr;
+  int tc_ntiles = 0, tc_nonempty = 0, tc_n = 0;
   int64_t tc_records = 0;
   int* d_gidx = nullptr;      // equispaced modes: grid row of each sensor
   int4* d_blk = nullptr;

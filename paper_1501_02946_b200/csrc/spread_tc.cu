@@ -26,6 +26,7 @@
 // layouts (8 x 16-byte core matrices), written conflict-free.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "patfft_internal.h"
@@ -37,7 +38,7 @@ constexpr int kTR = 8, kTC = 16, kTM = kTR * kTC;  // tile rows, cols, points (U
 constexpr int kKC = 16;                              // sensors per stage
 constexpr int kThreadsTC = 256;
 constexpr int kStages = 2;
-constexpr int kRecSlots = 3;  // record ring (bulk copies two stages ahead)
+constexpr int kRecSlots = 4;  // record ring (bulk copies three stages ahead)
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -90,6 +91,40 @@ __device__ __forceinline__ void split_tf32(float4 v, float4& h, float4& l) {
   l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
 }
 
+// Position in a CTA's stage sequence.  Work items w = (tile w / tblocks,
+// time block w % tblocks) are claimed dynamically (atomic counter, items in
+// longest-tile-first order) by thread 0's record cursor, which runs three
+// stages ahead and publishes each claimed item in a small shared ring; the
+// sample cursor (two stages ahead) and the build cursor follow the ring.
+constexpr int kRing = 8;
+struct Cursor {
+  int k, tb, c, nch, rec0, row0, col0;  // ring position, time block, chunk, chunks, first record, tile origin
+  bool valid;
+};
+__device__ __forceinline__ void cursor_load(const SpreadParams& p, Cursor& u, int w) {
+  u.valid = w < p.tc_nonempty * p.tc_tblocks;
+  if (!u.valid) return;
+  const int4 t = __ldg(&p.tc_tiles[w / p.tc_tblocks]);
+  u.tb = w % p.tc_tblocks;
+  u.c = 0;
+  u.nch = t.y / kKC;
+  u.rec0 = t.x;
+  u.row0 = t.z;
+  u.col0 = t.w;
+}
+__device__ __forceinline__ void cursor_next(const SpreadParams& p, Cursor& u, const int* ring) {
+  if (!u.valid || ++u.c < u.nch) return;
+  ++u.k;
+  cursor_load(p, u, ring[u.k & (kRing - 1)]);
+}
+__device__ __forceinline__ void cursor_claim(const SpreadParams& p, Cursor& u, int* ring) {  // thread 0
+  if (!u.valid || ++u.c < u.nch) return;
+  ++u.k;
+  const int w = atomicAdd(p.tc_counter, 1);
+  ring[u.k & (kRing - 1)] = w;
+  cursor_load(p, u, w);
+}
+
 template <int N>
 __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc_kernel(const SpreadParams p) {
   constexpr int A_BYTES = kTM * kKC * 4;          // 8 KB: [kKC/4][128][4]
@@ -107,12 +142,26 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc_kernel(const SpreadPa
   __shared__ uint64_t rec_bar[kRecSlots];
   __shared__ __align__(16) float recbuf[kRecSlots * kKC * 32];
   __shared__ uint32_t tmem_base_s;
+  __shared__ int ring[kRing];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int4 tile = p.tc_tiles[blockIdx.x / p.tc_tblocks];  // {first record, records, row0, col0}
-  const int tb = blockIdx.x % p.tc_tblocks;
-  const int t0 = p.t_begin + tb * N;
-  const int nch = tile.y / kKC;
+  const int q4 = warp & 3;
+
+  // ---- empty tiles (no sensor meets them): zeros, one warp per point row
+  for (int i = p.tc_nonempty + blockIdx.x; i < p.tc_ntiles; i += gridDim.x) {
+    const int4 t = __ldg(&p.tc_tiles[i]);
+    const int len = p.t_end - p.t_begin;
+    for (int pt = warp; pt < kTM; pt += kThreadsTC / 32) {
+      float* o = p.grid + ((size_t)(t.z + pt / kTC) * p.ncols + (t.w + pt % kTC)) * p.T + p.t_begin;
+      for (int q = lane * 4; q < len; q += 128) *reinterpret_cast<float4*>(o + q) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  Cursor cur, cs, cr;  // stage being built, sample prefetch (+2), record prefetch (+3, thread 0)
+  if (tid == 0) ring[0] = atomicAdd(p.tc_counter, 1);
+  __syncthreads();
+  cur.k = 0;
+  cursor_load(p, cur, ring[0]);
+  if (!cur.valid) return;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base_s)),
@@ -131,26 +180,33 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc_kernel(const SpreadPa
 
   // A producer: grid point pa (row pr, column pc), k-quads ga0, ga0 + 1
   const int pa = tid & (kTM - 1), pr = pa / kTC, pc = pa % kTC, ga0 = (tid >> 7) * 2;
-  const float* __restrict__ recs = p.tc_recs + (size_t)tile.x * 32;
-  // records: 3-slot ring filled by bulk (TMA) copies two stages ahead
-  auto fetch_recs = [&](int c) {
-    const int r = c % kRecSlots;
+  // records: 4-slot ring filled by bulk (TMA) copies three stages ahead (thread 0 only)
+  auto fetch_recs = [&](int g, const Cursor& u) {
+    const int r = g % kRecSlots;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rec_bar[r])), "r"(REC_BYTES)
                  : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      su32(recbuf + r * kKC * 32)),
-                 "l"(recs + (size_t)c * kKC * 32), "r"(REC_BYTES), "r"(su32(&rec_bar[r]))
+                 "l"(p.tc_recs + ((size_t)u.rec0 + (size_t)u.c * kKC) * 32), "r"(REC_BYTES), "r"(su32(&rec_bar[r]))
                  : "memory");
   };
-  if (tid == 0)
-    for (int c = 0; c < nch && c < kRecSlots - 1; ++c) fetch_recs(c);
-  // B producer: samples of the next stage prefetched into registers,
+  if (tid == 0) {
+    cr = cur;
+    for (int g = 0; g < kRecSlots - 1 && cr.valid; ++g) {
+      fetch_recs(g, cr);
+      cursor_claim(p, cr, ring);
+    }
+  }
+  __syncthreads();  // ring entries of the first stages
+  // B producer: samples prefetched into registers two stages ahead (two
+  // register sets, the stage loop is unrolled by two so indices stay static):
   // sv[i][k] = S[sensor k][t0 + tid + 256 i]
-  float sv[NI][kKC];
-  auto load_samples = [&](int c) {
-    const int r = c % kRecSlots;
-    mbar_wait_tc(&rec_bar[r], (c / kRecSlots) & 1);
+  float sv0[NI][kKC], sv1[NI][kKC];
+  auto load_samples = [&](int g, const Cursor& u, float (&sv)[NI][kKC]) {
+    const int r = g % kRecSlots;
+    mbar_wait_tc(&rec_bar[r], (g / kRecSlots) & 1);
     const float* rb = recbuf + r * kKC * 32;
+    const int t0 = p.t_begin + u.tb * N;
 #pragma unroll
     for (int k = 0; k < kKC; ++k) {
       const float* __restrict__ srow = p.samples + (size_t)__float_as_int(rb[k * 32]) * p.T + t0;
@@ -159,28 +215,68 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc_kernel(const SpreadPa
         if (tid + i * kThreadsTC < N) sv[i][k] = __ldg(srow + tid + i * kThreadsTC);
     }
   };
-  if (nch > 0) load_samples(0);
+  cs = cur;
+  load_samples(0, cs, sv0);
+  cursor_next(p, cs, ring);
+  if (cs.valid) load_samples(1, cs, sv1);
+  cursor_next(p, cs, ring);
 
-  for (int c = 0; c < nch; ++c) {
-    const int s = c & 1;
-    if (c >= kStages) mbar_wait_tc(&mma_bar[s], ((c >> 1) - 1) & 1);
+  auto epilogue = [&](int g) {
+    const int t0 = p.t_begin + cur.tb * N;
+    mbar_wait_tc(&mma_bar[g & 1], (g >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float* stg = reinterpret_cast<float*>(smem) + warp * 32 * 36;
+#pragma unroll 1
+    for (int j = warp >> 2; j < N / 32; j += kThreadsTC / 128) {
+      uint32_t r[32];
+      const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(j * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+          "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(ta));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<uint4*>(stg + lane * 36 + 4 * q) = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int pl = q * 4 + (lane >> 3), pt = q4 * 32 + pl;  // point within the tile
+        const float4 v = *reinterpret_cast<const float4*>(stg + pl * 36 + (lane & 7) * 4);
+        float* o = p.grid + ((size_t)(cur.row0 + pt / kTC) * p.ncols + (cur.col0 + pt % kTC)) * p.T + t0 + j * 32;
+        *reinterpret_cast<float4*>(o + (lane & 7) * 4) = v;
+      }
+      __syncwarp();
+    }
+    // TMEM and the staging area (stage slot 0) are reused by the next stages
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+  };
+
+  auto stage = [&](int g, float (&sv)[NI][kKC]) {
+    const int s = g & 1;
+    if (g >= kStages) mbar_wait_tc(&mma_bar[s], ((g >> 1) - 1) & 1);
     uint8_t* st = smem + s * STAGE;
     float* Ahi = reinterpret_cast<float*>(st);
     float* Alo = reinterpret_cast<float*>(st + A_BYTES);
     float* Bhi = reinterpret_cast<float*>(st + 2 * A_BYTES);
     float* Blo = reinterpret_cast<float*>(st + 2 * A_BYTES + B_BYTES);
-    const float* rb = recbuf + (c % kRecSlots) * kKC * 32;
+    const float* rb = recbuf + (g % kRecSlots) * kKC * 32;
     // ---- A: W[p][k] = wrow[k][pr] * wcol[k][pc], K-major [k/4][p][4]
 #pragma unroll
-    for (int g = ga0; g < ga0 + 2; ++g) {
-      const float4 v = make_float4(rb[(g * 4 + 0) * 32 + 8 + pr] * rb[(g * 4 + 0) * 32 + 16 + pc],
-                                   rb[(g * 4 + 1) * 32 + 8 + pr] * rb[(g * 4 + 1) * 32 + 16 + pc],
-                                   rb[(g * 4 + 2) * 32 + 8 + pr] * rb[(g * 4 + 2) * 32 + 16 + pc],
-                                   rb[(g * 4 + 3) * 32 + 8 + pr] * rb[(g * 4 + 3) * 32 + 16 + pc]);
+    for (int gq = ga0; gq < ga0 + 2; ++gq) {
+      const float4 v = make_float4(rb[(gq * 4 + 0) * 32 + 8 + pr] * rb[(gq * 4 + 0) * 32 + 16 + pc],
+                                   rb[(gq * 4 + 1) * 32 + 8 + pr] * rb[(gq * 4 + 1) * 32 + 16 + pc],
+                                   rb[(gq * 4 + 2) * 32 + 8 + pr] * rb[(gq * 4 + 2) * 32 + 16 + pc],
+                                   rb[(gq * 4 + 3) * 32 + 8 + pr] * rb[(gq * 4 + 3) * 32 + 16 + pc]);
       float4 h, l;
       split_tf32(v, h, l);
-      *reinterpret_cast<float4*>(Ahi + g * (A_LBO / 4) + pa * 4) = h;
-      *reinterpret_cast<float4*>(Alo + g * (A_LBO / 4) + pa * 4) = l;
+      *reinterpret_cast<float4*>(Ahi + gq * (A_LBO / 4) + pa * 4) = h;
+      *reinterpret_cast<float4*>(Alo + gq * (A_LBO / 4) + pa * 4) = l;
     }
     // ---- B: K-major [k/4][n][4], thread = time sample, 4 sensors per 16-byte store
 #pragma unroll
@@ -208,63 +304,29 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc_kernel(const SpreadPa
         const uint64_t dal = umma_desc(a_lo + ks * 2 * A_LBO, A_LBO, A_SBO);
         const uint64_t dbh = umma_desc(b_hi + ks * 2 * B_LBO, B_LBO, B_SBO);
         const uint64_t dbl = umma_desc(b_lo + ks * 2 * B_LBO, B_LBO, B_SBO);
-        umma_tf32(tmem, dah, dbh, IDESC, (c | ks) ? 1u : 0u);
+        umma_tf32(tmem, dah, dbh, IDESC, (cur.c | ks) ? 1u : 0u);
         umma_tf32(tmem, dah, dbl, IDESC, 1u);
         umma_tf32(tmem, dal, dbh, IDESC, 1u);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        su32(&mma_bar[s]))
                    : "memory");
-      // slot (c + 2) % 3 was last read in iteration c - 1 (before this iteration's barrier)
-      if (c + kRecSlots - 1 < nch) fetch_recs(c + kRecSlots - 1);
+      // slot (g + 3) % 4 was last read in stage g - 1 (before this stage's barrier)
+      if (cr.valid) {
+        fetch_recs(g + kRecSlots - 1, cr);
+        cursor_claim(p, cr, ring);
+      }
     }
-    if (c + 1 < nch) load_samples(c + 1);
+    if (cs.valid) load_samples(g + 2, cs, sv);
+    cursor_next(p, cs, ring);
+    const bool last = cur.c == cur.nch - 1;
+    if (last) epilogue(g);
+    cursor_next(p, cur, ring);
+  };
+  for (int g = 0; cur.valid; g += 2) {
+    stage(g, sv0);
+    if (cur.valid) stage(g + 1, sv1);
   }
-
-  // ---- epilogue: TMEM -> registers -> shared (per-warp transpose) -> grid.
-  // Warp w reads TMEM lanes 32 (w % 4) .. +31 (grid points) and the 32-sample
-  // column blocks j = w / 4, w / 4 + 2, ...; each store instruction then
-  // writes four points x 128 contiguous bytes.
-  const int q4 = warp & 3;
-  float* stg = reinterpret_cast<float*>(smem) + warp * 32 * 36;
-  if (nch > 0) {
-    const int cl = nch - 1;
-    mbar_wait_tc(&mma_bar[cl & 1], (cl >> 1) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  }
-#pragma unroll 1
-  for (int j = warp >> 2; j < N / 32; j += kThreadsTC / 128) {
-    uint32_t r[32];
-    if (nch > 0) {
-      const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(j * 32);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-          "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-          : "r"(ta));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    } else {
-#pragma unroll
-      for (int q = 0; q < 32; ++q) r[q] = 0u;
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      *reinterpret_cast<uint4*>(stg + lane * 36 + 4 * q) = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int pl = q * 4 + (lane >> 3), pt = q4 * 32 + pl;  // point within the tile
-      const float4 v = *reinterpret_cast<const float4*>(stg + pl * 36 + (lane & 7) * 4);
-      float* o = p.grid + ((size_t)(tile.z + pt / kTC) * p.ncols + (tile.w + pt % kTC)) * p.T + t0 + j * 32;
-      *reinterpret_cast<float4*>(o + (lane & 7) * 4) = v;
-    }
-    __syncwarp();
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
 }
 
@@ -275,10 +337,17 @@ cudaError_t go_tc(const SpreadParams& p, cudaStream_t s) {
   auto k = spread_tc_kernel<N>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err) return err;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   SpreadParams q = p;
   q.tc_tblocks = (p.t_end - p.t_begin) / N;
-  const unsigned blocks = (unsigned)(q.tc_ntiles * q.tc_tblocks);
-  if (blocks) k<<<blocks, kThreadsTC, smem, s>>>(q);
+  const int blocks = std::min(q.tc_ntiles * q.tc_tblocks, 2 * sms);
+  if ((err = cudaMemsetAsync(q.tc_counter, 0, sizeof(int), s))) return err;
+  if (blocks > 0 && q.tc_tblocks > 0) k<<<blocks, kThreadsTC, smem, s>>>(q);
   return cudaGetLastError();
 }
 

@@ -59,6 +59,8 @@ int main(int argc, char** argv) {
   p.tc_recs = dr;
   p.tc_tiles = dt;
   p.tc_ntiles = 1;
+  p.tc_nonempty = 1;
+  cudaMalloc(&p.tc_counter, sizeof(int));
   p.tc_n = spread_tc_block(T);
   cudaError_t e = launch_spread_tc(p, 0);
   cudaError_t e2 = cudaDeviceSynchronize();
