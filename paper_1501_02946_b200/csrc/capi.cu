@@ -544,11 +544,13 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
       start[t + 1] = start[t] + padded[t];
     }
     if (start[ntiles] > (int64_t)INT32_MAX / 32) return fail(PATFFT_ERR_UNSUPPORTED, "too many gridding records");
+    if ((int64_t)M * T > (int64_t)UINT32_MAX) return fail(PATFFT_ERR_UNSUPPORTED, "sample array too large for 32-bit offsets");
     tcrec.assign((size_t)start[ntiles] * 32, 0.f);
     std::vector<int64_t> fill(start.begin(), start.end() - 1);
     for (const Pair& q : pairs) {
       float* o = &tcrec[(size_t)fill[q.tile]++ * 32];
-      std::memcpy(&o[0], &q.m, 4);
+      const uint32_t soff = (uint32_t)q.m * (uint32_t)T;  // sample row offset (elements)
+      std::memcpy(&o[0], &soff, 4);
       std::copy(q.wr, q.wr + 8, o + 8);
       std::copy(q.wc, q.wc + 16, o + 16);
     }

@@ -50,7 +50,7 @@ struct SpreadParams {
   int T, ncols, nrows;
   int t_begin, t_end;     // time range processed by this launch (multiples of 128)
   // tensor-core gridding (spread_tc.cu); tc_tiles == nullptr selects the SIMT kernels
-  const float* tc_recs = nullptr;   // [records][32]: sensor id, 8 row weights at [8], 16 column weights at [16]
+  const float* tc_recs = nullptr;   // [records][32]: sample row offset m*T (u32), row weights at [8..15], column weights at [16..31]
   const int4* tc_tiles = nullptr;   // per tile (launch order): {first record, records (multiple of 16), row0, col0}
   int tc_ntiles = 0, tc_nonempty = 0;  // tiles (the non-empty ones first, longest first)
   int tc_n = 0, tc_tblocks = 0;       // time samples per block, time blocks per launch

@@ -88,7 +88,12 @@ __device__ __forceinline__ void split_tf32(float4 v, float4& h, float4& l) {
   h.y = __uint_as_float((__float_as_uint(v.y) + 0x1000u) & 0xFFFFE000u);
   h.z = __uint_as_float((__float_as_uint(v.z) + 0x1000u) & 0xFFFFE000u);
   h.w = __uint_as_float((__float_as_uint(v.w) + 0x1000u) & 0xFFFFE000u);
-  l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+  float2 l01, l23;
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tsub.rn.f32x2 d, a, b;\n\t"
+      "mov.b64 {%0, %1}, d;\n}" : "=f"(l01.x), "=f"(l01.y) : "f"(v.x), "f"(v.y), "f"(h.x), "f"(h.y));
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tsub.rn.f32x2 d, a, b;\n\t"
+      "mov.b64 {%0, %1}, d;\n}" : "=f"(l23.x), "=f"(l23.y) : "f"(v.z), "f"(v.w), "f"(h.z), "f"(h.w));
+  l = make_float4(l01.x, l01.y, l23.x, l23.y);
 }
 
 // Position in a CTA's stage sequence.  Work items w = (tile w / tblocks,
@@ -207,12 +212,13 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc_kernel(const SpreadPa
     mbar_wait_tc(&rec_bar[r], (g / kRecSlots) & 1);
     const float* rb = recbuf + r * kKC * 32;
     const int t0 = p.t_begin + u.tb * N;
+    const uint32_t base = (uint32_t)(t0 + tid);
 #pragma unroll
     for (int k = 0; k < kKC; ++k) {
-      const float* __restrict__ srow = p.samples + (size_t)__float_as_int(rb[k * 32]) * p.T + t0;
+      const uint32_t off = __float_as_uint(rb[k * 32]) + base;  // record word 0: sensor row offset m * T
 #pragma unroll
       for (int i = 0; i < NI; ++i)
-        if (tid + i * kThreadsTC < N) sv[i][k] = __ldg(srow + tid + i * kThreadsTC);
+        if (tid + i * kThreadsTC < N) sv[i][k] = __ldg(p.samples + (off + i * kThreadsTC));
     }
   };
   cs = cur;

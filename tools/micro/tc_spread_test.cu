@@ -23,14 +23,16 @@ int main(int argc, char** argv) {
   if (mode == 2) for (int m = 0; m < M; ++m) samples[(size_t)m * T + (m % T)] = 1.f + m;
   for (int k = 0; k < nsens; ++k) {
     int m = (k * 7) % M;
-    std::memcpy(&recs[k * 32], &m, 4);
+    unsigned off = (unsigned)m * T;
+    std::memcpy(&recs[k * 32], &off, 4);
     for (int r = 0; r < 8; ++r) recs[k * 32 + 8 + r] = mode ? (mode == 2 ? (r == (k % 8)) : 1.f) : U(rng);
     for (int c = 0; c < 16; ++c) recs[k * 32 + 16 + c] = mode ? (mode == 2 ? (c == (k % 16)) : 1.f) : U(rng);
   }
   std::vector<double> want((size_t)nrows * ncols * T, 0.0);
   for (int k = 0; k < nsens; ++k) {
-    int m;
-    std::memcpy(&m, &recs[k * 32], 4);
+    unsigned off;
+    std::memcpy(&off, &recs[k * 32], 4);
+    int m = off / T;
     for (int r = 0; r < 8; ++r)
       for (int c = 0; c < 16; ++c)
         for (int t = 0; t < T; ++t)
