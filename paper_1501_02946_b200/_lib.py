@@ -79,6 +79,7 @@ _SIGS = {
     "patfft_nedner_stage_name": (ctypes.c_char_p, [ctypes.c_int]),
     "patfft_nedner_stage_bytes": (ctypes.c_int, [_P, _D, ctypes.c_int]),
     "patfft_nedner_launches_per_execute": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    "patfft_nedner_spread_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
     "patfft_last_error": (ctypes.c_char_p, []),
     "patfft_version": (ctypes.c_char_p, []),
     "patfft_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),

@@ -1243,6 +1243,16 @@ int patfft_nedner_launches_per_execute(const patfft_nedner_plan* P, int* own, in
   return PATFFT_OK;
 }
 
+int patfft_nedner_spread_info(const patfft_nedner_plan* P, int64_t info[4]) {
+  if (!P || !info) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  const bool tc = P->tc_ntiles > 0;
+  info[0] = tc ? 1 : 0;                        // 1: tensor-core gridding (spread_tc.cu)
+  info[1] = tc ? P->tc_records : P->n_records;  // records (tile x sensor pairs, padded to 16 per tile)
+  info[2] = tc ? P->tc_ntiles : P->nblk;        // tiles / SIMT blocks
+  info[3] = tc ? P->tc_n : 0;                   // time samples per tensor-core item
+  return PATFFT_OK;
+}
+
 // ---- helpers ---------------------------------------------------------------
 int patfft_device_count(int* count) {
   CUDA_TRY(cudaGetDeviceCount(count));
