@@ -590,6 +590,23 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   const Window& wt = P->win_t;
   const double norm_t = 1.0 / (2.0 * M_PI * wt.c_eff);  // nufft.py:284
   const double psh0 = kb_psihat(wt, 0.0);
+  // DCT form of the NER transform (ner.cu, ner_dct_kernel): pre[n] = the
+  // Makhoul twiddle exp(i pi n / (4T)) times the pre-window of the even
+  // extension sample that lands in slot n of the length-2T DCT-III input
+  std::vector<float2> pre(n_ext, make_float2(0.f, 0.f));
+  for (int nn = 1; nn < n_ext; ++nn) {
+    if (nn == P->T) continue;
+    const int i = nn < P->T ? P->T + nn : 3 * P->T - nn;  // ext index
+    const double w = psh0 * norm_t / kb_psi(wt, 2.0 * M_PI * i / n_ext - M_PI);
+    const double a = M_PI * nn / (2.0 * n_ext);
+    double re = w * std::cos(a), im = w * std::sin(a);
+    if (nn > P->T) {  // -i * (re + i im)
+      const double t = re;
+      re = im;
+      im = -t;
+    }
+    pre[nn] = make_float2((float)re, (float)im);
+  }
   std::vector<float> iw(n_ext);
   for (int i = 0; i < n_ext; ++i) {
     const double th = 2.0 * M_PI * i / n_ext - M_PI;  // nufft.py:281
@@ -634,6 +651,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   if ((rc = upload(&P->d_jt0, jt0))) return rc;
   if ((rc = upload(&P->d_jt1, jt1))) return rc;
   if ((rc = upload(&P->d_iw, iw))) return rc;
+  if ((rc = upload(&P->d_pre, pre))) return rc;
   if ((rc = upload(&P->d_tw, tw))) return rc;
   if ((rc = dalloc(&P->d_grid, (size_t)nrows * ncols * T))) return rc;
   if ((rc = dalloc(&P->d_Y, (size_t)nrows * P->N1h * T))) return rc;
@@ -680,6 +698,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   q.gh = P->d_gh;
   q.z = P->d_z;
   q.iw = P->d_iw;
+  q.pre = P->d_pre;
   q.tw = P->d_tw;
   q.jt0 = P->d_jt0;
   q.jt1 = P->d_jt1;
@@ -1164,7 +1183,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->have_l) cufftDestroy(P->fft_l);
   for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_gh,
                   (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_tc_recs, (void*)P->d_tc_tiles, (void*)P->d_tc_counter, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
-                  (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_tw, (void*)P->d_jt0,
+                  (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_pre, (void*)P->d_tw, (void*)P->d_jt0,
                   (void*)P->d_jt1})
     free_dev(p);
   if (P->stream2) cudaStreamSynchronize(P->stream2);

@@ -19,6 +19,8 @@
 //     two rows for the lateral Nyquist split).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "fft_smem.cuh"
 #include "patfft_internal.h"
 
@@ -313,6 +315,129 @@ __global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_k
   }
 }
 
+// DCT form of the compile-time NER kernel (T = 2^LOGT, n_over = 4T, default
+// window, upsample 1).  The rotated, windowed even extension x (x[-m] =
+// x[m], support |m| < T) makes its 4T-point spectrum D[k] = 2 sum_m x_m
+// cos(pi m k / 2T) even, so half the FFT is redundant.  The interpolation
+// grid is shifted by half a bin, bins at (k + 1/2) / c: the Kaiser-Bessel
+// identity holds for any grid offset (nufft.py:287-293 with kappa -> kappa -
+// 1/(2c)), the tap weights keep their form in z = frac(c kappa - 1/2) - 1/2,
+// and the rotation still absorbs the per-tap phase.  On that grid
+//   D'[q] = 2 sum_{m<T} x_m cos(pi m (2q + 1) / 4T),   q = 0 .. 2T-1,
+// is a DCT-III of length 2T, computed with ONE 2T-point complex inverse FFT
+// (Makhoul): input W_n = exp(i pi n / 4T) (x_n - i x_{2T-n}) (table pre[]
+// times the gh sample), output D'[2j] = Z[j], D'[2j+1] = Z[2T-1-j]; bins
+// outside [0, 2T) fold by D'[-1-q] = D'[q] = D'[4T-1-q].  Half the points and
+// one radix stage fewer than the 4T-point FFT of the plain form.
+template <int K2, int D, int LOGT>
+__global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_dct_kernel(const NerParams p) {
+  constexpr int T = 1 << LOGT;
+  constexpr int NTH = ner_ct_threads(LOGT);
+  constexpr int L = LOGT + 1;  // DCT length 2T
+  constexpr int N2 = 2 * T;
+  constexpr int K = K2 / 2;
+  extern __shared__ float2 sbuf[];
+  const int rl = blockIdx.x;
+  const int r = p.row0 + rl;
+  const int tid = threadIdx.x;
+  const int tci = p.in_tchunk;
+  const float2* __restrict__ g = p.gh + (size_t)rl * tci;
+  const size_t gstride = (size_t)p.rows_local * tci;
+  auto gload = [&](int t) { return __ldcs(&g[(t >> p.in_tshift) * gstride + (t & p.in_tmask)]); };
+
+  // 1. DCT-III of the windowed half extension via a 2T-point inverse FFT
+  fft::fft_ct_loaded<true, L, 4, true, 0, NTH>(sbuf, p.tw, tid, fft::SwzC<L>(), [&](int n, int) {
+    if (n == 0 || n == T) return make_float2(0.f, 0.f);
+    const float2 gv = gload(n < T ? T - n : n - T);
+    return fft::cmul(gv, __ldg(&p.pre[n]));
+  });
+  const fft::SwzC<L> ad;
+
+  // 2. targets (as ner_kernel)
+  const int j0w = r / p.N1h;
+  const int j1 = r - j0w * p.N1h;
+  const double j2 = p.jt0[j0w] + p.jt1[j1];  // recon.py:210-214 summation order
+  constexpr double halfT = (double)T / 2.0;
+  constexpr double band_r2 = halfT * halfT;
+  auto interp_D = [&](double ke) {
+    const double xi = __dmul_rn(p.c_eff, ke) - 0.5;  // half-bin grid
+    const double k0d = floor(xi);
+    const int k0 = (int)k0d;
+    const float z = (float)(xi - k0d) - 0.5f;
+    const float z2 = z * z;
+    // D'[k]: fold into [0, 2T), then the Makhoul output permutation
+    auto at = [&](int k) {
+      int km = k & (4 * T - 1);
+      km = km >= N2 ? (~km) & (4 * T - 1) : km;
+      const int idx = (km >> 1) ^ ((km & 1) ? (N2 - 1) : 0);
+      return sbuf[ad(idx, 0)];
+    };
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      constexpr int DE = D % 2 ? D - 1 : D;
+      constexpr int DO = D % 2 ? D : D - 1;
+      float2 eo = make_float2(p.poly[j][DE], p.poly[j][DO]);
+#pragma unroll
+      for (int s2 = 1; s2 <= DO / 2; ++s2)
+        eo = fft::f2fma(eo, make_float2(z2, z2), make_float2(p.poly[j][DE - 2 * s2], p.poly[j][DO - 2 * s2]));
+#pragma unroll
+      for (int d = DE - 2 * (DO / 2) - 2; d >= 0; d -= 2) eo.x = fmaf(eo.x, z2, p.poly[j][d]);
+      const float wa = fmaf(z, eo.y, eo.x);
+      const float wb = fmaf(-z, eo.y, eo.x);
+      const float2 Fa = at(k0 + j - K + 1);
+      const float2 Fb = at(k0 + K - j);
+      acc = fft::f2fma(Fa, make_float2(wa, wa), fft::f2fma(Fb, make_float2(wb, wb), acc));
+    }
+    return acc;
+  };
+  constexpr int kPairs = (T / 2 + NTH) / NTH;  // |l| in [0, T/2]
+  float2 valsP[kPairs], valsM[kPairs];
+  const float2 g0 = gload(0);
+#pragma unroll
+  for (int it = 0; it < kPairs; ++it) {
+    const int lh = tid + it * NTH;
+    float2 vp = make_float2(0.f, 0.f), vm = make_float2(0.f, 0.f);
+    if (lh <= T / 2 && lh > 0) {
+      const double lv = __dmul_rn(__dmul_rn((double)lh, 1.0 / (double)T), (double)T);  // fftfreq(T)*T
+      const double r2 = __dadd_rn(j2, __dmul_rn(lv, lv));
+      if (r2 <= band_r2) {
+        const double kap = sqrt(r2);
+        const double ke = 2.0 * kap;
+        const float2 Dv = interp_D(ke);
+        const double red = ke - 2.0 * floor(0.5 * ke + 0.5);
+        const float2 cs = cospi_sinpi((float)red);  // (cos, sin)(pi kappa_e)
+        const float amp = __fdividef(2.f * (float)lv, (float)kap);
+        const float a = 0.5f * amp * p.scale;
+        const float rx = Dv.x * cs.x, ry = Dv.y * cs.x, sx = Dv.x * cs.y, sy = Dv.y * cs.y;
+        vp = make_float2(a * (rx + sy + g0.x), a * (ry - sx + g0.y));  // e^{-i pi ke} D + g0
+        vm = make_float2(a * (rx - sy + g0.x), a * (ry + sx + g0.y));  // e^{+i pi ke} D + g0
+      }
+    }
+    valsP[it] = vp;
+    valsM[it] = vm;
+  }
+
+  // 3. depth inverse FFT (recon.py:255) straight to z (up == 1: row j0w * N1h + j1)
+  __syncthreads();  // spectrum fully consumed
+  {
+    const fft::SwzC<LOGT> iad;
+#pragma unroll
+    for (int it = 0; it < kPairs; ++it) {
+      const int lh = tid + it * NTH;
+      if (lh > T / 2) break;
+      if (lh < T / 2) sbuf[iad(fft::brev(lh, LOGT), 0)] = valsP[it];
+      if (lh > 0) sbuf[iad(fft::brev(T - lh, LOGT), 0)] = valsM[it];
+    }
+  }
+  __syncthreads();
+  const int tco = p.out_tchunk;
+  const size_t zstride = (size_t)p.rows_out * tco;
+  float2* __restrict__ z0 = p.z + (size_t)(r - p.out_row0) * tco;
+  fft::fft_ct_stored<true, LOGT, PATFFT_NER_INV_MAXR, true, 0, NTH>(
+      sbuf, p.tw, tid, fft::SwzC<LOGT>(), [&](int i, int, float2 v) { z0[(i >> p.out_tshift) * zstride + (i & p.out_tmask)] = v; });
+}
+
 }  // namespace
 
 size_t ner_smem_bytes(int n_over, int Tu) {
@@ -342,6 +467,28 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
   // upsample 1 and T = 2^7 .. 2^11
   const bool ct_ok = K2 == 12 && degree == 8 && p.fused_ifft && p.up == 1 && p.n_over == 4 * p.T &&
                      p.Tu == p.T && p.log_n_over >= 9 && p.log_n_over <= 13;
+  static const bool dct = [] {
+    const char* e = std::getenv("PATFFT_NER_DCT");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  if (ct_ok && dct && p.n_lat >= 1 && p.pre) {
+    // DCT form: 2T-point transform, half the shared memory
+    threads = ner_threads(p.n_over);
+    const size_t smem2 = (size_t)2 * p.T * sizeof(float2);
+    auto go2 = [&](auto kern) {
+      err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+      if (err != cudaSuccess) return;
+      kern<<<rows, threads, smem2, s>>>(p);
+      err = cudaGetLastError();
+    };
+    switch (p.log_n_over - 2) {
+      case 7: go2(ner_dct_kernel<12, 8, 7>); return err;
+      case 8: go2(ner_dct_kernel<12, 8, 8>); return err;
+      case 9: go2(ner_dct_kernel<12, 8, 9>); return err;
+      case 10: go2(ner_dct_kernel<12, 8, 10>); return err;
+      case 11: go2(ner_dct_kernel<12, 8, 11>); return err;
+    }
+  }
   if (ct_ok) {
     threads = ner_threads(p.n_over);
     switch (p.log_n_over - 2) {

@@ -79,6 +79,7 @@ struct NerParams {
   const float2* gh;    // [N0][N1h][T]
   float2* z;           // [N0u][N1uh][Tu]
   const float* iw;     // [2T] psihat(0)*norm/psi(theta_n) (nufft.py:281-284)
+  const float2* pre;   // [2T] DCT-III input twiddle x pre-window (ner_dct_kernel)
   const float2* tw;    // exp(-2 pi i k / 2^14)
   const double* jt0;   // [N0] (j0*ratio0)^2 on the wrapped grid (recon.py:211)
   const double* jt1;   // [N1h]
@@ -175,6 +176,7 @@ struct patfft_nedner_plan {
   float* d_dp0 = nullptr;
   float* d_dp1 = nullptr;
   float* d_iw = nullptr;
+  float2* d_pre = nullptr;
   float2* d_tw = nullptr;
   double* d_jt0 = nullptr;
   double* d_jt1 = nullptr;
