@@ -19,6 +19,7 @@
 //     two rows for the lateral Nyquist split).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "fft_smem.cuh"
@@ -329,10 +330,47 @@ __global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_k
 // times the gh sample), output D'[2j] = Z[j], D'[2j+1] = Z[2T-1-j]; bins
 // outside [0, 2T) fold by D'[-1-q] = D'[q] = D'[4T-1-q].  Half the points and
 // one radix stage fewer than the 4T-point FFT of the plain form.
+// Last radix-2^R pass of a compile-time transform, in place: every thread
+// first reads and transforms all of its items, then (after a barrier) hands
+// each output, natural index n, to store(n, v) -- which may write anywhere in
+// the same buffer.  No trailing barrier.
+template <int R, bool INV, int L, int LOGH, int NTH, class Addr, class Store>
+__device__ __forceinline__ void last_pass_inplace(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
+                                                  Addr addr, Store store) {
+  constexpr int PR = 1 << R;
+  constexpr int H = 1 << LOGH;
+  constexpr int ITEMS = 1 << (L - R);
+  constexpr int ITER = (ITEMS + NTH - 1) / NTH;
+  float2 e[ITER][PR];
+  int base[ITER];
+#pragma unroll
+  for (int j = 0; j < ITER; ++j) {
+    const int q = tid + j * NTH;
+    base[j] = -1;
+    if ((ITEMS % NTH) != 0 && q >= ITEMS) continue;
+    const int k = q & (H - 1);
+    base[j] = ((q >> LOGH) << (LOGH + R)) + k;
+    const int ab = addr(base[j], 0);
+#pragma unroll
+    for (int m = 0; m < PR; ++m) e[j][m] = buf[ab ^ addr(m * H, 0)];
+    fft::pass_butterflies<R, INV, LOGH>(e[j], k, tw);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < ITER; ++j) {
+    if (base[j] < 0) continue;
+#pragma unroll
+    for (int m = 0; m < PR; ++m) store(base[j] + m * H, e[j][m]);
+  }
+}
+
+constexpr int ner_dct_threads(int logt) { return (1 << logt) / 8 < 64 ? 64 : ((1 << logt) / 8 > 512 ? 512 : (1 << logt) / 8); }
+constexpr int ner_dct_minb(int logt) { return (65536 / 80) / ner_dct_threads(logt); }
+
 template <int K2, int D, int LOGT>
-__global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_dct_kernel(const NerParams p) {
+__global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner_dct_kernel(const NerParams p) {
   constexpr int T = 1 << LOGT;
-  constexpr int NTH = ner_ct_threads(LOGT);
+  constexpr int NTH = ner_dct_threads(LOGT);
   constexpr int L = LOGT + 1;  // DCT length 2T
   constexpr int N2 = 2 * T;
   constexpr int K = K2 / 2;
@@ -345,13 +383,22 @@ __global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_d
   const size_t gstride = (size_t)p.rows_local * tci;
   auto gload = [&](int t) { return __ldcs(&g[(t >> p.in_tshift) * gstride + (t & p.in_tmask)]); };
 
-  // 1. DCT-III of the windowed half extension via a 2T-point inverse FFT
-  fft::fft_ct_loaded<true, L, 4, true, 0, NTH>(sbuf, p.tw, tid, fft::SwzC<L>(), [&](int n, int) {
+  // 1. DCT-III of the windowed half extension via a 2T-point inverse FFT;
+  // the last pass stores D'[q] in natural order (Makhoul output permutation
+  // Z[n] -> D'[n < 2T/2 ? 2n : 4T-1-2n]) into the same swizzled buffer
+  const fft::SwzC<L> ad;
+  fft::fft_ct_loaded<true, L, 4, true, 0, NTH, true>(sbuf, p.tw, tid, ad, [&](int n, int) {
     if (n == 0 || n == T) return make_float2(0.f, 0.f);
     const float2 gv = gload(n < T ? T - n : n - T);
     return fft::cmul(gv, __ldg(&p.pre[n]));
   });
-  const fft::SwzC<L> ad;
+  {
+    constexpr int LH = fft::LastPassLogh<L, 4, true>::value;
+    last_pass_inplace<L - LH, true, L, LH, NTH>(sbuf, p.tw, tid, ad, [&](int n, float2 v) {
+      sbuf[ad(n < T ? 2 * n : 4 * T - 1 - 2 * n, 0)] = v;
+    });
+  }
+  __syncthreads();
 
   // 2. targets (as ner_kernel)
   const int j0w = r / p.N1h;
@@ -365,12 +412,15 @@ __global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_d
     const int k0 = (int)k0d;
     const float z = (float)(xi - k0d) - 0.5f;
     const float z2 = z * z;
-    // D'[k]: fold into [0, 2T), then the Makhoul output permutation
+    // D'[k] in natural order; taps outside [0, 2T) (targets at the ends of the
+    // band) fold by D'[-1-q] = D'[q] = D'[4T-1-q]
+    const bool edge = k0 < K - 1 || k0 + K >= N2;
     auto at = [&](int k) {
-      int km = k & (4 * T - 1);
-      km = km >= N2 ? (~km) & (4 * T - 1) : km;
-      const int idx = (km >> 1) ^ ((km & 1) ? (N2 - 1) : 0);
-      return sbuf[ad(idx, 0)];
+      if (edge) {
+        k &= 4 * T - 1;
+        k = k >= N2 ? (~k) & (4 * T - 1) : k;
+      }
+      return sbuf[ad(k, 0)];
     };
     float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
@@ -471,9 +521,9 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
     const char* e = std::getenv("PATFFT_NER_DCT");
     return e ? std::atoi(e) != 0 : true;
   }();
-  if (ct_ok && dct && p.n_lat >= 1 && p.pre) {
+  if (ct_ok && dct && p.pre) {
     // DCT form: 2T-point transform, half the shared memory
-    threads = ner_threads(p.n_over);
+    threads = std::max(64, std::min(512, p.T / 8));
     const size_t smem2 = (size_t)2 * p.T * sizeof(float2);
     auto go2 = [&](auto kern) {
       err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
