@@ -364,7 +364,16 @@ __device__ __forceinline__ void last_pass_inplace(float2* __restrict__ buf, cons
   }
 }
 
-constexpr int ner_dct_threads(int logt) { return (1 << logt) / 8 < 64 ? 64 : ((1 << logt) / 8 > 512 ? 512 : (1 << logt) / 8); }
+#ifndef PATFFT_NER_DCT_DIV
+#define PATFFT_NER_DCT_DIV 8  // threads per CTA = T / 8 (measured: 4 and 16 slower)
+#endif
+#ifndef PATFFT_NER_DCT_MAXR
+#define PATFFT_NER_DCT_MAXR 4
+#endif
+constexpr int ner_dct_threads(int logt) {
+  return (1 << logt) / PATFFT_NER_DCT_DIV < 64 ? 64
+         : ((1 << logt) / PATFFT_NER_DCT_DIV > 512 ? 512 : (1 << logt) / PATFFT_NER_DCT_DIV);
+}
 constexpr int ner_dct_minb(int logt) { return (65536 / 80) / ner_dct_threads(logt); }
 
 template <int K2, int D, int LOGT>
@@ -387,13 +396,13 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   // the last pass stores D'[q] in natural order (Makhoul output permutation
   // Z[n] -> D'[n < 2T/2 ? 2n : 4T-1-2n]) into the same swizzled buffer
   const fft::SwzC<L> ad;
-  fft::fft_ct_loaded<true, L, 4, true, 0, NTH, true>(sbuf, p.tw, tid, ad, [&](int n, int) {
+  fft::fft_ct_loaded<true, L, PATFFT_NER_DCT_MAXR, true, 0, NTH, true>(sbuf, p.tw, tid, ad, [&](int n, int) {
     if (n == 0 || n == T) return make_float2(0.f, 0.f);
     const float2 gv = gload(n < T ? T - n : n - T);
     return fft::cmul(gv, __ldg(&p.pre[n]));
   });
   {
-    constexpr int LH = fft::LastPassLogh<L, 4, true>::value;
+    constexpr int LH = fft::LastPassLogh<L, PATFFT_NER_DCT_MAXR, true>::value;
     last_pass_inplace<L - LH, true, L, LH, NTH>(sbuf, p.tw, tid, ad, [&](int n, float2 v) {
       sbuf[ad(n < T ? 2 * n : 4 * T - 1 - 2 * n, 0)] = v;
     });
@@ -523,7 +532,7 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
   }();
   if (ct_ok && dct && p.pre) {
     // DCT form: 2T-point transform, half the shared memory
-    threads = std::max(64, std::min(512, p.T / 8));
+    threads = std::max(64, std::min(512, p.T / PATFFT_NER_DCT_DIV));
     const size_t smem2 = (size_t)2 * p.T * sizeof(float2);
     auto go2 = [&](auto kern) {
       err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
