@@ -390,7 +390,13 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   const int tci = p.in_tchunk;
   const float2* __restrict__ g = p.gh + (size_t)rl * tci;
   const size_t gstride = (size_t)p.rows_local * tci;
-  auto gload = [&](int t) { return __ldcs(&g[(t >> p.in_tshift) * gstride + (t & p.in_tmask)]); };
+  const bool flat_in = p.in_tshift >= 31;  // single GPU: one time chunk per row
+  auto gload = [&](int t) {
+    return __ldcs(flat_in ? &g[t] : &g[(t >> p.in_tshift) * gstride + (t & p.in_tmask)]);
+  };
+  // natural-order D' array (after the transform): one pad slot per 16, which
+  // keeps the stride-~4 tap gathers of neighbouring threads conflict-free
+  auto dpad = [](int q) { return q + (q >> 4); };
 
   // 1. DCT-III of the windowed half extension via a 2T-point inverse FFT;
   // the last pass stores D'[q] in natural order (Makhoul output permutation
@@ -404,7 +410,7 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   {
     constexpr int LH = fft::LastPassLogh<L, PATFFT_NER_DCT_MAXR, true>::value;
     last_pass_inplace<L - LH, true, L, LH, NTH>(sbuf, p.tw, tid, ad, [&](int n, float2 v) {
-      sbuf[ad(n < T ? 2 * n : 4 * T - 1 - 2 * n, 0)] = v;
+      sbuf[dpad(n < T ? 2 * n : 4 * T - 1 - 2 * n)] = v;
     });
   }
   __syncthreads();
@@ -421,15 +427,17 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
     const int k0 = (int)k0d;
     const float z = (float)(xi - k0d) - 0.5f;
     const float z2 = z * z;
-    // D'[k] in natural order; taps outside [0, 2T) (targets at the ends of the
-    // band) fold by D'[-1-q] = D'[q] = D'[4T-1-q]
-    const bool edge = k0 < K - 1 || k0 + K >= N2;
-    auto at = [&](int k) {
-      if (edge) {
-        k &= 4 * T - 1;
-        k = k >= N2 ? (~k) & (4 * T - 1) : k;
-      }
-      return sbuf[ad(k, 0)];
+    // taps k0-K+1 .. k0+K of D' (natural order, padded).  Inside the band the
+    // taps span at most two 16-blocks: tap t sits at base0 + t or base1 + t.
+    // Targets at the ends of the band fold by D'[-1-q] = D'[q] = D'[4T-1-q].
+    const int kb = k0 - K + 1;
+    const bool edge = kb < 0 || k0 + K >= N2;
+    const int base0 = dpad(kb), tb = 16 - (kb & 15);
+    auto at = [&](int t) {
+      if (!edge) return sbuf[(t < tb ? base0 : base0 + 1) + t];
+      int k = (kb + t) & (4 * T - 1);
+      k = k >= N2 ? (~k) & (4 * T - 1) : k;
+      return sbuf[dpad(k)];
     };
     float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
@@ -444,8 +452,8 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
       for (int d = DE - 2 * (DO / 2) - 2; d >= 0; d -= 2) eo.x = fmaf(eo.x, z2, p.poly[j][d]);
       const float wa = fmaf(z, eo.y, eo.x);
       const float wb = fmaf(-z, eo.y, eo.x);
-      const float2 Fa = at(k0 + j - K + 1);
-      const float2 Fb = at(k0 + K - j);
+      const float2 Fa = at(j);
+      const float2 Fb = at(K2 - 1 - j);
       acc = fft::f2fma(Fa, make_float2(wa, wa), fft::f2fma(Fb, make_float2(wb, wb), acc));
     }
     return acc;
@@ -493,8 +501,11 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   const int tco = p.out_tchunk;
   const size_t zstride = (size_t)p.rows_out * tco;
   float2* __restrict__ z0 = p.z + (size_t)(r - p.out_row0) * tco;
+  const bool flat_out = p.out_tshift >= 31;
   fft::fft_ct_stored<true, LOGT, PATFFT_NER_INV_MAXR, true, 0, NTH>(
-      sbuf, p.tw, tid, fft::SwzC<LOGT>(), [&](int i, int, float2 v) { z0[(i >> p.out_tshift) * zstride + (i & p.out_tmask)] = v; });
+      sbuf, p.tw, tid, fft::SwzC<LOGT>(), [&](int i, int, float2 v) {
+        z0[flat_out ? (size_t)i : (i >> p.out_tshift) * zstride + (i & p.out_tmask)] = v;
+      });
 }
 
 }  // namespace
@@ -533,7 +544,7 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
   if (ct_ok && dct && p.pre) {
     // DCT form: 2T-point transform, half the shared memory
     threads = std::max(64, std::min(512, p.T / PATFFT_NER_DCT_DIV));
-    const size_t smem2 = (size_t)2 * p.T * sizeof(float2);
+    const size_t smem2 = (size_t)(2 * p.T + 2 * p.T / 16) * sizeof(float2);
     auto go2 = [&](auto kern) {
       err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
       if (err != cudaSuccess) return;
