@@ -38,14 +38,34 @@ using fft::TileAddr;
 #define PATFFT_INVCOL_STORED 1
 #endif
 
+// launch bounds (max threads, min CTAs per SM) per kernel; 512 threads is the
+// largest tile (P = 16 transforms of 512 points)
+#ifndef PATFFT_LB_COL_T
+#define PATFFT_LB_COL_T 512
+#endif
+#ifndef PATFFT_LB_COL_B
+#define PATFFT_LB_COL_B 2
+#endif
+#ifndef PATFFT_LB_ROW_T
+#define PATFFT_LB_ROW_T 512
+#endif
+#ifndef PATFFT_LB_ROW_B
+#define PATFFT_LB_ROW_B 2
+#endif
+#ifndef PATFFT_LB_INV_MINB256
+#define PATFFT_LB_INV_MINB256 5  // inverse kernels with <= 256 threads: 5 CTAs/SM (48 regs); measured 4 / 6 slower
+#endif
+
 constexpr int nth_for(int L, int PLOG) {
   return ((L >= 4 ? (1 << (L - 4)) : 1) << PLOG) < 64 ? 64
          : (((L >= 4 ? (1 << (L - 4)) : 1) << PLOG) > 512 ? 512 : ((L >= 4 ? (1 << (L - 4)) : 1) << PLOG));
 }
+constexpr int inv_lb_threads(int PLOG, int LC) { return LC > 0 ? nth_for(LC, PLOG) : 512; }
+constexpr int inv_lb_minb(int PLOG, int LC) { return inv_lb_threads(PLOG, LC) <= 256 ? PATFFT_LB_INV_MINB256 : 2; }
 
 // LC > 0: compile-time transform length 2^LC (launched with nth_for(LC, PLOG) threads)
 template <int PLOG, int LC>
-__global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
+__global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int u0 = blockIdx.x;
@@ -104,7 +124,7 @@ __global__ void __launch_bounds__(512, 2) colfft_kernel(const LateralParams p) {
 }
 
 template <int PLOG, int LC>
-__global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
+__global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int j1 = blockIdx.x;
@@ -173,7 +193,7 @@ __global__ void __launch_bounds__(512, 2) rowfft_kernel(const LateralParams p) {
 }
 
 template <int PLOG, int LC>
-__global__ void __launch_bounds__(512, 2) inv_col_kernel(const LateralParams p) {
+__global__ void __launch_bounds__(inv_lb_threads(PLOG, LC), inv_lb_minb(PLOG, LC)) inv_col_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int j1 = blockIdx.x;
@@ -208,7 +228,7 @@ __global__ void __launch_bounds__(512, 2) inv_col_kernel(const LateralParams p) 
 }
 
 template <int PLOG, int LC>
-__global__ void __launch_bounds__(512, 2) inv_c2r_kernel(const LateralParams p) {
+__global__ void __launch_bounds__(inv_lb_threads(PLOG, LC), inv_lb_minb(PLOG, LC)) inv_c2r_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
   const int n0 = blockIdx.x;
