@@ -374,7 +374,10 @@ constexpr int ner_dct_threads(int logt) {
   return (1 << logt) / PATFFT_NER_DCT_DIV < 64 ? 64
          : ((1 << logt) / PATFFT_NER_DCT_DIV > 512 ? 512 : (1 << logt) / PATFFT_NER_DCT_DIV);
 }
-constexpr int ner_dct_minb(int logt) { return (65536 / 80) / ner_dct_threads(logt); }
+#ifndef PATFFT_NER_DCT_REGS
+#define PATFFT_NER_DCT_REGS 64  // 8 CTAs of 128 threads per SM (measured best; 48, 56, 72, 80, 96 slower)
+#endif
+constexpr int ner_dct_minb(int logt) { return (65536 / PATFFT_NER_DCT_REGS) / ner_dct_threads(logt); }
 
 template <int K2, int D, int LOGT>
 __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner_dct_kernel(const NerParams p) {
