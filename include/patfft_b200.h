@@ -95,6 +95,14 @@ int patfft_nedner_output_shape(const patfft_nedner_plan* plan, int64_t shape[3])
 int patfft_nedner_execute(patfft_nedner_plan* plan, const double* samples, double* image,
                           double* imag_residual);
 
+/* patfft_nedner_execute that also counts the non-finite voxels of the image
+ * (written to *nonfinite when non-NULL) in the same host pass that widens the
+ * float32 volume to float64, so the caller can apply the ScalarField
+ * finiteness rule (reference recon.py:62-63, DataValidationError) without a
+ * second sweep over the volume.                                           */
+int patfft_nedner_execute_checked(patfft_nedner_plan* plan, const double* samples, double* image,
+                                  double* imag_residual, int64_t* nonfinite);
+
 /* Device-resident execution on `stream` (NULL = the plan's own stream):
  *   samples_dev : M x N_t float32 on the plan's device
  *   image_dev   : output float32 on the plan's device

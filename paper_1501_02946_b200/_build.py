@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpatfft_b200.so")
-SOURCES = ["capi.cu", "spread.cu", "spread_tc.cu", "lateral.cu", "ner.cu", "ner_api.cu", "util.cu", "window.cpp"]
+SOURCES = ["capi.cu", "spread.cu", "spread_tc.cu", "lateral.cu", "ner.cu", "ner_api.cu", "util.cu", "window.cpp", "hoststage.cpp"]
 HEADERS = ["patfft_internal.h", "fft_smem.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, ex
 
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcufft", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcufft", "-lpthread", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -48,6 +48,7 @@ _SIGS = {
                                                      ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
     "patfft_nedner_output_shape": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
     "patfft_nedner_execute": (ctypes.c_int, [_P, _P, _P, _D]),
+    "patfft_nedner_execute_checked": (ctypes.c_int, [_P, _P, _P, _D, ctypes.POINTER(ctypes.c_int64)]),
     "patfft_nedner_execute_device": (ctypes.c_int, [_P, _P, _P, _P]),
     "patfft_nedner_execute_frames_device": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P]),
     "patfft_nedner_plan_destroy": (None, [_P]),

@@ -664,6 +664,8 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   if (const char* e = std::getenv("PATFFT_OVERLAP_CHUNKS")) P->overlap_chunks = std::max(1, std::min(4, std::atoi(e)));
   if (const char* e = std::getenv("PATFFT_GRAPHS")) P->use_graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("PATFFT_H2D_CHUNKS")) P->h2d_chunks = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PATFFT_HOST_CONVERT")) P->host_convert = std::atoi(e) != 0;
+  if (const char* e = std::getenv("PATFFT_HOST_BLOCKS")) P->host_blocks = std::max(1, std::min(16, std::atoi(e)));
   {
     int lo = 0, hi = 0;
     CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1080,11 +1082,8 @@ int patfft_nedner_execute_frames_device(patfft_nedner_plan* P, int n_frames, con
   return execute_graphed(P, n_frames, samples, images, st);
 }
 
-int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* image, double* imag_residual) {
-  if (!P || !samples || !image) return fail(PATFFT_ERR_PARAMETER, "null argument");
-  std::lock_guard<std::mutex> lk(P->mu);
-  CUDA_TRY(cudaSetDevice(P->device));
-  if (P->world != 1) return fail(PATFFT_ERR_PARAMETER, "sharded plan: use the patfft_nedner_shard_* stages");
+// Device-side conversion: float64 crosses PCIe (PATFFT_HOST_CONVERT=0).
+static int execute_host_devconvert(patfft_nedner_plan* P, const double* samples, double* image) {
   const size_t in_n = (size_t)P->M * P->T, out_n = (size_t)P->N0u * P->N1u * P->Tu;
   int rc;
   if (!P->d_samples && (rc = dalloc(&P->d_samples, in_n))) return rc;
@@ -1170,8 +1169,159 @@ int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* 
   CUDA_TRY(launch_f32_to_f64(P->d_out, P->d_out64, out_n, st));
   CUDA_TRY(cudaMemcpyAsync(image, P->d_out64, out_n * sizeof(double), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  if (imag_residual) *imag_residual = 0.0;
   return PATFFT_OK;
+}
+
+
+// Enqueues the forward stages (spread + lateral FFTs) of samples [tb, te) on st.
+static int enqueue_forward_chunk(patfft_nedner_plan* P, int tb, int te, cudaStream_t st) {
+  SpreadParams sp;
+  sp.samples = P->d_samples;
+  sp.recs = P->d_recs;
+  sp.blk = P->d_blk;
+  sp.blk_grp = P->d_blkgrp;
+  set_tc(P, sp);
+  sp.grid = P->d_grid;
+  sp.T = P->T;
+  sp.ncols = P->ncols;
+  sp.nrows = P->nrows;
+  sp.t_begin = tb;
+  sp.t_end = te;
+  LateralParams L = P->lat;
+  L.gh = P->d_gh;
+  L.t_begin = tb;
+  L.t_end = te;
+  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
+  CUDA_TRY(launch_lateral_col(L, st));
+  CUDA_TRY(launch_lateral_row(L, st));
+  return PATFFT_OK;
+}
+
+// Enqueues NER + inverse (every time sample) on st; the image lands in P->d_out.
+static int enqueue_backward(patfft_nedner_plan* P, cudaStream_t st) {
+  LateralParams L = P->lat;
+  L.gh = P->d_gh;
+  L.t_begin = 0;
+  L.t_end = P->T;
+  L.out = P->d_out;
+  if (P->up > 1 || !P->fused_ifft)
+    CUDA_TRY(cudaMemsetAsync(P->d_z, 0, sizeof(float2) * (size_t)P->N0u * P->N1uh * P->Tu, st));
+  CUDA_TRY(launch_ner(P->ner, P->K2, P->poly_degree, st));
+  if (!P->fused_ifft) {
+    CUFFT_TRY(cufftSetStream(P->fft_l, st));
+    CUFFT_TRY(cufftExecC2C(P->fft_l, reinterpret_cast<cufftComplex*>(P->d_z), reinterpret_cast<cufftComplex*>(P->d_z),
+                           CUFFT_INVERSE));
+  }
+  if (P->custom_inverse) {
+    CUDA_TRY(launch_lateral_inverse(L, st));
+  } else {
+    CUFFT_TRY(cufftSetStream(P->fft_c2r, st));
+    CUFFT_TRY(cufftExecC2R(P->fft_c2r, reinterpret_cast<cufftComplex*>(P->d_z), P->d_out));
+  }
+  return PATFFT_OK;
+}
+
+// Host conversion (hoststage.cpp): the host cores narrow block b of the
+// samples into pinned staging while the copy engine uploads block b-1 as
+// float32 and the device spreads earlier time chunks; on the way back the
+// float32 volume downloads in blocks that the host widens into the caller's
+// float64 buffer while the next block is in flight.  Half the PCIe bytes of
+// the device-conversion path, and caller buffers may be pageable.
+static int execute_host_staged(patfft_nedner_plan* P, const double* samples, double* image, int64_t* bad) {
+  const int M = P->M, T = P->T;
+  const size_t in_n = (size_t)M * T, out_n = (size_t)P->N0u * P->N1u * P->Tu;
+  int rc;
+  if (!P->d_samples && (rc = dalloc(&P->d_samples, in_n))) return rc;
+  if (!P->d_out && (rc = dalloc(&P->d_out, out_n))) return rc;
+  const size_t need = std::max(in_n, out_n);
+  if (P->h_stage_n < need) {
+    if (P->h_stage) cudaFreeHost(P->h_stage);
+    P->h_stage = nullptr;
+    P->h_stage_n = 0;
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&P->h_stage), need * sizeof(float), cudaHostAllocDefault));
+    P->h_stage_n = need;
+  }
+  if (!P->copy_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : P->ev_h2d) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (!P->ev_done) {
+    for (auto& e : P->ev_d2h) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_done, cudaEventDisableTiming));
+  }
+  cudaStream_t st = P->stream;
+  // time chunks: whole spread CTA time blocks, so each chunk's spread starts on a block edge
+  const int tgran = (1 << 20) / spread_time_chunks(1 << 20, P->R);
+  int nc = (P->mode == 0 && !P->profiling) ? std::max(1, std::min(P->h2d_chunks, T / tgran)) : 1;
+  nc = std::min(nc, (int)patfft_nedner_plan::kMaxH2dChunks);
+  const int chunk = nc > 1 ? ((T + nc - 1) / nc + tgran - 1) / tgran * tgran : T;
+  int used = 0;
+  while (used < nc && used * chunk < T) ++used;
+  // small records: one block (the pool's wake-up costs more than it saves)
+  const int rb = in_n * sizeof(double) < (size_t)(4 << 20) ? 1 : std::min(P->host_blocks, M);
+  const int rows_per = (M + rb - 1) / rb;
+  CUDA_TRY(cudaEventRecord(P->ev_fork, st));  // device buffers are free once earlier work on st is done
+  CUDA_TRY(cudaStreamWaitEvent(P->copy_stream, P->ev_fork, 0));
+  for (int k = 0; k < used; ++k) {
+    const int tb = k * chunk, te = std::min(T, tb + chunk), tc = te - tb;
+    float* stage = P->h_stage + (size_t)M * tb;  // chunk k: [M][tc] compact
+    for (int m0 = 0; m0 < M; m0 += rows_per) {
+      const int m1 = std::min(M, m0 + rows_per);
+      host_narrow_rows(samples + (size_t)m0 * T + tb, T, stage + (size_t)m0 * tc, tc, m1 - m0, tc);
+      CUDA_TRY(cudaMemcpy2DAsync(P->d_samples + (size_t)m0 * T + tb, (size_t)T * sizeof(float),
+                                 stage + (size_t)m0 * tc, (size_t)tc * sizeof(float), (size_t)tc * sizeof(float),
+                                 (size_t)(m1 - m0), cudaMemcpyHostToDevice, P->copy_stream));
+    }
+    CUDA_TRY(cudaEventRecord(P->ev_h2d[k], P->copy_stream));
+    CUDA_TRY(cudaStreamWaitEvent(st, P->ev_h2d[k], 0));
+    if (used > 1 && (rc = enqueue_forward_chunk(P, tb, te, st))) return rc;
+  }
+  if (used > 1) {
+    if ((rc = enqueue_backward(P, st))) return rc;
+  } else if ((rc = execute_graphed(P, 1, P->d_samples, P->d_out, st))) {
+    return rc;
+  }
+  CUDA_TRY(cudaEventRecord(P->ev_done, st));
+  CUDA_TRY(cudaStreamWaitEvent(P->copy_stream, P->ev_done, 0));
+  // the upload staging is free once the compute started (it waited for the last upload)
+  const int ob = out_n * sizeof(double) < (size_t)(4 << 20) ? 1 : std::min((int)patfft_nedner_plan::kMaxH2dChunks, 4 * P->host_blocks);
+  const size_t per = ((out_n + ob - 1) / ob + 255) / 256 * 256;
+  int nb = 0;
+  for (size_t a = 0; a < out_n; a += per, ++nb) {
+    const size_t n = std::min(per, out_n - a);
+    CUDA_TRY(cudaMemcpyAsync(P->h_stage + a, P->d_out + a, n * sizeof(float), cudaMemcpyDeviceToHost, P->copy_stream));
+    CUDA_TRY(cudaEventRecord(P->ev_d2h[nb], P->copy_stream));
+  }
+  for (int b = 0; b < nb; ++b) {
+    const size_t a = (size_t)b * per, n = std::min(per, out_n - a);
+    CUDA_TRY(cudaEventSynchronize(P->ev_d2h[b]));
+    *bad += host_widen(P->h_stage + a, image + a, (int64_t)n);
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PATFFT_OK;
+}
+
+int patfft_nedner_execute_checked(patfft_nedner_plan* P, const double* samples, double* image,
+                                  double* imag_residual, int64_t* nonfinite) {
+  if (!P || !samples || !image) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  if (P->world != 1) return fail(PATFFT_ERR_PARAMETER, "sharded plan: use the patfft_nedner_shard_* stages");
+  int64_t bad = 0;
+  int rc;
+  if (P->host_convert) {
+    rc = execute_host_staged(P, samples, image, &bad);
+  } else if ((rc = execute_host_devconvert(P, samples, image)) == PATFFT_OK && nonfinite) {
+    bad = host_count_nonfinite(image, (int64_t)P->N0u * P->N1u * P->Tu);
+  }
+  if (rc != PATFFT_OK) return rc;
+  if (imag_residual) *imag_residual = 0.0;
+  if (nonfinite) *nonfinite = bad;
+  return PATFFT_OK;
+}
+
+int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* image, double* imag_residual) {
+  return patfft_nedner_execute_checked(P, samples, image, imag_residual, nullptr);
 }
 
 void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
@@ -1186,6 +1336,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_pre, (void*)P->d_tw, (void*)P->d_jt0,
                   (void*)P->d_jt1})
     free_dev(p);
+  if (P->h_stage) cudaFreeHost(P->h_stage);
   if (P->stream2) cudaStreamSynchronize(P->stream2);
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
@@ -1197,6 +1348,9 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
     cudaStreamSynchronize(P->copy_stream);
     for (auto& e : P->ev_h2d)
       if (e) cudaEventDestroy(e);
+    for (auto& e : P->ev_d2h)
+      if (e) cudaEventDestroy(e);
+    if (P->ev_done) cudaEventDestroy(P->ev_done);
     cudaStreamDestroy(P->copy_stream);
   }
   if (P->stream2) cudaStreamDestroy(P->stream2);

@@ -118,6 +118,13 @@ cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStrea
 cudaError_t launch_fill(float* dst, size_t n, float v, cudaStream_t s);
 cudaError_t launch_gather_rows(const float* samples, const int* gidx, float* grid, int M, int T, cudaStream_t s);
 
+// host-side float64 <-> float32 staging (hoststage.cpp), parallel over a process-wide thread pool
+int host_threads();
+void host_narrow_rows(const double* src, int64_t src_stride, float* dst, int64_t dst_stride, int64_t rows,
+                      int64_t cols);
+int64_t host_widen(const float* src, double* dst, int64_t n);  // returns #non-finite
+int64_t host_count_nonfinite(const double* x, int64_t n);
+
 }  // namespace patfft
 
 // ---------------------------------------------------------------------------
@@ -133,6 +140,12 @@ struct patfft_nedner_plan {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_h2d[kMaxH2dChunks] = {};
   int h2d_chunks = 8;
+  // host conversion (hoststage.cpp): float32 crosses PCIe, the host cores narrow/widen
+  bool host_convert = true;
+  int host_blocks = 4;       // row blocks per time chunk (upload) / volume blocks (download, x4)
+  float* h_stage = nullptr;  // pinned, max(M*T, out voxels) floats
+  size_t h_stage_n = 0;
+  cudaEvent_t ev_d2h[kMaxH2dChunks] = {}, ev_done = nullptr;
   int overlap_chunks = 1;  // time chunks of the overlapped forward stages (1 = off)
   // CUDA graph of the last executed (samples, image, frames) triple
   bool use_graphs = true;

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import sys
 import threading
 from collections import OrderedDict
 from dataclasses import dataclass, field
@@ -61,6 +62,17 @@ class ScalarField:
             raise DataValidationError("spacings must be positive")
         if not np.all(np.isfinite(self.values)):
             raise DataValidationError("field values must be finite")
+
+    @classmethod
+    def _checked(cls, values: np.ndarray, spacing, meta: dict) -> "ScalarField":
+        """A field whose float64 values are already known finite (counted by the producer)."""
+        f = cls.__new__(cls)
+        f.values = values
+        f.spacing = tuple(float(s) for s in spacing)
+        f.meta = meta
+        if len(f.spacing) != values.ndim or any(s <= 0 for s in f.spacing):
+            raise DataValidationError("spacing must be positive, one per array axis")
+        return f
 
     @property
     def n_lateral(self):
@@ -267,15 +279,44 @@ class NedNerPlan:
 
     def execute(self, samples: np.ndarray, out: np.ndarray | None = None):
         """Host float64 (M, Nt) -> host float64 volume; returns (image, imag_residual)."""
+        img, resid, _ = self.execute_checked(samples, out)
+        return img, resid
+
+    def execute_checked(self, samples: np.ndarray, out: np.ndarray | None = None):
+        """As ``execute``, plus the number of non-finite voxels (counted while the
+        host widens the float32 volume, for the ScalarField finiteness rule)."""
         samples = np.ascontiguousarray(samples, dtype=np.float64)
         if samples.shape != (self.n_sensors, self.n_time):
             raise DataValidationError("samples shape does not match the plan")
-        if out is None:
-            out = np.empty(self.out_shape, dtype=np.float64)
+        if out is not None and (out.shape != self.out_shape or out.dtype != np.float64
+                                or not out.flags.c_contiguous):
+            raise DataValidationError("out must be a C-contiguous float64 array of the output shape")
         resid = ctypes.c_double(0.0)
+        bad = ctypes.c_int64(0)
         with self._lock:
-            _lib.check(self._lib.patfft_nedner_execute(self._h, _lib.ptr(samples), _lib.ptr(out), ctypes.byref(resid)))
-        return out, resid.value
+            if out is None:
+                out = self._fresh_out()
+            _lib.check(self._lib.patfft_nedner_execute_checked(self._h, _lib.ptr(samples), _lib.ptr(out),
+                                                               ctypes.byref(resid), ctypes.byref(bad)))
+        return out, resid.value, int(bad.value)
+
+    # Output volumes handed to callers are recycled once the caller has dropped
+    # every reference (the array, its views and the ScalarField holding it):
+    # a fresh 0.5 GB numpy array costs more in first-touch page faults than the
+    # reconstruction's whole PCIe transfer.  Only arrays this plan allocated and
+    # nobody else references are reused; anything still referenced is left alone.
+    _OUT_POOL_SIZE = 2
+
+    def _fresh_out(self) -> np.ndarray:
+        pool = self.__dict__.setdefault("_out_pool", [])
+        for a in pool:
+            # references: the pool list, the loop variable and getrefcount's argument
+            if sys.getrefcount(a) == 3:
+                return a
+        a = np.empty(self.out_shape, dtype=np.float64)
+        if len(pool) < self._OUT_POOL_SIZE:
+            pool.append(a)
+        return a
 
     def execute_device(self, samples_ptr: int, image_ptr: int, stream: int = 0) -> None:
         """Device float32 pointers; enqueued on ``stream`` (0 = plan stream)."""
@@ -427,8 +468,16 @@ def reconstruct_nedner(rec, out_dims=None, upsample: int = 1, spec: WindowSpec |
     elif not isinstance(spec, WindowSpec):  # e.g. the reference's own WindowSpec
         spec = WindowSpec(c=spec.c, K=spec.K, alpha=spec.alpha, beta=spec.beta)
     plan = _plan_for(rec, dims, int(upsample), spec, device)
-    img, resid = plan.execute(np.asarray(rec.samples, dtype=np.float64))
-    return ScalarField(img, plan.spacing, meta={"imag_residual": float(resid)})
+    return _field(plan, rec.samples)
+
+
+def _field(plan, samples) -> ScalarField:
+    """Execute and wrap as ScalarField (recon.py:51-88): the finiteness rule is
+    applied from the count the host pass produced instead of a second sweep."""
+    img, resid, nonfinite = plan.execute_checked(np.asarray(samples, dtype=np.float64))
+    if nonfinite:
+        raise DataValidationError("field values must be finite")
+    return ScalarField._checked(img, plan.spacing, {"imag_residual": float(resid)})
 
 
 def _as_spec(spec):
@@ -447,8 +496,7 @@ def reconstruct_equispaced(rec, upsample: int = 1, spec: WindowSpec | None = Non
     _check_upsample(upsample)
     n_lateral = tuple(int(n) for n in np.atleast_1d(rec.n_lateral))
     plan = _plan_for(rec, n_lateral, int(upsample), _as_spec(spec), device, kind="nufft")
-    img, resid = plan.execute(np.asarray(rec.samples, dtype=np.float64))
-    return ScalarField(img, plan.spacing, meta={"imag_residual": float(resid)})
+    return _field(plan, rec.samples)
 
 
 def reconstruct_interp_fft(rec, upsample: int = 1, *, device: int = 0) -> ScalarField:
@@ -456,5 +504,4 @@ def reconstruct_interp_fft(rec, upsample: int = 1, *, device: int = 0) -> Scalar
     _check_upsample(upsample)
     n_lateral = tuple(int(n) for n in np.atleast_1d(rec.n_lateral))
     plan = _plan_for(rec, n_lateral, int(upsample), WindowSpec(), device, kind="interp")
-    img, resid = plan.execute(np.asarray(rec.samples, dtype=np.float64))
-    return ScalarField(img, plan.spacing, meta={"imag_residual": float(resid)})
+    return _field(plan, rec.samples)

@@ -300,3 +300,65 @@ def test_gpu_frames_file_stream_matches_per_frame_reconstruction(tmp_path):
     with pytest.raises(pb.ParameterError):
         pb.reconstruct_frames_file(pb.NedNerPlan(s.positions, s.weights, 64, s.dt, s.sound_speed, s.dx,
                                                  s.n_lateral), src, dst)
+
+
+def _plan_env(s, **env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        return pb.NedNerPlan(s.positions, s.weights, s.samples.shape[1], s.dt, s.sound_speed, s.dx, s.n_lateral)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_gpu_host_staging_bit_identical_to_device_conversion(name):
+    """Host-core f64->f32 narrowing + f32 PCIe (default) == device-side conversion (f64 over PCIe)."""
+    s = synth.CONFIGS[name]()
+    a, _, bad = _plan_env(s, PATFFT_HOST_CONVERT=1).execute_checked(s.samples)
+    b, _ = _plan_env(s, PATFFT_HOST_CONVERT=0).execute(s.samples)
+    assert bad == 0
+    assert np.array_equal(a, b)
+    # misaligned (8-byte) pageable caller buffers on both sides, several row blocks
+    buf_in = np.empty(s.samples.size + 1)
+    sin = buf_in[1:].reshape(s.samples.shape)
+    sin[...] = s.samples
+    p = _plan_env(s, PATFFT_HOST_BLOCKS=3)
+    buf_out = np.empty(a.size + 1)
+    out = buf_out[1:].reshape(a.shape)
+    p.execute(sin, out)
+    assert np.array_equal(out, a)
+
+
+def test_gpu_nonfinite_samples_raise_like_scalarfield():
+    s = synth.CONFIGS["cfg2"]()
+    bad = s.samples.copy()
+    bad[7, 11] = np.nan
+    r = pb.SensorRecord(s.positions, s.weights, bad, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    with pytest.raises(pb.DataValidationError, match="finite"):
+        pb.reconstruct_nedner(r)
+    f = pb.reconstruct_nedner(s.as_record())  # the plan still works afterwards
+    assert np.all(np.isfinite(f.values))
+
+
+def test_gpu_recycled_outputs_never_alias_live_results():
+    s = synth.CONFIGS["cfg2"]()
+    r = s.as_record()
+    f1 = pb.reconstruct_nedner(r)
+    keep = f1.values.copy()
+    view = f1.values[3]
+    del f1  # a view still references the array: it must not be reused
+    r2 = pb.SensorRecord(s.positions, s.weights, 2.0 * s.samples, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    f2 = pb.reconstruct_nedner(r2)
+    f3 = pb.reconstruct_nedner(r2)
+    assert np.array_equal(view, keep[3])
+    assert f2.values is not f3.values
+    assert np.array_equal(f2.values, f3.values)
+    assert np.allclose(f2.values, 2.0 * keep, rtol=1e-5, atol=1e-6 * np.abs(keep).max())
+    del f2, f3, view
+    f4 = pb.reconstruct_nedner(r)  # everything dropped: a pooled buffer comes back, refilled
+    assert np.array_equal(f4.values, keep)
