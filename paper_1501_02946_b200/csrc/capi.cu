@@ -12,6 +12,7 @@
 #include <cufft.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -110,6 +111,11 @@ void set_tc(const patfft_nedner_plan* P, SpreadParams& sp) {
   sp.tc_nonempty = P->tc_nonempty;
   sp.tc_counter = P->d_tc_counter;
   sp.tc_n = P->tc_n;
+  sp.tc_f16 = P->tc_f16;
+  sp.tc_wexp = P->tc_wexp;
+  sp.tc_m = P->M;
+  sp.tc_a16 = P->d_tc_a16;
+  sp.tc_off = P->d_tc_off;
 }
 
 // Interpolating polynomial of degree D through Chebyshev nodes on
@@ -562,6 +568,29 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     P->tc_nonempty = (int)std::count_if(padded.begin(), padded.end(), [](int64_t v) { return v > 0; });
     P->tc_n = spread_tc_block(T);
     P->tc_records = start[ntiles];
+    // fp16 two-term operands: scale row and column weights by powers of two so
+    // every product W = wr * wc stays below 2^14 (undone in the epilogue)
+    static const bool f16_on = [] {
+      const char* e = std::getenv("PATFFT_SPREAD_F16");
+      return e ? std::atoi(e) != 0 : true;
+    }();
+    P->tc_f16 = f16_on ? 1 : 0;
+    if (P->tc_f16) {
+      float mr = 0.f, mc = 0.f;
+      for (size_t r = 0; r < tcrec.size(); r += 32) {
+        for (int i = 8; i < 16; ++i) mr = std::max(mr, std::fabs(tcrec[r + i]));
+        for (int i = 16; i < 32; ++i) mc = std::max(mc, std::fabs(tcrec[r + i]));
+      }
+      int er = 0, ec = 0;
+      if (mr > 0) std::frexp(mr, &er);
+      if (mc > 0) std::frexp(mc, &ec);
+      const int ar = 7 - er, ac = 7 - ec;  // max |w| * 2^a < 2^7
+      for (size_t r = 0; r < tcrec.size(); r += 32) {
+        for (int i = 8; i < 16; ++i) tcrec[r + i] = std::ldexp(tcrec[r + i], ar);
+        for (int i = 16; i < 32; ++i) tcrec[r + i] = std::ldexp(tcrec[r + i], ac);
+      }
+      P->tc_wexp = ar + ac;
+    }
   }
 
   // ---- deapodisation (nufft.py:367-371), normalised by psi_hat(0) --------
@@ -631,7 +660,14 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   if (P->tc_ntiles) {
     if ((rc = upload(&P->d_tc_recs, tcrec))) return rc;
     if ((rc = upload(&P->d_tc_tiles, tctiles))) return rc;
-    if ((rc = dalloc(&P->d_tc_counter, 1))) return rc;
+    if ((rc = dalloc(&P->d_tc_counter, 2))) return rc;
+    if (P->tc_f16) {  // per-stage A operands (fp16 hi/lo) and sample row offsets, built on the device
+      const int nst = (int)(P->tc_records / 16);
+      if ((rc = dalloc(&P->d_tc_a16, (size_t)nst * 512))) return rc;
+      if ((rc = dalloc(&P->d_tc_off, (size_t)nst * 16))) return rc;
+      CUDA_TRY(spread_tc16_build(P->d_tc_recs, nst, P->d_tc_a16, P->d_tc_off, 0));
+      CUDA_TRY(cudaDeviceSynchronize());
+    }
   }
   if (mode == 1 || mode == 2) {
     std::vector<int> gi(M);
@@ -666,6 +702,10 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   if (const char* e = std::getenv("PATFFT_H2D_CHUNKS")) P->h2d_chunks = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PATFFT_HOST_CONVERT")) P->host_convert = std::atoi(e) != 0;
   if (const char* e = std::getenv("PATFFT_HOST_BLOCKS")) P->host_blocks = std::max(1, std::min(16, std::atoi(e)));
+  if (const char* e = std::getenv("PATFFT_HOST_TRACE")) P->host_trace = std::atoi(e) != 0;
+  if (const char* e = std::getenv("PATFFT_HOST_DIRECT")) P->direct_in = P->direct_out = std::max(0.0, std::min(1.0, std::atof(e)));
+  if (const char* e = std::getenv("PATFFT_HOST_DIRECT_IN")) P->direct_in = std::max(0.0, std::min(1.0, std::atof(e)));
+  if (const char* e = std::getenv("PATFFT_HOST_DIRECT_OUT")) P->direct_out = std::max(0.0, std::min(1.0, std::atof(e)));
   {
     int lo = 0, hi = 0;
     CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1227,7 +1267,34 @@ static int enqueue_backward(patfft_nedner_plan* P, cudaStream_t st) {
 // float32 volume downloads in blocks that the host widens into the caller's
 // float64 buffer while the next block is in flight.  Half the PCIe bytes of
 // the device-conversion path, and caller buffers may be pageable.
+static double wall_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+static bool host_pinned(const void* p, size_t bytes) {
+  cudaPointerAttributes a;
+  const char* c = static_cast<const char*>(p);
+  for (const char* q : {c, c + bytes - 1}) {
+    if (cudaPointerGetAttributes(&a, q) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (a.type != cudaMemoryTypeHost) return false;
+  }
+  return true;
+}
+
+// Host conversion (hoststage.cpp): the host cores narrow block b of the
+// samples into pinned staging while the copy engine uploads block b-1 as
+// float32 and the device spreads earlier time chunks; on the way back the
+// float32 volume downloads in blocks that the host widens into the caller's
+// float64 buffer while the next block is in flight.  Half the PCIe bytes of
+// the device-conversion path, and caller buffers may be pageable.  When a
+// caller buffer is pinned, a fraction (direct_in / direct_out) of it moves as float64 by
+// DMA with the conversion on the device, so the PCIe link and the host
+// memory system share the work (both are near their limits otherwise).
 static int execute_host_staged(patfft_nedner_plan* P, const double* samples, double* image, int64_t* bad) {
+  const double w0 = P->host_trace ? wall_ms() : 0.0;
   const int M = P->M, T = P->T;
   const size_t in_n = (size_t)M * T, out_n = (size_t)P->N0u * P->N1u * P->Tu;
   int rc;
@@ -1249,6 +1316,16 @@ static int execute_host_staged(patfft_nedner_plan* P, const double* samples, dou
     for (auto& e : P->ev_d2h) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&P->ev_done, cudaEventDisableTiming));
   }
+  const bool big = in_n * sizeof(double) >= (size_t)(4 << 20);
+  // sensor rows [0, Md) and voxels [0, od) take the direct float64 route
+  const int Md = (big && P->direct_in > 0 && host_pinned(samples, in_n * sizeof(double)))
+                     ? (int)(P->direct_in * M) : 0;
+  const size_t od = (out_n * sizeof(double) >= (size_t)(4 << 20) && P->direct_out > 0 &&
+                     host_pinned(image, out_n * sizeof(double)))
+                        ? (size_t)(P->direct_out * out_n) / 256 * 256 : 0;
+  if (Md && !P->d_samples64 && (rc = dalloc(&P->d_samples64, in_n))) return rc;  // (full size: shared with other paths)
+  if (od && !P->d_out64 && (rc = dalloc(&P->d_out64, out_n))) return rc;
+  if (od && !P->d_bad) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&P->d_bad), sizeof(unsigned long long)));
   cudaStream_t st = P->stream;
   // time chunks: whole spread CTA time blocks, so each chunk's spread starts on a block edge
   const int tgran = (1 << 20) / spread_time_chunks(1 << 20, P->R);
@@ -1258,14 +1335,18 @@ static int execute_host_staged(patfft_nedner_plan* P, const double* samples, dou
   int used = 0;
   while (used < nc && used * chunk < T) ++used;
   // small records: one block (the pool's wake-up costs more than it saves)
-  const int rb = in_n * sizeof(double) < (size_t)(4 << 20) ? 1 : std::min(P->host_blocks, M);
-  const int rows_per = (M + rb - 1) / rb;
+  const int rb = big ? std::min(P->host_blocks, std::max(1, M - Md)) : 1;
+  const int rows_per = (M - Md + rb - 1) / rb;
   CUDA_TRY(cudaEventRecord(P->ev_fork, st));  // device buffers are free once earlier work on st is done
   CUDA_TRY(cudaStreamWaitEvent(P->copy_stream, P->ev_fork, 0));
   for (int k = 0; k < used; ++k) {
     const int tb = k * chunk, te = std::min(T, tb + chunk), tc = te - tb;
+    if (Md)  // the DMA works on the direct rows while the host narrows the first staged block
+      CUDA_TRY(cudaMemcpy2DAsync(P->d_samples64 + tb, (size_t)T * sizeof(double), samples + tb,
+                                 (size_t)T * sizeof(double), (size_t)tc * sizeof(double), (size_t)Md,
+                                 cudaMemcpyHostToDevice, P->copy_stream));
     float* stage = P->h_stage + (size_t)M * tb;  // chunk k: [M][tc] compact
-    for (int m0 = 0; m0 < M; m0 += rows_per) {
+    for (int m0 = Md; m0 < M; m0 += rows_per) {
       const int m1 = std::min(M, m0 + rows_per);
       host_narrow_rows(samples + (size_t)m0 * T + tb, T, stage + (size_t)m0 * tc, tc, m1 - m0, tc);
       CUDA_TRY(cudaMemcpy2DAsync(P->d_samples + (size_t)m0 * T + tb, (size_t)T * sizeof(float),
@@ -1274,6 +1355,7 @@ static int execute_host_staged(patfft_nedner_plan* P, const double* samples, dou
     }
     CUDA_TRY(cudaEventRecord(P->ev_h2d[k], P->copy_stream));
     CUDA_TRY(cudaStreamWaitEvent(st, P->ev_h2d[k], 0));
+    if (Md) CUDA_TRY(launch_f64_to_f32_cols(P->d_samples64, P->d_samples, Md, T, tb, te, st));
     if (used > 1 && (rc = enqueue_forward_chunk(P, tb, te, st))) return rc;
   }
   if (used > 1) {
@@ -1282,22 +1364,64 @@ static int execute_host_staged(patfft_nedner_plan* P, const double* samples, dou
     return rc;
   }
   CUDA_TRY(cudaEventRecord(P->ev_done, st));
+  if (od) {
+    CUDA_TRY(cudaMemsetAsync(P->d_bad, 0, sizeof(unsigned long long), st));
+    CUDA_TRY(launch_f32_to_f64_count(P->d_out, P->d_out64, od, P->d_bad, st));
+  }
   CUDA_TRY(cudaStreamWaitEvent(P->copy_stream, P->ev_done, 0));
-  // the upload staging is free once the compute started (it waited for the last upload)
-  const int ob = out_n * sizeof(double) < (size_t)(4 << 20) ? 1 : std::min((int)patfft_nedner_plan::kMaxH2dChunks, 4 * P->host_blocks);
-  const size_t per = ((out_n + ob - 1) / ob + 255) / 256 * 256;
+  double w1 = 0.0, w2 = 0.0;
+  if (P->host_trace) {  // (serialises the download behind the compute; diagnostics only)
+    w1 = wall_ms();
+    CUDA_TRY(cudaEventSynchronize(P->ev_done));
+    w2 = wall_ms();
+  }
+  // the upload staging is free once the compute started (it waited for the last upload);
+  // staged blocks go first so the host starts widening early, the direct part fills the gaps
+  const size_t sn = out_n - od;
+  const int ob = big ? std::min((int)patfft_nedner_plan::kMaxH2dChunks, 4 * P->host_blocks) : 1;
+  const size_t per = ((sn + ob - 1) / ob + 255) / 256 * 256;
+  const size_t dper = od ? ((od + ob - 1) / ob + 255) / 256 * 256 : 0;
+  if (od) {
+    CUDA_TRY(cudaEventRecord(P->ev_fork, st));  // direct part converted
+  }
   int nb = 0;
-  for (size_t a = 0; a < out_n; a += per, ++nb) {
-    const size_t n = std::min(per, out_n - a);
-    CUDA_TRY(cudaMemcpyAsync(P->h_stage + a, P->d_out + a, n * sizeof(float), cudaMemcpyDeviceToHost, P->copy_stream));
+  size_t da = 0;
+  for (size_t a = 0; a < sn; a += per, ++nb) {
+    const size_t n = std::min(per, sn - a);
+    CUDA_TRY(cudaMemcpyAsync(P->h_stage + a, P->d_out + od + a, n * sizeof(float), cudaMemcpyDeviceToHost,
+                             P->copy_stream));
     CUDA_TRY(cudaEventRecord(P->ev_d2h[nb], P->copy_stream));
+    if (od && da < od) {
+      if (nb == 0) CUDA_TRY(cudaStreamWaitEvent(P->copy_stream, P->ev_fork, 0));
+      const size_t dn = std::min(dper, od - da);
+      CUDA_TRY(cudaMemcpyAsync(image + da, P->d_out64 + da, dn * sizeof(double), cudaMemcpyDeviceToHost,
+                               P->copy_stream));
+      da += dn;
+    }
+  }
+  if (od && da < od) {
+    if (nb == 0) CUDA_TRY(cudaStreamWaitEvent(P->copy_stream, P->ev_fork, 0));
+    CUDA_TRY(cudaMemcpyAsync(image + da, P->d_out64 + da, (od - da) * sizeof(double), cudaMemcpyDeviceToHost,
+                             P->copy_stream));
   }
   for (int b = 0; b < nb; ++b) {
-    const size_t a = (size_t)b * per, n = std::min(per, out_n - a);
+    const size_t a = (size_t)b * per, n = std::min(per, sn - a);
     CUDA_TRY(cudaEventSynchronize(P->ev_d2h[b]));
-    *bad += host_widen(P->h_stage + a, image + a, (int64_t)n);
+    *bad += host_widen(P->h_stage + a, image + od + a, (int64_t)n);
   }
+  CUDA_TRY(cudaStreamSynchronize(P->copy_stream));
   CUDA_TRY(cudaStreamSynchronize(st));
+  if (od) {
+    unsigned long long nbad = 0;
+    CUDA_TRY(cudaMemcpy(&nbad, P->d_bad, sizeof(nbad), cudaMemcpyDeviceToHost));
+    *bad += (int64_t)nbad;
+  }
+  if (P->host_trace) {
+    const double w3 = wall_ms();
+    std::fprintf(stderr, "[patfft host] narrow+upload issue %.2f ms | compute tail %.2f ms | download+widen %.2f ms | "
+                 "total %.2f ms (%d host threads, direct rows %d/%d, direct voxels %zu/%zu)\n", w1 - w0, w2 - w1,
+                 w3 - w2, w3 - w0, host_threads(), Md, M, od, out_n);
+  }
   return PATFFT_OK;
 }
 
@@ -1332,11 +1456,12 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
   for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_gh,
-                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_tc_recs, (void*)P->d_tc_tiles, (void*)P->d_tc_counter, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
+                  (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_tc_recs, (void*)P->d_tc_tiles, (void*)P->d_tc_counter, (void*)P->d_tc_a16, (void*)P->d_tc_off, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_pre, (void*)P->d_tw, (void*)P->d_jt0,
                   (void*)P->d_jt1})
     free_dev(p);
   if (P->h_stage) cudaFreeHost(P->h_stage);
+  if (P->d_bad) cudaFree(P->d_bad);
   if (P->stream2) cudaStreamSynchronize(P->stream2);
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);

@@ -54,7 +54,13 @@ struct SpreadParams {
   const int4* tc_tiles = nullptr;   // per tile (launch order): {first record, records (multiple of 16), row0, col0}
   int tc_ntiles = 0, tc_nonempty = 0;  // tiles (the non-empty ones first, longest first)
   int tc_n = 0, tc_tblocks = 0;       // time samples per block, time blocks per launch
-  int* tc_counter = nullptr;          // work-item counter (zeroed before each launch)
+  int* tc_counter = nullptr;          // [0] work-item counter, [1] |sample| max bits (zeroed before each launch)
+  // fp16 two-term operands (kind::f16): records pre-scaled by 2^tc_wexp at plan
+  // time, samples by a power of two from their max per launch, undone in the epilogue
+  int tc_f16 = 0, tc_wexp = 0;
+  int tc_m = 0;                        // sensor rows of `samples`
+  const uint4* tc_a16 = nullptr;       // per stage: A operands hi/lo (fp16, UMMA layout), 8 KB
+  const uint32_t* tc_off = nullptr;    // per stage: 16 sample row offsets
 };
 
 struct LateralParams {
@@ -99,6 +105,7 @@ struct NerParams {
 // Kernel launchers
 cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaStream_t s);
 cudaError_t launch_spread_tc(const SpreadParams& p, cudaStream_t s);
+cudaError_t spread_tc16_build(const float* recs, int nstages, void* a16, uint32_t* offs, cudaStream_t s);
 bool spread_tc_supported(int n_lat, int nrows, int ncols, int T);
 int spread_tc_block(int T);
 int spread_rows_per_group(int n_lat, int K2);
@@ -115,6 +122,8 @@ int ner_threads(int n_over);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);
 cudaError_t launch_f64_to_f32_cols(const double* src, float* dst, int M, int T, int tb, int te, cudaStream_t s);
 cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s);
+cudaError_t launch_f32_to_f64_count(const float* src, double* dst, size_t n, unsigned long long* bad,
+                                    cudaStream_t s);
 cudaError_t launch_fill(float* dst, size_t n, float v, cudaStream_t s);
 cudaError_t launch_gather_rows(const float* samples, const int* gidx, float* grid, int M, int T, cudaStream_t s);
 
@@ -142,8 +151,14 @@ struct patfft_nedner_plan {
   int h2d_chunks = 8;
   // host conversion (hoststage.cpp): float32 crosses PCIe, the host cores narrow/widen
   bool host_convert = true;
+  bool host_trace = false;  // PATFFT_HOST_TRACE=1: per-call phase times on stderr
   int host_blocks = 4;       // row blocks per time chunk (upload) / volume blocks (download, x4)
   float* h_stage = nullptr;  // pinned, max(M*T, out voxels) floats
+  // pinned caller buffers: this fraction of the samples / voxels crosses PCIe as
+  // float64 by DMA (device converts) instead of through the host cores
+  double direct_in = 0.25;  // measured at cfg4: upload 8.2 -> 7.0 ms
+  double direct_out = 0.0;  // measured at cfg4: download 7.5 -> 7.9 ms at 0.2 (host memory bound either way)
+  unsigned long long* d_bad = nullptr;  // non-finite count of the direct part
   size_t h_stage_n = 0;
   cudaEvent_t ev_d2h[kMaxH2dChunks] = {}, ev_done = nullptr;
   int overlap_chunks = 1;  // time chunks of the overlapped forward stages (1 = off)
@@ -180,7 +195,10 @@ struct patfft_nedner_plan {
   float* d_recs = nullptr;
   float* d_tc_recs = nullptr;   // tensor-core gridding records (spread_tc.cu)
   int4* d_tc_tiles = nullptr;
-  int* d_tc_counter = nullptr;
+  int* d_tc_counter = nullptr;  // 2 ints
+  uint4* d_tc_a16 = nullptr;
+  uint32_t* d_tc_off = nullptr;
+  int tc_f16 = 0, tc_wexp = 0;
   int tc_ntiles = 0, tc_nonempty = 0, tc_n = 0;
   int64_t tc_records = 0;
   int* d_gidx = nullptr;      // equispaced modes: grid row of each sensor

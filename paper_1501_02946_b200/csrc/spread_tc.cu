@@ -24,6 +24,7 @@
 // accumulator (thread = grid point, 32 time samples per load) straight to
 // the [nrows][ncols][T] grid.  Layouts are the canonical no-swizzle UMMA
 // layouts (8 x 16-byte core matrices), written conflict-free.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -357,6 +358,324 @@ cudaError_t go_tc(const SpreadParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+
+// ===========================================================================
+// fp16 two-term variant (default): kind::f16 UMMAs on hi/lo halves.
+//
+// x = hi + lo with hi = fp16(x), lo = fp16(x - hi) keeps 22 significant bits
+// (as the tf32 split), provided |x| stays inside the fp16 range: the records
+// are scaled by powers of two at plan time so every weight product is below
+// 2^14, the samples by a power of two from their maximum per launch
+// (absmax_kernel), and the epilogue undoes both exactly.  Half the operand
+// bytes and MMA work of 3xTF32.
+//
+// The weights W[p][k] do not depend on the data, so the A operands (hi, lo)
+// of every 16-sensor stage are built once per plan, in the UMMA layout
+// (build_a16_kernel, 8 KB per stage), and each stage just bulk-copies them.
+// The 16 gathered sample rows of a stage (N samples each, contiguous in HBM)
+// are bulk-copied too, two stages ahead, into a staging ring, so no thread
+// holds prefetched samples in registers or issues per-sample loads.
+// ===========================================================================
+
+__device__ __forceinline__ void split_f16x8(const float (&v)[8], uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const __half2 a = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+    const float2 af = __half22float2(a);
+    const __half2 b = __floats2half2_rn(v[2 * j] - af.x, v[2 * j + 1] - af.y);  // v - hi exact in fp32
+    h[j] = *reinterpret_cast<const uint32_t*>(&a);
+    l[j] = *reinterpret_cast<const uint32_t*>(&b);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// D f32, A/B f16, both K-major, M = 128, N.
+__host__ __device__ constexpr uint32_t umma_idesc_f16(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_f16(uint32_t dt, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dt),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+
+// Plan time: per stage of 16 records, A hi/lo in the K-major no-swizzle UMMA
+// layout [part][octet][128 points][8 halves] (8 KB) and the 16 sample row offsets.
+__global__ void build_a16_kernel(const float* __restrict__ recs, int nstages, uint4* __restrict__ a16,
+                                 uint32_t* __restrict__ offs) {
+  const int tid = threadIdx.x, pa = tid & (kTM - 1), pr = pa / kTC, pc = pa % kTC, o = tid >> 7;
+  for (int st = blockIdx.x; st < nstages; st += gridDim.x) {
+    const float* rb = recs + (size_t)st * kKC * 32;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = rb[(o * 8 + j) * 32 + 8 + pr] * rb[(o * 8 + j) * 32 + 16 + pc];
+    uint4 h, l;
+    split_f16x8(v, h, l);
+    uint4* d = a16 + (size_t)st * 512;  // 512 x 16 B
+    d[o * kTM + pa] = h;
+    d[256 + o * kTM + pa] = l;
+    if (tid < kKC) offs[(size_t)st * kKC + tid] = __float_as_uint(rb[tid * 32]);
+  }
+}
+
+// max |s| over rows [0, M), samples [tb, te), as float bits; one warp per row
+__global__ void absmax_kernel(const float* __restrict__ s, int M, int T, int tb, int te, unsigned* __restrict__ out) {
+  const int lane = threadIdx.x & 31, w4 = (te - tb) >> 2;
+  unsigned m = 0;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < M; r += gridDim.x * (blockDim.x >> 5)) {
+    const float4* row = reinterpret_cast<const float4*>(s + (size_t)r * T + tb);
+#pragma unroll 4
+    for (int c = lane; c < w4; c += 32) {
+      const float4 v = __ldcs(row + c);
+      m = max(m, max(max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu),
+                     max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu)));
+    }
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if (lane == 0 && m) atomicMax(out, m);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const SpreadParams p) {
+  constexpr int A_SLOT = 8192;                     // hi + lo, [part][octet][128][8] halves
+  constexpr int A_SLOTS = 4;
+  constexpr int B_HALF = kKC * N * 2;              // one part: [octet][N][8] halves
+  constexpr int B_SLOT = 2 * B_HALF;
+  constexpr int S_SLOT = kKC * N * 4;              // gathered rows [16][N] fp32
+  constexpr uint32_t A_LBO = kTM * 16, A_SBO = 128;
+  constexpr uint32_t B_LBO = N * 16, B_SBO = 128;
+  constexpr uint32_t TCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  constexpr uint32_t IDESC = umma_idesc_f16(N);
+  constexpr int NH = N / 2;
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* const a_ring = smem;                               // A_SLOTS x 8 KB
+  constexpr int BO_AREA = 2 * B_SLOT > 32768 ? 2 * B_SLOT : 32768;  // B slots, also the epilogue staging
+  uint8_t* const b_ops = smem + A_SLOTS * A_SLOT;
+  float* const s_ring = reinterpret_cast<float*>(b_ops + BO_AREA);  // 2 x S_SLOT
+  __shared__ uint64_t mma_bar[2], ld_bar[2], off_bar[kRecSlots];
+  __shared__ __align__(16) uint32_t offbuf[kRecSlots * kKC];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ int ring[kRing];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q4 = warp & 3;
+
+  // ---- empty tiles (no sensor meets them): zeros
+  for (int i = p.tc_nonempty + blockIdx.x; i < p.tc_ntiles; i += gridDim.x) {
+    const int4 t = __ldg(&p.tc_tiles[i]);
+    const int len = p.t_end - p.t_begin;
+    for (int pt = warp; pt < kTM; pt += kThreadsTC / 32) {
+      float* o = p.grid + ((size_t)(t.z + pt / kTC) * p.ncols + (t.w + pt % kTC)) * p.T + p.t_begin;
+      for (int q = lane * 4; q < len; q += 128) *reinterpret_cast<float4*>(o + q) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  Cursor cur, cs, cr;  // stage being built, loads (+2, thread 0), offsets (+3, thread 0, claims items)
+  if (tid == 0) ring[0] = atomicAdd(p.tc_counter, 1);
+  __syncthreads();
+  cur.k = 0;
+  cursor_load(p, cur, ring[0]);
+  if (!cur.valid) return;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base_s)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+  }
+  if (tid == 0) {
+    for (int s2 = 0; s2 < 2; ++s2) {
+      mbar_init_tc(&mma_bar[s2], 1);
+      mbar_init_tc(&ld_bar[s2], 1);
+    }
+    for (int s2 = 0; s2 < kRecSlots; ++s2) mbar_init_tc(&off_bar[s2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+
+  // scales: samples by 2^es (max |s| * 2^es < 2^14), output by 2^-(wexp + es)
+  float s_scale, o_scale;
+  {
+    const float mx = __uint_as_float(p.tc_counter[1]);
+    int es = 0;
+    if (mx > 0.f && mx <= 3.4e38f) {
+      int e;
+      frexpf(mx, &e);
+      es = 14 - e;
+    }
+    es = min(es, 126 - p.tc_wexp);
+    s_scale = ldexpf(1.f, es);
+    o_scale = ldexpf(1.f, -(p.tc_wexp + es));
+  }
+
+  // thread 0: offsets of stage g (16 sample row offsets, 64 B) into slot g % kRecSlots
+  auto fetch_offs = [&](int g, const Cursor& u) {
+    const int r = g % kRecSlots;
+    mbar_expect(&off_bar[r], kKC * 4);
+    bulk_g2s(offbuf + r * kKC, p.tc_off + ((size_t)u.rec0 / kKC + u.c) * kKC, kKC * 4, &off_bar[r]);
+  };
+  // warp 1 (all lanes, uniform cursor): A operands and the 16 sample rows of stage g,
+  // one bulk copy per lane, while thread 0 issues the MMAs of the current stage
+  auto issue_loads = [&](int g, const Cursor& u) {
+    const int r = g % kRecSlots;
+    mbar_wait_tc(&off_bar[r], (g / kRecSlots) & 1);
+    uint64_t* bar = &ld_bar[g & 1];
+    if (lane == 0) mbar_expect(bar, A_SLOT + S_SLOT);
+    __syncwarp();
+    if (lane < kKC) {
+      const int t0 = p.t_begin + u.tb * N;
+      bulk_g2s(s_ring + (g & 1) * (S_SLOT / 4) + lane * N, p.samples + ((size_t)offbuf[r * kKC + lane] + t0), N * 4,
+               bar);
+    } else if (lane == kKC) {
+      bulk_g2s(a_ring + (g % A_SLOTS) * A_SLOT, p.tc_a16 + ((size_t)u.rec0 / kKC + u.c) * (A_SLOT / 16), A_SLOT, bar);
+    }
+  };
+  if (tid == 0) {
+    cr = cur;
+    for (int g = 0; g < kRecSlots - 1 && cr.valid; ++g) {
+      fetch_offs(g, cr);
+      cursor_claim(p, cr, ring);
+    }
+  }
+  __syncthreads();  // ring entries of the first stages
+  if (warp == 1) {
+    cs = cur;
+    for (int g = 0; g < 2 && cs.valid; ++g) {
+      issue_loads(g, cs);
+      cursor_next(p, cs, ring);
+    }
+  }
+
+  // B builder: thread = (time sample tq and tq + N/2, sensor octet ko)
+  const int tq = tid % NH, ko = tid / NH;
+
+  auto epilogue = [&](int g) {
+    const int t0 = p.t_begin + cur.tb * N;
+    mbar_wait_tc(&mma_bar[g & 1], (g >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // staging: per warp 32 points x 32 floats, 16-byte chunks XOR-swizzled (conflict-free both ways)
+    float* stg = reinterpret_cast<float*>(b_ops) + warp * 32 * 32;
+#pragma unroll 1
+    for (int j = warp >> 2; j < N / 32; j += kThreadsTC / 128) {
+      uint32_t r[32];
+      const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(j * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+          "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(ta));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(stg + lane * 32 + ((q ^ (lane & 7)) * 4)) =
+            make_float4(__uint_as_float(r[4 * q]) * o_scale, __uint_as_float(r[4 * q + 1]) * o_scale,
+                        __uint_as_float(r[4 * q + 2]) * o_scale, __uint_as_float(r[4 * q + 3]) * o_scale);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int pl = q * 4 + (lane >> 3), pt = q4 * 32 + pl, c = lane & 7;  // point within the tile
+        const float4 v = *reinterpret_cast<const float4*>(stg + pl * 32 + ((c ^ (pl & 7)) * 4));
+        float* o = p.grid + ((size_t)(cur.row0 + pt / kTC) * p.ncols + (cur.col0 + pt % kTC)) * p.T + t0 + j * 32;
+        *reinterpret_cast<float4*>(o + c * 4) = v;
+      }
+      __syncwarp();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+  };
+
+  for (int g = 0; cur.valid; ++g) {
+    const int sb = g & 1;
+    if (g >= 2) mbar_wait_tc(&mma_bar[sb], ((g >> 1) - 1) & 1);  // B slot free (stage g - 2 done)
+    mbar_wait_tc(&ld_bar[sb], (g >> 1) & 1);                      // A + samples of stage g landed
+    uint8_t* bo = b_ops + sb * B_SLOT;
+    const float* sr = s_ring + sb * (S_SLOT / 4);
+    if (tid < N) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = tq + h * NH;
+        float w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = sr[(8 * ko + j) * N + n] * s_scale;
+        uint4 bh, bl;
+        split_f16x8(w, bh, bl);
+        *reinterpret_cast<uint4*>(bo + ko * B_LBO + n * 16) = bh;
+        *reinterpret_cast<uint4*>(bo + B_HALF + ko * B_LBO + n * 16) = bl;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a_hi = su32(a_ring + (g % A_SLOTS) * A_SLOT), a_lo = a_hi + A_SLOT / 2;
+      const uint32_t b_hi = su32(bo), b_lo = b_hi + B_HALF;
+      const uint64_t dah = umma_desc(a_hi, A_LBO, A_SBO), dal = umma_desc(a_lo, A_LBO, A_SBO);
+      const uint64_t dbh = umma_desc(b_hi, B_LBO, B_SBO), dbl = umma_desc(b_lo, B_LBO, B_SBO);
+      umma_f16(tmem, dah, dbh, IDESC, cur.c ? 1u : 0u);
+      umma_f16(tmem, dah, dbl, IDESC, 1u);
+      umma_f16(tmem, dal, dbh, IDESC, 1u);
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       su32(&mma_bar[sb]))
+                   : "memory");
+      // offsets slot (g + 3) % 4 held stage g - 1's, consumed when its loads were issued (stage g - 3)
+      if (cr.valid) {
+        fetch_offs(g + kRecSlots - 1, cr);
+        cursor_claim(p, cr, ring);
+      }
+    } else if (warp == 1) {
+      // stage g + 2: A slot (g + 2) % 4 was read by stage g - 2 (complete), sample slot sb was
+      // read by this stage's B build (before the barrier above)
+      if (cs.valid) issue_loads(g + 2, cs);
+      cursor_next(p, cs, ring);
+    }
+    if (cur.c == cur.nch - 1) epilogue(g);
+    cursor_next(p, cur, ring);
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
+
+template <int N>
+cudaError_t go_tc16(const SpreadParams& p, cudaStream_t s) {
+  const size_t smem = 4 * 8192 + std::max(2 * (2 * kKC * N * 2), 32768) + 2 * (kKC * N * 4);
+  auto k = spread_tc16_kernel<N>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err) return err;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  SpreadParams q = p;
+  q.tc_tblocks = (p.t_end - p.t_begin) / N;
+  const int blocks = std::min(q.tc_ntiles * q.tc_tblocks, 2 * sms);
+  if ((err = cudaMemsetAsync(q.tc_counter, 0, 2 * sizeof(int), s))) return err;
+  absmax_kernel<<<4 * sms, 256, 0, s>>>(p.samples, p.tc_m, p.T, p.t_begin, p.t_end,
+                                        reinterpret_cast<unsigned*>(q.tc_counter + 1));
+  if ((err = cudaGetLastError())) return err;
+  if (blocks > 0 && q.tc_tblocks > 0) k<<<blocks, kThreadsTC, smem, s>>>(q);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool spread_tc_supported(int n_lat, int nrows, int ncols, int T) {
@@ -369,9 +688,24 @@ int spread_tc_block(int T) {
   return 0;
 }
 
+cudaError_t spread_tc16_build(const float* recs, int nstages, void* a16, uint32_t* offs, cudaStream_t s) {
+  if (nstages <= 0) return cudaSuccess;
+  build_a16_kernel<<<std::min(nstages, 148 * 8), kThreadsTC, 0, s>>>(recs, nstages, static_cast<uint4*>(a16), offs);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spread_tc(const SpreadParams& p, cudaStream_t s) {
   const int n = p.tc_n;
   if ((p.t_end - p.t_begin) % n || p.t_begin % n) return cudaErrorInvalidValue;
+  if (p.tc_f16) {
+    switch (n) {
+      case 256: return go_tc16<256>(p, s);
+      case 128: return go_tc16<128>(p, s);
+      case 64: return go_tc16<64>(p, s);
+      case 32: return go_tc16<32>(p, s);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (n) {
     case 256: return go_tc<256>(p, s);
     case 128: return go_tc<128>(p, s);

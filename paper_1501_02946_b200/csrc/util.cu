@@ -14,6 +14,18 @@ __global__ void f32_to_f64_kernel(const float* __restrict__ s, double* __restric
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     d[i] = (double)s[i];
 }
+// widening that also counts non-finite values (the ScalarField finiteness rule)
+__global__ void f32_to_f64_count_kernel(const float* __restrict__ s, double* __restrict__ d, size_t n,
+                                        unsigned long long* __restrict__ bad) {
+  unsigned k = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float v = __ldcs(&s[i]);
+    k += !isfinite(v);
+    __stcs(&d[i], (double)v);
+  }
+  k = __reduce_add_sync(0xffffffffu, k);
+  if (k && (threadIdx.x & 31) == 0) atomicAdd(bad, (unsigned long long)k);
+}
 // columns [tb, te) of an M x T row-major array
 __global__ void f64_to_f32_cols_kernel(const double* __restrict__ s, float* __restrict__ d, int M, int T, int tb,
                                        int te) {
@@ -46,6 +58,11 @@ unsigned grid_for(size_t n) {
 }
 }  // namespace
 
+cudaError_t launch_f32_to_f64_count(const float* src, double* dst, size_t n, unsigned long long* bad,
+                                    cudaStream_t s) {
+  f32_to_f64_count_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n, bad);
+  return cudaGetLastError();
+}
 cudaError_t launch_f64_to_f32_cols(const double* src, float* dst, int M, int T, int tb, int te, cudaStream_t s) {
   f64_to_f32_cols_kernel<<<grid_for((size_t)M * (te - tb)), 256, 0, s>>>(src, dst, M, T, tb, te);
   return cudaGetLastError();

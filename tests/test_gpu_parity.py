@@ -362,3 +362,38 @@ def test_gpu_recycled_outputs_never_alias_live_results():
     del f2, f3, view
     f4 = pb.reconstruct_nedner(r)  # everything dropped: a pooled buffer comes back, refilled
     assert np.array_equal(f4.values, keep)
+
+
+def _pinned(shape):
+    import ctypes
+
+    from paper_1501_02946_b200 import _lib
+    lib = _lib.load()
+    p = ctypes.c_void_p()
+    n = int(np.prod(shape))
+    _lib.check(lib.patfft_host_alloc(8 * n, ctypes.byref(p)))
+    a = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_double)), shape=(n,)).reshape(shape)
+    return a, p
+
+
+@pytest.mark.parametrize("frac", ["0.35", "1.0"])  # PATFFT_HOST_DIRECT sets both directions
+def test_gpu_pinned_direct_split_bit_identical(frac):
+    """Pinned caller buffers: part of the rows/voxels move as float64 by DMA (device conversion)."""
+    from paper_1501_02946_b200 import _lib
+    lib = _lib.load()
+    s = synth.CONFIGS["cfg3"]()
+    want, _ = _plan_env(s, PATFFT_HOST_DIRECT=0).execute(s.samples)
+    p = _plan_env(s, PATFFT_HOST_DIRECT=frac)
+    hin, pin = _pinned(s.samples.shape)
+    hout, pout = _pinned(want.shape)
+    try:
+        hin[...] = s.samples
+        _, _, bad = p.execute_checked(hin, hout)
+        assert bad == 0
+        assert np.array_equal(hout, want)
+        hin[5, 9] = np.inf  # non-finite output must be counted in the direct and the staged part
+        _, _, bad = p.execute_checked(hin, hout)
+        assert bad > 0 and bad == int(np.count_nonzero(~np.isfinite(hout)))
+    finally:
+        lib.patfft_host_free(pin)
+        lib.patfft_host_free(pout)
