@@ -391,6 +391,24 @@ __device__ __forceinline__ void split_f16x8(const float (&v)[8], uint4& hi, uint
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
+// Same split of s * v[0..7] with packed FP32 ops (FMUL2 / FADD2) and f16x2 conversions.
+__device__ __forceinline__ void split_f16x8_scaled(const float (&v)[8], float sc, uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    asm("{\n\t.reg .b64 x, s, hf, d;\n\t.reg .b32 x0, x1, h0f, h1f, d0, d1;\n\t.reg .b16 h0, h1;\n\t"
+        "mov.b64 x, {%2, %3};\n\tmov.b64 s, {%4, %4};\n\tmul.rn.f32x2 x, x, s;\n\t"
+        "mov.b64 {x0, x1}, x;\n\tcvt.rn.f16x2.f32 %0, x1, x0;\n\t"
+        "mov.b32 {h0, h1}, %0;\n\tcvt.f32.f16 h0f, h0;\n\tcvt.f32.f16 h1f, h1;\n\t"
+        "mov.b64 hf, {h0f, h1f};\n\tsub.rn.f32x2 d, x, hf;\n\tmov.b64 {d0, d1}, d;\n\t"
+        "cvt.rn.f16x2.f32 %1, d1, d0;\n\t}"
+        : "=r"(h[j]), "=r"(l[j])
+        : "f"(v[2 * j]), "f"(v[2 * j + 1]), "f"(sc));
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 // D f32, A/B f16, both K-major, M = 128, N.
 __host__ __device__ constexpr uint32_t umma_idesc_f16(int n) {
   return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
@@ -449,6 +467,53 @@ __global__ void absmax_kernel(const float* __restrict__ s, int M, int T, int tb,
   if (lane == 0 && m) atomicMax(out, m);
 }
 
+// Work items of the fp16 kernel, resolved by thread 0 into a shared ring:
+// {tile's first record / 16, stages, row0, col0, time block}; stages == 0
+// marks the end.  Thread 0 claims items two ahead (atomicAdd result and the
+// tile-table load are consumed one item later), so neither latency stalls
+// the stage loop.
+struct Item16 {
+  int st0, nch, row0, col0, tb;
+};
+struct Claimer16 {  // thread 0 only
+  int wb, wc;       // claimed ids: B (tile loaded into tb_), C (atomic in flight)
+  int4 tb_;
+};
+__device__ __forceinline__ Item16 item16_make(const SpreadParams& p, int w, int4 t) {
+  Item16 it;
+  if (w < p.tc_nonempty * p.tc_tblocks) {
+    it.st0 = t.x / kKC;
+    it.nch = t.y / kKC;
+    it.row0 = t.z;
+    it.col0 = t.w;
+    it.tb = w % p.tc_tblocks;
+  } else {
+    it.st0 = it.nch = it.row0 = it.col0 = it.tb = 0;
+  }
+  return it;
+}
+__device__ __forceinline__ int4 item16_tile(const SpreadParams& p, int w) {
+  return w < p.tc_nonempty * p.tc_tblocks ? __ldg(&p.tc_tiles[w / p.tc_tblocks]) : make_int4(0, 0, 0, 0);
+}
+// next item into ring slot k: B's resolved item; B <- C (issue its tile load); C <- new claim
+__device__ __forceinline__ void claim16(const SpreadParams& p, Claimer16& q, Item16* ring, int k) {
+  ring[k & (kRing - 1)] = item16_make(p, q.wb, q.tb_);
+  q.wb = q.wc;
+  q.tb_ = item16_tile(p, q.wb);
+  q.wc = atomicAdd(p.tc_counter, 1);
+}
+struct Cursor16 {
+  int k, c;  // ring position, stage within the item
+  Item16 it;
+};
+__device__ __forceinline__ bool c16_valid(const Cursor16& u) { return u.it.nch > 0; }
+__device__ __forceinline__ void c16_next(Cursor16& u, const Item16* ring) {
+  if (!c16_valid(u) || ++u.c < u.it.nch) return;
+  ++u.k;
+  u.c = 0;
+  u.it = ring[u.k & (kRing - 1)];
+}
+
 template <int N>
 __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const SpreadParams p) {
   constexpr int A_SLOT = 8192;                     // hi + lo, [part][octet][128][8] halves
@@ -467,10 +532,11 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
   constexpr int BO_AREA = 2 * B_SLOT > 32768 ? 2 * B_SLOT : 32768;  // B slots, also the epilogue staging
   uint8_t* const b_ops = smem + A_SLOTS * A_SLOT;
   float* const s_ring = reinterpret_cast<float*>(b_ops + BO_AREA);  // 2 x S_SLOT
-  __shared__ uint64_t mma_bar[2], ld_bar[2], off_bar[kRecSlots];
-  __shared__ __align__(16) uint32_t offbuf[kRecSlots * kKC];
+  constexpr int OFF_SLOTS = 8;  // sample row offsets of stage x: slot x % 8, fetched at stage x - 4
+  __shared__ uint64_t mma_bar[2], ld_bar[2], off_bar[OFF_SLOTS];
+  __shared__ __align__(16) uint32_t offbuf[OFF_SLOTS * kKC];
   __shared__ uint32_t tmem_base_s;
-  __shared__ int ring[kRing];
+  __shared__ Item16 ring[kRing];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q4 = warp & 3;
@@ -484,12 +550,20 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
       for (int q = lane * 4; q < len; q += 128) *reinterpret_cast<float4*>(o + q) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  Cursor cur, cs, cr;  // stage being built, loads (+2, thread 0), offsets (+3, thread 0, claims items)
-  if (tid == 0) ring[0] = atomicAdd(p.tc_counter, 1);
+  Cursor16 cur, cs, cr;  // stage being built, loads (+2, warp 1), offsets (+3, thread 0)
+  Claimer16 claim;
+  if (tid == 0) {
+    const int w0 = atomicAdd(p.tc_counter, 1);
+    claim.wb = atomicAdd(p.tc_counter, 1);
+    claim.wc = atomicAdd(p.tc_counter, 1);
+    ring[0] = item16_make(p, w0, item16_tile(p, w0));
+    claim.tb_ = item16_tile(p, claim.wb);
+  }
   __syncthreads();
   cur.k = 0;
-  cursor_load(p, cur, ring[0]);
-  if (!cur.valid) return;
+  cur.c = 0;
+  cur.it = ring[0];
+  if (!c16_valid(cur)) return;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base_s)),
@@ -501,7 +575,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
       mbar_init_tc(&mma_bar[s2], 1);
       mbar_init_tc(&ld_bar[s2], 1);
     }
-    for (int s2 = 0; s2 < kRecSlots; ++s2) mbar_init_tc(&off_bar[s2], 1);
+    for (int s2 = 0; s2 < OFF_SLOTS; ++s2) mbar_init_tc(&off_bar[s2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -524,41 +598,49 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
     o_scale = ldexpf(1.f, -(p.tc_wexp + es));
   }
 
-  // thread 0: offsets of stage g (16 sample row offsets, 64 B) into slot g % kRecSlots
-  auto fetch_offs = [&](int g, const Cursor& u) {
-    const int r = g % kRecSlots;
+  // thread 0: offsets of stage g (16 sample row offsets, 64 B) into slot g % OFF_SLOTS
+  auto fetch_offs = [&](int g, const Cursor16& u) {
+    const int r = g % OFF_SLOTS;
     mbar_expect(&off_bar[r], kKC * 4);
-    bulk_g2s(offbuf + r * kKC, p.tc_off + ((size_t)u.rec0 / kKC + u.c) * kKC, kKC * 4, &off_bar[r]);
+    bulk_g2s(offbuf + r * kKC, p.tc_off + ((size_t)u.it.st0 + u.c) * kKC, kKC * 4, &off_bar[r]);
+  };
+  // thread 0: advance the offsets cursor, resolving the next item at a crossing
+  auto cr_next = [&]() {
+    if (!c16_valid(cr) || ++cr.c < cr.it.nch) return;
+    ++cr.k;
+    cr.c = 0;
+    claim16(p, claim, ring, cr.k);
+    cr.it = ring[cr.k & (kRing - 1)];
   };
   // warp 1 (all lanes, uniform cursor): A operands and the 16 sample rows of stage g,
   // one bulk copy per lane, while thread 0 issues the MMAs of the current stage
-  auto issue_loads = [&](int g, const Cursor& u) {
-    const int r = g % kRecSlots;
-    mbar_wait_tc(&off_bar[r], (g / kRecSlots) & 1);
+  auto issue_loads = [&](int g, const Cursor16& u) {
+    const int r = g % OFF_SLOTS;
+    mbar_wait_tc(&off_bar[r], (g / OFF_SLOTS) & 1);
     uint64_t* bar = &ld_bar[g & 1];
     if (lane == 0) mbar_expect(bar, A_SLOT + S_SLOT);
     __syncwarp();
     if (lane < kKC) {
-      const int t0 = p.t_begin + u.tb * N;
+      const int t0 = p.t_begin + u.it.tb * N;
       bulk_g2s(s_ring + (g & 1) * (S_SLOT / 4) + lane * N, p.samples + ((size_t)offbuf[r * kKC + lane] + t0), N * 4,
                bar);
     } else if (lane == kKC) {
-      bulk_g2s(a_ring + (g % A_SLOTS) * A_SLOT, p.tc_a16 + ((size_t)u.rec0 / kKC + u.c) * (A_SLOT / 16), A_SLOT, bar);
+      bulk_g2s(a_ring + (g % A_SLOTS) * A_SLOT, p.tc_a16 + ((size_t)u.it.st0 + u.c) * (A_SLOT / 16), A_SLOT, bar);
     }
   };
   if (tid == 0) {
     cr = cur;
-    for (int g = 0; g < kRecSlots - 1 && cr.valid; ++g) {
+    for (int g = 0; g < 4 && c16_valid(cr); ++g) {
       fetch_offs(g, cr);
-      cursor_claim(p, cr, ring);
+      cr_next();
     }
   }
   __syncthreads();  // ring entries of the first stages
   if (warp == 1) {
     cs = cur;
-    for (int g = 0; g < 2 && cs.valid; ++g) {
+    for (int g = 0; g < 2 && c16_valid(cs); ++g) {
       issue_loads(g, cs);
-      cursor_next(p, cs, ring);
+      c16_next(cs, ring);
     }
   }
 
@@ -566,7 +648,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
   const int tq = tid % NH, ko = tid / NH;
 
   auto epilogue = [&](int g) {
-    const int t0 = p.t_begin + cur.tb * N;
+    const int t0 = p.t_begin + cur.it.tb * N;
     mbar_wait_tc(&mma_bar[g & 1], (g >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // staging: per warp 32 points x 32 floats, 16-byte chunks XOR-swizzled (conflict-free both ways)
@@ -594,7 +676,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
       for (int q = 0; q < 8; ++q) {
         const int pl = q * 4 + (lane >> 3), pt = q4 * 32 + pl, c = lane & 7;  // point within the tile
         const float4 v = *reinterpret_cast<const float4*>(stg + pl * 32 + ((c ^ (pl & 7)) * 4));
-        float* o = p.grid + ((size_t)(cur.row0 + pt / kTC) * p.ncols + (cur.col0 + pt % kTC)) * p.T + t0 + j * 32;
+        float* o = p.grid + ((size_t)(cur.it.row0 + pt / kTC) * p.ncols + (cur.it.col0 + pt % kTC)) * p.T + t0 + j * 32;
         *reinterpret_cast<float4*>(o + c * 4) = v;
       }
       __syncwarp();
@@ -603,7 +685,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
     __syncthreads();
   };
 
-  for (int g = 0; cur.valid; ++g) {
+  for (int g = 0; c16_valid(cur); ++g) {
     const int sb = g & 1;
     if (g >= 2) mbar_wait_tc(&mma_bar[sb], ((g >> 1) - 1) & 1);  // B slot free (stage g - 2 done)
     mbar_wait_tc(&ld_bar[sb], (g >> 1) & 1);                      // A + samples of stage g landed
@@ -615,9 +697,9 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
         const int n = tq + h * NH;
         float w[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) w[j] = sr[(8 * ko + j) * N + n] * s_scale;
+        for (int j = 0; j < 8; ++j) w[j] = sr[(8 * ko + j) * N + n];
         uint4 bh, bl;
-        split_f16x8(w, bh, bl);
+        split_f16x8_scaled(w, s_scale, bh, bl);
         *reinterpret_cast<uint4*>(bo + ko * B_LBO + n * 16) = bh;
         *reinterpret_cast<uint4*>(bo + B_HALF + ko * B_LBO + n * 16) = bl;
       }
@@ -636,19 +718,19 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        su32(&mma_bar[sb]))
                    : "memory");
-      // offsets slot (g + 3) % 4 held stage g - 1's, consumed when its loads were issued (stage g - 3)
-      if (cr.valid) {
-        fetch_offs(g + kRecSlots - 1, cr);
-        cursor_claim(p, cr, ring);
+      // offsets of stage g + 4 into slot (g + 4) % 8, last read when stage g - 4's loads were issued
+      if (c16_valid(cr)) {
+        fetch_offs(g + 4, cr);
+        cr_next();
       }
     } else if (warp == 1) {
       // stage g + 2: A slot (g + 2) % 4 was read by stage g - 2 (complete), sample slot sb was
       // read by this stage's B build (before the barrier above)
-      if (cs.valid) issue_loads(g + 2, cs);
-      cursor_next(p, cs, ring);
+      if (c16_valid(cs)) issue_loads(g + 2, cs);
+      c16_next(cs, ring);
     }
-    if (cur.c == cur.nch - 1) epilogue(g);
-    cursor_next(p, cur, ring);
+    if (cur.c == cur.it.nch - 1) epilogue(g);
+    c16_next(cur, ring);
   }
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
 }
