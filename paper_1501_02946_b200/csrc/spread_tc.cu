@@ -514,6 +514,20 @@ __device__ __forceinline__ void c16_next(Cursor16& u, const Item16* ring) {
   u.it = ring[u.k & (kRing - 1)];
 }
 
+// experiment switches (tools/variants.sh): drop one part of the work to time the rest
+#ifndef PATFFT_TC16_NOSTORE
+#define PATFFT_TC16_NOSTORE 0
+#endif
+#ifndef PATFFT_TC16_NOBUILD
+#define PATFFT_TC16_NOBUILD 0
+#endif
+#ifndef PATFFT_TC16_NOMMA
+#define PATFFT_TC16_NOMMA 0
+#endif
+#ifndef PATFFT_TC16_NOEPI
+#define PATFFT_TC16_NOEPI 0
+#endif
+
 template <int N>
 __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const SpreadParams p) {
   constexpr int A_SLOT = 8192;                     // hi + lo, [part][octet][128][8] halves
@@ -651,6 +665,10 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
     const int t0 = p.t_begin + cur.it.tb * N;
     mbar_wait_tc(&mma_bar[g & 1], (g >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (PATFFT_TC16_NOEPI) {
+      __syncthreads();
+      return;
+    }
     // staging: per warp 32 points x 32 floats, 16-byte chunks XOR-swizzled (conflict-free both ways)
     float* stg = reinterpret_cast<float*>(b_ops) + warp * 32 * 32;
 #pragma unroll 1
@@ -677,7 +695,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
         const int pl = q * 4 + (lane >> 3), pt = q4 * 32 + pl, c = lane & 7;  // point within the tile
         const float4 v = *reinterpret_cast<const float4*>(stg + pl * 32 + ((c ^ (pl & 7)) * 4));
         float* o = p.grid + ((size_t)(cur.it.row0 + pt / kTC) * p.ncols + (cur.it.col0 + pt % kTC)) * p.T + t0 + j * 32;
-        *reinterpret_cast<float4*>(o + c * 4) = v;
+        if (!PATFFT_TC16_NOSTORE || v.x == 12345.f) *reinterpret_cast<float4*>(o + c * 4) = v;
       }
       __syncwarp();
     }
@@ -691,7 +709,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
     mbar_wait_tc(&ld_bar[sb], (g >> 1) & 1);                      // A + samples of stage g landed
     uint8_t* bo = b_ops + sb * B_SLOT;
     const float* sr = s_ring + sb * (S_SLOT / 4);
-    if (tid < N) {
+    if (tid < N && !PATFFT_TC16_NOBUILD) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int n = tq + h * NH;
@@ -712,9 +730,11 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
       const uint32_t b_hi = su32(bo), b_lo = b_hi + B_HALF;
       const uint64_t dah = umma_desc(a_hi, A_LBO, A_SBO), dal = umma_desc(a_lo, A_LBO, A_SBO);
       const uint64_t dbh = umma_desc(b_hi, B_LBO, B_SBO), dbl = umma_desc(b_lo, B_LBO, B_SBO);
-      umma_f16(tmem, dah, dbh, IDESC, cur.c ? 1u : 0u);
-      umma_f16(tmem, dah, dbl, IDESC, 1u);
-      umma_f16(tmem, dal, dbh, IDESC, 1u);
+      if (!PATFFT_TC16_NOMMA) {
+        umma_f16(tmem, dah, dbh, IDESC, cur.c ? 1u : 0u);
+        umma_f16(tmem, dah, dbl, IDESC, 1u);
+        umma_f16(tmem, dal, dbh, IDESC, 1u);
+      }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        su32(&mma_bar[sb]))
                    : "memory");
