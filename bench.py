@@ -483,20 +483,25 @@ def run_gpu_arm(args):
     sp_ms = per["spread"]
     taps = 12 ** len(rec.n_lateral)
     useful = 2.0 * rec.positions.shape[0] * taps * rec.samples.shape[1]  # useful FLOPs: 2 x M x (2K)^d x T
-    spread = {"kernel": "spread_tc_kernel (tcgen05 3xTF32)" if info[0] else "spread_tp_kernel (SIMT FP32)",
+    spread = {"kernel": {2: "spread_tc16_kernel (tcgen05 kind::f16, two-term fp16 split) + absmax_kernel",
+                         1: "spread_tc_kernel (tcgen05 3xTF32)"}.get(int(info[0]), "spread_tp_kernel (SIMT FP32)"),
               "launch_ms": sp_ms, "algorithmic_bytes": sbytes["spread"],
               "hbm": {"achieved": sbytes["spread"] / (sp_ms / 1e3) / 1e9, "peak": peak,
                       "frac": sbytes["spread"] / (sp_ms / 1e3) / 1e9 / peak},
               "traffic": _traffic_from_profiles(args.config, "spread")}
     if info[0]:
-        tc_peak = _tf32_peak()
-        executed = 3 * 2.0 * 128 * info[1] * rec.samples.shape[1]  # 3 tf32 products per 128-point record
+        f16 = int(info[0]) == 2
+        tc_peak = _tf32_peak() * (2.0 if f16 else 1.0)
+        executed = 3 * 2.0 * 128 * info[1] * rec.samples.shape[1]  # 3 products per 128-point record
         spread["tensor"] = {"executed_tflops": executed / (sp_ms / 1e3) / 1e12, "peak_tflops": tc_peak,
                             "frac": executed / (sp_ms / 1e3) / 1e12 / tc_peak,
                             "useful_tflops_fp32": useful / (sp_ms / 1e3) / 1e12,
                             "records": int(info[1]),
-                            "note": "executed = 3 tf32 products x 2 x 128 grid points x records x T; peak = "
-                                    "measured bf16 dense / 2 (tf32 runs at half the bf16 rate)"}
+                            "note": ("executed = 3 fp16 products (hi*hi, hi*lo, lo*hi) x 2 x 128 grid points x "
+                                     "records x T; peak = measured bf16 dense (fp16 runs at the bf16 rate)"
+                                     if f16 else
+                                     "executed = 3 tf32 products x 2 x 128 grid points x records x T; peak = "
+                                     "measured bf16 dense / 2 (tf32 runs at half the bf16 rate)")}
     else:
         fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
         spread["fp32"] = {"achieved_tflops": useful / (sp_ms / 1e3) / 1e12, "peak_tflops": fp32_peak,

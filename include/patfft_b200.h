@@ -211,8 +211,9 @@ int patfft_nedner_stage_bytes(const patfft_nedner_plan* plan, double* bytes, int
  * library (cuFFT) kernels (the latter only on fallback sizes). */
 int patfft_nedner_launches_per_execute(const patfft_nedner_plan* plan, int* own, int* library);
 
-/* Gridding (spread) kernel of the plan: info[0] = 1 for the tcgen05 tensor-core
- * kernel (spread_tc.cu), 0 for the SIMT kernel; info[1] = records (tensor
+/* Gridding (spread) kernel of the plan: info[0] = 2 for the tcgen05 tensor-core
+ * kernel with fp16 two-term operands (spread_tc.cu, default), 1 for its 3xTF32
+ * form (PATFFT_SPREAD_F16=0), 0 for the SIMT kernel; info[1] = records (tensor
  * core: tile x sensor pairs, padded to 16 per tile -- each is 128 grid points
  * x N_t MACs per product); info[2] = tiles (or SIMT blocks); info[3] = time
  * samples per tensor-core work item. */

@@ -570,11 +570,17 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     P->tc_records = start[ntiles];
     // fp16 two-term operands: scale row and column weights by powers of two so
     // every product W = wr * wc stays below 2^14 (undone in the epilogue)
-    static const bool f16_on = [] {
+    const bool f16_on = [] {
       const char* e = std::getenv("PATFFT_SPREAD_F16");
       return e ? std::atoi(e) != 0 : true;
     }();
-    P->tc_f16 = f16_on ? 1 : 0;
+    // (the fp16 kernel's longer per-item pipeline only pays off with many work
+    // items: measured cfg4 (8192 items) 0.563 -> 0.481 ms, cfg3 (1024) even, cfg2 (128) 2.4x slower)
+    const int64_t f16_min_items = [] {
+      const char* e = std::getenv("PATFFT_SPREAD_F16_MIN_ITEMS");
+      return e ? std::atoll(e) : (int64_t)2048;
+    }();
+    P->tc_f16 = (f16_on && (int64_t)P->tc_nonempty * (T / P->tc_n) >= f16_min_items) ? 1 : 0;
     if (P->tc_f16) {
       float mr = 0.f, mc = 0.f;
       for (size_t r = 0; r < tcrec.size(); r += 32) {
@@ -1544,7 +1550,7 @@ int patfft_nedner_launches_per_execute(const patfft_nedner_plan* P, int* own, in
 int patfft_nedner_spread_info(const patfft_nedner_plan* P, int64_t info[4]) {
   if (!P || !info) return fail(PATFFT_ERR_PARAMETER, "null argument");
   const bool tc = P->tc_ntiles > 0;
-  info[0] = tc ? 1 : 0;                        // 1: tensor-core gridding (spread_tc.cu)
+  info[0] = tc ? (P->tc_f16 ? 2 : 1) : 0;      // tensor-core gridding (spread_tc.cu): 2 fp16 two-term, 1 3xTF32
   info[1] = tc ? P->tc_records : P->n_records;  // records (tile x sensor pairs, padded to 16 per tile)
   info[2] = tc ? P->tc_ntiles : P->nblk;        // tiles / SIMT blocks
   info[3] = tc ? P->tc_n : 0;                   // time samples per tensor-core item

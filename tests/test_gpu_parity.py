@@ -397,3 +397,40 @@ def test_gpu_pinned_direct_split_bit_identical(frac):
     finally:
         lib.patfft_host_free(pin)
         lib.patfft_host_free(pout)
+
+
+@pytest.mark.parametrize("scale", [1e-30, 1e-12, 1e12, 1e30])
+def test_gpu_gridding_scale_invariance(scale):
+    """The fp16 two-term gridding rescales samples by a power of two from their
+    maximum: any overall amplitude gives the same relative answer."""
+    s = synth.CONFIGS["cfg2"]()
+    p = _plan_env(s, PATFFT_SPREAD_F16_MIN_ITEMS=0)  # the fp16 kernel even at this small size
+    base, _ = p.execute(s.samples)
+    got, _ = p.execute(s.samples * scale)
+    err = rel_l2(got / scale, base)
+    print(f"scale {scale:g}: rel-L2 vs unscaled {err:.3e}")
+    assert err <= 3e-6  # fp32 rounding of the rescaled input (5e-7 measured); a broken scale shows as O(1)
+
+
+@pytest.mark.parametrize("f16", [0, 1])
+def test_gpu_gridding_forms_match_oracle(f16):
+    """Both tensor-core gridding forms (3xTF32, fp16 two-term) forced on cfg3 vs the oracle."""
+    s = synth.CONFIGS["cfg3"]()
+    got, _ = _plan_env(s, PATFFT_SPREAD_F16=f16, PATFFT_SPREAD_F16_MIN_ITEMS=0).execute(s.samples)
+    want, _ = O.reconstruct_nedner(s.positions, s.weights, s.samples, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    err = rel_l2(got, want)
+    print(f"cfg3 gridding form f16={f16}: rel-L2 {err:.3e}")
+    assert err <= TOL
+
+
+def test_gpu_gridding_mixed_amplitudes_vs_oracle():
+    """One loud sensor row next to quiet ones: still within the parity bar."""
+    s = synth.CONFIGS["cfg2"]()
+    smp = s.samples.copy()
+    smp[17] *= 1e4
+    smp[1000] *= 1e-4
+    got, _ = _plan_env(s, PATFFT_SPREAD_F16_MIN_ITEMS=0).execute(smp)
+    want, _ = O.reconstruct_nedner(s.positions, s.weights, smp, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    err = rel_l2(got, want)
+    print(f"mixed amplitudes: rel-L2 {err:.3e}")
+    assert err <= TOL
