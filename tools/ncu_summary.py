@@ -60,7 +60,7 @@ for k in res:
         k["warps_active_pct"], k["regs"]))
 if len(sys.argv) > 4:
     tj, cfg = sys.argv[3], sys.argv[4]
-    stage_of = [("spread", "spread"), ("colfft", "lateral_col"), ("rowfft", "lateral_row"), ("ner_", "ner"),
+    stage_of = [("spread", "spread"), ("absmax", "spread"), ("colfft", "lateral_col"), ("rowfft", "lateral_row"), ("ner_", "ner"),
                 ("inv_", "inverse")]
     traffic = {}
     for k in res:

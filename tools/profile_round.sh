@@ -14,3 +14,8 @@ timeout 900 ncu --set full --import-source on --clock-control none -f -o gpurun_
   python tools/profile_step.py --iters 1 > gpurun_out/prof/ncu_full.log 2>&1
 python tools/ncu_summary.py gpurun_out/prof/full_cfg4.ncu-rep gpurun_out/prof/ncu_full_summary.json gpurun_out/prof/traffic.json cfg4
 echo PROFILE_OK
+# the sharded (multi-GPU) code path at world size 1 under torchrun, as the driver launches N > 1
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 \
+  bench.py --gpus 1 --sharded --steps 10 --warmup 3 > gpurun_out/prof/bench_cfg4_sharded_w1.json 2> gpurun_out/prof/sharded.err || tail -5 gpurun_out/prof/sharded.err
+timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/prof/bench_cfg4_reference.json 2> gpurun_out/prof/ref.err || tail -5 gpurun_out/prof/ref.err
+echo PROFILE_DONE
