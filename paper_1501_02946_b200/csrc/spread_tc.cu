@@ -527,6 +527,9 @@ __device__ __forceinline__ void c16_next(Cursor16& u, const Item16* ring) {
 #ifndef PATFFT_TC16_NOEPI
 #define PATFFT_TC16_NOEPI 0
 #endif
+#ifndef PATFFT_TC16_MBAR
+#define PATFFT_TC16_MBAR 0  // B hand-off by an mbarrier only the MMA thread and load warp wait on (1): measured 0.504 vs 0.480 ms
+#endif
 
 template <int N>
 __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const SpreadParams p) {
@@ -547,7 +550,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
   uint8_t* const b_ops = smem + A_SLOTS * A_SLOT;
   float* const s_ring = reinterpret_cast<float*>(b_ops + BO_AREA);  // 2 x S_SLOT
   constexpr int OFF_SLOTS = 8;  // sample row offsets of stage x: slot x % 8, fetched at stage x - 4
-  __shared__ uint64_t mma_bar[2], ld_bar[2], off_bar[OFF_SLOTS];
+  __shared__ uint64_t mma_bar[2], ld_bar[2], off_bar[OFF_SLOTS], full_bar[2];
   __shared__ __align__(16) uint32_t offbuf[OFF_SLOTS * kKC];
   __shared__ uint32_t tmem_base_s;
   __shared__ Item16 ring[kRing];
@@ -588,6 +591,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
     for (int s2 = 0; s2 < 2; ++s2) {
       mbar_init_tc(&mma_bar[s2], 1);
       mbar_init_tc(&ld_bar[s2], 1);
+      mbar_init_tc(&full_bar[s2], kThreadsTC);
     }
     for (int s2 = 0; s2 < OFF_SLOTS; ++s2) mbar_init_tc(&off_bar[s2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -705,7 +709,11 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
 
   for (int g = 0; c16_valid(cur); ++g) {
     const int sb = g & 1;
-    if (g >= 2) mbar_wait_tc(&mma_bar[sb], ((g >> 1) - 1) & 1);  // B slot free (stage g - 2 done)
+    if (g >= 2) {
+      mbar_wait_tc(&mma_bar[sb], ((g >> 1) - 1) & 1);  // B slot free (stage g - 2 done)
+      // (acquire of everyone's stage g - 2 arrival: the ring entries thread 0 resolved before it)
+      if (PATFFT_TC16_MBAR) mbar_wait_tc(&full_bar[sb], ((g >> 1) - 1) & 1);
+    }
     mbar_wait_tc(&ld_bar[sb], (g >> 1) & 1);                      // A + samples of stage g landed
     uint8_t* bo = b_ops + sb * B_SLOT;
     const float* sr = s_ring + sb * (S_SLOT / 4);
@@ -723,7 +731,14 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
+    if (PATFFT_TC16_MBAR) {
+      // B of stage g is complete once all threads arrived; only the MMA thread and the
+      // load warp wait for it, the other warps go on to stage g + 1
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full_bar[sb])) : "memory");
+      if (tid == 0 || warp == 1) mbar_wait_tc(&full_bar[sb], (g >> 1) & 1);
+    } else {
+      __syncthreads();
+    }
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a_hi = su32(a_ring + (g % A_SLOTS) * A_SLOT), a_lo = a_hi + A_SLOT / 2;
@@ -745,7 +760,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
       }
     } else if (warp == 1) {
       // stage g + 2: A slot (g + 2) % 4 was read by stage g - 2 (complete), sample slot sb was
-      // read by this stage's B build (before the barrier above)
+      // read by this stage's B build (all threads arrived above)
       if (c16_valid(cs)) issue_loads(g + 2, cs);
       c16_next(cs, ring);
     }
