@@ -367,6 +367,10 @@ __device__ __forceinline__ void last_pass_inplace(float2* __restrict__ buf, cons
 #ifndef PATFFT_NER_DCT_DIV
 #define PATFFT_NER_DCT_DIV 8  // threads per CTA = T / 8 (measured: 4 and 16 slower)
 #endif
+#ifndef PATFFT_NER_DIRECT
+#define PATFFT_NER_DIRECT 0  // 1: targets stored straight to a second buffer, loop not unrolled (kernel code
+                             // 3672 -> 2152 instructions) -- measured 0.567 vs 0.560 ms, so not the bound
+#endif
 #ifndef PATFFT_NER_DCT_MAXR
 #define PATFFT_NER_DCT_MAXR 4
 #endif
@@ -462,9 +466,22 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
     return acc;
   };
   constexpr int kPairs = (T / 2 + NTH) / NTH;  // |l| in [0, T/2]
+#if PATFFT_NER_DIRECT
+  // targets go straight into a separate depth-spectrum buffer (bit-reversed,
+  // swizzled) behind the D' array: no per-target registers, and the target
+  // loop is not unrolled (five inlined copies of the interpolation made the
+  // kernel's code larger than the instruction cache)
+  float2* __restrict__ obuf = sbuf + (2 * T + 2 * T / 16);
+  const fft::SwzC<LOGT> iad;
+#else
   float2 valsP[kPairs], valsM[kPairs];
+#endif
   const float2 g0 = gload(0);
+#if PATFFT_NER_DIRECT
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
   for (int it = 0; it < kPairs; ++it) {
     const int lh = tid + it * NTH;
     float2 vp = make_float2(0.f, 0.f), vm = make_float2(0.f, 0.f);
@@ -484,11 +501,22 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
         vm = make_float2(a * (rx - sy + g0.x), a * (ry + sx + g0.y));  // e^{+i pi ke} D + g0
       }
     }
+#if PATFFT_NER_DIRECT
+    if (lh <= T / 2) {
+      if (lh < T / 2) obuf[iad(fft::brev(lh, LOGT), 0)] = vp;
+      if (lh > 0) obuf[iad(fft::brev(T - lh, LOGT), 0)] = vm;
+    }
+#else
     valsP[it] = vp;
     valsM[it] = vm;
+#endif
   }
 
   // 3. depth inverse FFT (recon.py:255) straight to z (up == 1: row j0w * N1h + j1)
+#if PATFFT_NER_DIRECT
+  float2* __restrict__ ibuf = obuf;
+#else
+  float2* __restrict__ ibuf = sbuf;
   __syncthreads();  // spectrum fully consumed
   {
     const fft::SwzC<LOGT> iad;
@@ -500,13 +528,14 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
       if (lh > 0) sbuf[iad(fft::brev(T - lh, LOGT), 0)] = valsM[it];
     }
   }
+#endif
   __syncthreads();
   const int tco = p.out_tchunk;
   const size_t zstride = (size_t)p.rows_out * tco;
   float2* __restrict__ z0 = p.z + (size_t)(r - p.out_row0) * tco;
   const bool flat_out = p.out_tshift >= 31;
   fft::fft_ct_stored<true, LOGT, PATFFT_NER_INV_MAXR, true, 0, NTH>(
-      sbuf, p.tw, tid, fft::SwzC<LOGT>(), [&](int i, int, float2 v) {
+      ibuf, p.tw, tid, fft::SwzC<LOGT>(), [&](int i, int, float2 v) {
         z0[flat_out ? (size_t)i : (i >> p.out_tshift) * zstride + (i & p.out_tmask)] = v;
       });
 }
@@ -547,7 +576,7 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
   if (ct_ok && dct && p.pre) {
     // DCT form: 2T-point transform, half the shared memory
     threads = std::max(64, std::min(512, p.T / PATFFT_NER_DCT_DIV));
-    const size_t smem2 = (size_t)(2 * p.T + 2 * p.T / 16) * sizeof(float2);
+    const size_t smem2 = (size_t)(2 * p.T + 2 * p.T / 16 + (PATFFT_NER_DIRECT ? p.T : 0)) * sizeof(float2);
     auto go2 = [&](auto kern) {
       err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
       if (err != cudaSuccess) return;
