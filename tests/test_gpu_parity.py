@@ -434,3 +434,14 @@ def test_gpu_gridding_mixed_amplitudes_vs_oracle():
     err = rel_l2(got, want)
     print(f"mixed amplitudes: rel-L2 {err:.3e}")
     assert err <= TOL
+
+
+@pytest.mark.parametrize("nt", [96, 320, 384])
+def test_gpu_fp16_gridding_short_time_blocks_vs_oracle(nt):
+    """fp16 tensor-core gridding with N = 32 / 64 / 128 time samples per work item."""
+    s = synth.make_3d(11, 32, nt, 20e-9, "jittered", 2)
+    got, _ = _plan_env(s, PATFFT_SPREAD_F16_MIN_ITEMS=0).execute(s.samples)
+    want, _ = O.reconstruct_nedner(s.positions, s.weights, s.samples, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    err = rel_l2(got, want)
+    print(f"fp16 gridding T={nt}: rel-L2 {err:.3e}")
+    assert err <= TOL
