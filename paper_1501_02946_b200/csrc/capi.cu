@@ -9,6 +9,7 @@
 // per contributing sensor (R row weights, 2K column weights, column window),
 // sorted by column window and split into column segments for load balance.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <cufft.h>
 
 #include <algorithm>
@@ -115,6 +116,8 @@ void set_tc(const patfft_nedner_plan* P, SpreadParams& sp) {
   sp.tc_wexp = P->tc_wexp;
   sp.tc_m = P->M;
   sp.tc_a16 = P->d_tc_a16;
+  sp.tc_tma_store = P->tc_tma_store ? 1 : 0;
+  if (P->tc_tma_store) sp.tc_gmap = P->tc_gmap;
   sp.tc_off = P->d_tc_off;
 }
 
@@ -696,6 +699,30 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   if ((rc = upload(&P->d_pre, pre))) return rc;
   if ((rc = upload(&P->d_tw, tw))) return rc;
   if ((rc = dalloc(&P->d_grid, (size_t)nrows * ncols * T))) return rc;
+  // fp16 gridding epilogue: TMA tensor stores of 32-sample x 16-column x 2-row boxes of the grid,
+  // read from the kernel's 128B-swizzled staging (PATFFT_TC16_TMA=0: per-thread stores)
+  if (P->tc_f16 && T % 32 == 0) {
+    const char* e = std::getenv("PATFFT_TC16_TMA");
+    if (!e || std::atoi(e) != 0) {
+      static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+      if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+          encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        cudaGetLastError();
+      }
+      if (encode) {
+        const cuuint64_t dims[3] = {(cuuint64_t)T, (cuuint64_t)ncols, (cuuint64_t)nrows};
+        const cuuint64_t strides[2] = {(cuuint64_t)T * 4, (cuuint64_t)ncols * T * 4};
+        const cuuint32_t box[3] = {32, 16, 2}, estr[3] = {1, 1, 1};
+        P->tc_tma_store = encode(&P->tc_gmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, P->d_grid, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      }
+    }
+  }
   if ((rc = dalloc(&P->d_Y, (size_t)nrows * P->N1h * T))) return rc;
   if (world == 1) {
     if ((rc = dalloc(&P->d_gh, (size_t)P->N0 * P->N1h * T))) return rc;

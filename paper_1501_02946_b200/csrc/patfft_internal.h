@@ -2,6 +2,7 @@
 // the C ABI.  Not part of the public interface (include/patfft_b200.h).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cufft.h>
 
@@ -61,6 +62,8 @@ struct SpreadParams {
   int tc_m = 0;                        // sensor rows of `samples`
   const uint4* tc_a16 = nullptr;       // per stage: A operands hi/lo (fp16, UMMA layout), 8 KB
   const uint32_t* tc_off = nullptr;    // per stage: 16 sample row offsets
+  int tc_tma_store = 0;                // 1: epilogue stores through tc_gmap (TMA tensor stores)
+  CUtensorMap tc_gmap;                 // grid [nrows][ncols][T] f32, box 32 t x 16 cols x 2 rows, 128B swizzle
 };
 
 struct LateralParams {
@@ -197,6 +200,8 @@ struct patfft_nedner_plan {
   int4* d_tc_tiles = nullptr;
   int* d_tc_counter = nullptr;  // 2 ints
   uint4* d_tc_a16 = nullptr;
+  bool tc_tma_store = false;
+  CUtensorMap tc_gmap;
   uint32_t* d_tc_off = nullptr;
   int tc_f16 = 0, tc_wexp = 0;
   int tc_ntiles = 0, tc_nonempty = 0, tc_n = 0;

@@ -532,7 +532,7 @@ __device__ __forceinline__ void c16_next(Cursor16& u, const Item16* ring) {
 #endif
 
 template <int N>
-__global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const SpreadParams p) {
+__global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid_constant__ SpreadParams p) {
   constexpr int A_SLOT = 8192;                     // hi + lo, [part][octet][128][8] halves
   constexpr int A_SLOTS = 4;
   constexpr int B_HALF = kKC * N * 2;              // one part: [octet][N][8] halves
@@ -688,11 +688,30 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
             "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
           : "r"(ta));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (p.tc_tma_store) {  // the previous chunk's tensor store must have read the staging
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+      }
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         *reinterpret_cast<float4*>(stg + lane * 32 + ((q ^ (lane & 7)) * 4)) =
             make_float4(__uint_as_float(r[4 * q]) * o_scale, __uint_as_float(r[4 * q + 1]) * o_scale,
                         __uint_as_float(r[4 * q + 2]) * o_scale, __uint_as_float(r[4 * q + 3]) * o_scale);
+      if (p.tc_tma_store) {
+        // the warp's 32 points are 2 grid rows x 16 columns: one 32 x 16 x 2 box; the staging's XOR
+        // swizzle (16-byte chunk q of point row pl at q ^ (pl & 7)) is the 128B swizzle of the map
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && !PATFFT_TC16_NOSTORE) {
+          asm volatile(
+              "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                  reinterpret_cast<uint64_t>(&p.tc_gmap)),
+              "r"(t0 + j * 32), "r"(cur.it.col0), "r"(cur.it.row0 + q4 * 2), "r"(su32(stg))
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        continue;
+      }
       __syncwarp();
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -703,6 +722,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
       }
       __syncwarp();
     }
+    if (p.tc_tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
   };
@@ -767,6 +787,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const Spread
     if (cur.c == cur.it.nch - 1) epilogue(g);
     c16_next(cur, ring);
   }
+  if (p.tc_tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
 }
 
