@@ -316,6 +316,51 @@ __device__ __forceinline__ float2 last_pass_output(const float2* __restrict__ bu
 // from a bit-reversed shared-memory copy: saves one shared-memory round trip.
 // With a single transform (PLOG = 0) item q is given to thread brev(q), so a
 // warp's loads are consecutive natural indices.  Ends with __syncthreads.
+// fft_ct_loaded for inputs that are rows of a strided array: rowptr(nat, p)
+// returns the address of element (row nat, transform p), or nullptr when
+// transform p is out of range (zeros); consecutive rows are `stride` float2
+// apart.  The first pass then loads its radix-2^R elements from one base
+// pointer with a running offset instead of recomputing each address.
+template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, bool SKIP_LAST = false, class Addr, class RowPtr>
+__device__ __forceinline__ void fft_ct_loaded_rows(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
+                                                   Addr addr, RowPtr rowptr, size_t stride) {
+  constexpr int R = PassRadix<L, MAXR, EVEN, 0>::value;
+  constexpr int PR = 1 << R;
+  constexpr int ITEMS = 1 << (L - R + PLOG);
+  constexpr int ITER = (ITEMS + NTH - 1) / NTH;
+  const size_t st = stride << (L - R);  // natural row k of the item: nat0 + k 2^(L-R)
+#pragma unroll
+  for (int j = 0; j < ITER; ++j) {
+    const int it = tid + j * NTH;
+    if ((ITEMS % NTH) != 0 && it >= ITEMS) break;
+    const int p = it & ((1 << PLOG) - 1);
+    const int qi = it >> PLOG;
+    const int q = PLOG == 0 ? brev(qi, L - R) : qi;
+    const int nat0 = PLOG == 0 ? qi : brev(qi, L - R);
+    float2 e[PR];
+    const float2* b = rowptr(nat0, p);
+    if (b) {
+#pragma unroll
+      for (int k = 0; k < PR; ++k) e[brev_c(k, R)] = __ldcs(b + k * st);  // element m = brev(k)
+    } else {
+#pragma unroll
+      for (int k = 0; k < PR; ++k) e[k] = make_float2(0.f, 0.f);
+    }
+    pass_butterflies<R, INV, 0>(e, 0, tw);
+    const int base = q << R;
+    int ab = 0;
+    if constexpr (XorLinear<Addr>::value) ab = addr(base, p);
+#pragma unroll
+    for (int m = 0; m < PR; ++m) {
+      if constexpr (XorLinear<Addr>::value) buf[ab ^ addr(m, 0)] = e[m];
+      else buf[addr(base + m, p)] = e[m];
+    }
+  }
+  __syncthreads();
+  if constexpr (SKIP_LAST) fft_ct_but_last<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
+  else fft_ct<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
+}
+
 template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, bool SKIP_LAST = false, class Addr, class Load>
 __device__ __forceinline__ void fft_ct_loaded(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
                                               Addr addr, Load load) {

@@ -31,6 +31,9 @@ using fft::TileAddr;
 #ifndef PATFFT_LAT_FUSED
 #define PATFFT_LAT_FUSED 1  // colfft/rowfft: last FFT pass evaluated inside the crop/unpack epilogue
 #endif
+#ifndef PATFFT_LAT_ROWPTR
+#define PATFFT_LAT_ROWPTR 1  // colfft/rowfft first pass: one base pointer + running row offset per item
+#endif
 #ifndef PATFFT_ROW_FUSED
 #define PATFFT_ROW_FUSED 0  // measured slower for rowfft (half the outputs are cropped away anyway)
 #endif
@@ -81,7 +84,15 @@ __global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kerne
   };
   constexpr int LLAST = LC > 0 ? fft::LastPassLogh<(LC > 0 ? LC : 1), 4, false>::value : 0;
   constexpr bool FUSED = PATFFT_LAT_FUSED && LC > 0 && LLAST > 0;
-  if constexpr (LC > 0) {
+  if constexpr (LC > 0 && PATFFT_LAT_ROWPTR) {
+    fft::fft_ct_loaded_rows<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(
+        sm, p.tw, tid, fft::TileC<PLOG>(),
+        [&](int row, int q) -> const float2* {
+          const int t = t0 + 2 * q;
+          return t < p.t_end ? reinterpret_cast<const float2*>(src + (size_t)row * T + t) : nullptr;
+        },
+        (size_t)(T / 2));
+  } else if constexpr (LC > 0) {
     fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
   } else {
     fft::staged_copy<8, float2>(
@@ -139,7 +150,15 @@ __global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kerne
   };
   constexpr int LLAST = LC > 0 ? fft::LastPassLogh<(LC > 0 ? LC : 1), 4, false>::value : 0;
   constexpr bool FUSED = PATFFT_ROW_FUSED && LC > 0 && LLAST > 0;
-  if constexpr (LC > 0) {
+  if constexpr (LC > 0 && PATFFT_LAT_ROWPTR) {
+    fft::fft_ct_loaded_rows<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(
+        sm, p.tw, tid, fft::TileC<PLOG>(),
+        [&](int row, int q) -> const float2* {
+          const int t = t0 + q;
+          return t < p.t_end ? p.Y + ((size_t)row * p.ny + j1) * T + t : nullptr;
+        },
+        (size_t)p.ny * T);
+  } else if constexpr (LC > 0) {
     fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
   } else {
     fft::staged_copy<8, float2>(
