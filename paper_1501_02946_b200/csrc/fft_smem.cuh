@@ -311,56 +311,68 @@ __device__ __forceinline__ float2 last_pass_output(const float2* __restrict__ bu
   return acc;
 }
 
+// Global operands that are rows of a strided array: ptr(row, p) is the
+// address of element (row, transform p), or nullptr when transform p is out
+// of range (loads give zeros, stores are dropped); consecutive rows are
+// `stride` float2 apart.  The first pass then loads an item's radix-2^R
+// elements, and the last pass stores them, from one base pointer with a
+// running offset instead of recomputing every address.
+template <class F, bool STREAM>
+struct RowsLd {
+  F ptr;
+  size_t stride;
+};
+template <class F>
+struct RowsSt {
+  F ptr;
+  size_t stride;
+};
+template <bool STREAM = true, class F>
+__device__ __forceinline__ RowsLd<F, STREAM> rows_ld(F f, size_t stride) {
+  return {f, stride};
+}
+template <class F>
+__device__ __forceinline__ RowsSt<F> rows_st(F f, size_t stride) {
+  return {f, stride};
+}
+// element m of the first-pass item at natural row (brev(m) << (L - R)) + nat0
+template <int R, int L, class Load>
+__device__ __forceinline__ void load_items(float2 (&e)[1 << R], int nat0, int p, const Load& load) {
+#pragma unroll
+  for (int m = 0; m < (1 << R); ++m) e[m] = load((brev_c(m, R) << (L - R)) + nat0, p);
+}
+template <int R, int L, class F, bool STREAM>
+__device__ __forceinline__ void load_items(float2 (&e)[1 << R], int nat0, int p, const RowsLd<F, STREAM>& rl) {
+  const float2* b = rl.ptr(nat0, p);
+  const size_t st = rl.stride << (L - R);
+  if (b) {
+#pragma unroll
+    for (int k = 0; k < (1 << R); ++k) e[brev_c(k, R)] = STREAM ? __ldcs(b + k * st) : b[k * st];
+  } else {
+#pragma unroll
+    for (int k = 0; k < (1 << R); ++k) e[k] = make_float2(0.f, 0.f);
+  }
+}
+// last-pass outputs m of an item at natural rows base + m H
+template <int R, int H, class Store>
+__device__ __forceinline__ void store_items(const float2 (&e)[1 << R], int base, int p, const Store& store) {
+#pragma unroll
+  for (int m = 0; m < (1 << R); ++m) store(base + m * H, p, e[m]);
+}
+template <int R, int H, class F>
+__device__ __forceinline__ void store_items(const float2 (&e)[1 << R], int base, int p, const RowsSt<F>& rs) {
+  float2* b = rs.ptr(base, p);
+  if (!b) return;
+  const size_t st = rs.stride * H;
+#pragma unroll
+  for (int m = 0; m < (1 << R); ++m) b[m * st] = e[m];
+}
+
 // Full compile-time transform whose first pass reads its inputs straight
 // from `load(n, p)` (element n in natural order of transform p) instead of
 // from a bit-reversed shared-memory copy: saves one shared-memory round trip.
 // With a single transform (PLOG = 0) item q is given to thread brev(q), so a
 // warp's loads are consecutive natural indices.  Ends with __syncthreads.
-// fft_ct_loaded for inputs that are rows of a strided array: rowptr(nat, p)
-// returns the address of element (row nat, transform p), or nullptr when
-// transform p is out of range (zeros); consecutive rows are `stride` float2
-// apart.  The first pass then loads its radix-2^R elements from one base
-// pointer with a running offset instead of recomputing each address.
-template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, bool SKIP_LAST = false, class Addr, class RowPtr>
-__device__ __forceinline__ void fft_ct_loaded_rows(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
-                                                   Addr addr, RowPtr rowptr, size_t stride) {
-  constexpr int R = PassRadix<L, MAXR, EVEN, 0>::value;
-  constexpr int PR = 1 << R;
-  constexpr int ITEMS = 1 << (L - R + PLOG);
-  constexpr int ITER = (ITEMS + NTH - 1) / NTH;
-  const size_t st = stride << (L - R);  // natural row k of the item: nat0 + k 2^(L-R)
-#pragma unroll
-  for (int j = 0; j < ITER; ++j) {
-    const int it = tid + j * NTH;
-    if ((ITEMS % NTH) != 0 && it >= ITEMS) break;
-    const int p = it & ((1 << PLOG) - 1);
-    const int qi = it >> PLOG;
-    const int q = PLOG == 0 ? brev(qi, L - R) : qi;
-    const int nat0 = PLOG == 0 ? qi : brev(qi, L - R);
-    float2 e[PR];
-    const float2* b = rowptr(nat0, p);
-    if (b) {
-#pragma unroll
-      for (int k = 0; k < PR; ++k) e[brev_c(k, R)] = __ldcs(b + k * st);  // element m = brev(k)
-    } else {
-#pragma unroll
-      for (int k = 0; k < PR; ++k) e[k] = make_float2(0.f, 0.f);
-    }
-    pass_butterflies<R, INV, 0>(e, 0, tw);
-    const int base = q << R;
-    int ab = 0;
-    if constexpr (XorLinear<Addr>::value) ab = addr(base, p);
-#pragma unroll
-    for (int m = 0; m < PR; ++m) {
-      if constexpr (XorLinear<Addr>::value) buf[ab ^ addr(m, 0)] = e[m];
-      else buf[addr(base + m, p)] = e[m];
-    }
-  }
-  __syncthreads();
-  if constexpr (SKIP_LAST) fft_ct_but_last<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
-  else fft_ct<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
-}
-
 template <bool INV, int L, int MAXR, bool EVEN, int PLOG, int NTH, bool SKIP_LAST = false, class Addr, class Load>
 __device__ __forceinline__ void fft_ct_loaded(float2* __restrict__ buf, const float2* __restrict__ tw, int tid,
                                               Addr addr, Load load) {
@@ -377,8 +389,7 @@ __device__ __forceinline__ void fft_ct_loaded(float2* __restrict__ buf, const fl
     const int q = PLOG == 0 ? brev(qi, L - R) : qi;
     const int nat0 = PLOG == 0 ? qi : brev(qi, L - R);  // natural index of element m = 0
     float2 e[PR];
-#pragma unroll
-    for (int m = 0; m < PR; ++m) e[m] = load((brev_c(m, R) << (L - R)) + nat0, p);
+    load_items<R, L>(e, nat0, p, load);
     pass_butterflies<R, INV, 0>(e, 0, tw);
     const int base = q << R;
     int ab = 0;
@@ -393,6 +404,7 @@ __device__ __forceinline__ void fft_ct_loaded(float2* __restrict__ buf, const fl
   if constexpr (SKIP_LAST) fft_ct_but_last<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
   else fft_ct<INV, L, MAXR, EVEN, PLOG, NTH, R>(buf, tw, tid, addr);
 }
+
 
 // Last pass that hands its outputs (natural order) to `store(n, p, v)`
 // instead of writing them back to shared memory.  No trailing barrier.
@@ -420,8 +432,7 @@ __device__ __forceinline__ void dit_pass_ct_st(float2* __restrict__ buf, const f
       else e[m] = buf[addr(base + m * H, p)];
     }
     pass_butterflies<R, INV, LOGH>(e, k, tw);
-#pragma unroll
-    for (int m = 0; m < PR; ++m) store(base + m * H, p, e[m]);
+    store_items<R, H>(e, base, p, store);
   }
 }
 
@@ -464,8 +475,7 @@ __device__ __forceinline__ void fft_ct_loaded_stored(float2* __restrict__ buf, c
     const int q = PLOG == 0 ? brev(qi, L - R) : qi;
     const int nat0 = PLOG == 0 ? qi : brev(qi, L - R);
     float2 e[PR];
-#pragma unroll
-    for (int m = 0; m < PR; ++m) e[m] = load((brev_c(m, R) << (L - R)) + nat0, p);
+    load_items<R, L>(e, nat0, p, load);
     pass_butterflies<R, INV, 0>(e, 0, tw);
     const int base = q << R;
     int ab = 0;

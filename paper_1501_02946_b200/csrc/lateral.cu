@@ -85,13 +85,11 @@ __global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kerne
   constexpr int LLAST = LC > 0 ? fft::LastPassLogh<(LC > 0 ? LC : 1), 4, false>::value : 0;
   constexpr bool FUSED = PATFFT_LAT_FUSED && LC > 0 && LLAST > 0;
   if constexpr (LC > 0 && PATFFT_LAT_ROWPTR) {
-    fft::fft_ct_loaded_rows<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(
-        sm, p.tw, tid, fft::TileC<PLOG>(),
-        [&](int row, int q) -> const float2* {
+    fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(
+        sm, p.tw, tid, fft::TileC<PLOG>(), fft::rows_ld([&](int row, int q) -> const float2* {
           const int t = t0 + 2 * q;
           return t < p.t_end ? reinterpret_cast<const float2*>(src + (size_t)row * T + t) : nullptr;
-        },
-        (size_t)(T / 2));
+        }, (size_t)(T / 2)));
   } else if constexpr (LC > 0) {
     fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
   } else {
@@ -151,13 +149,11 @@ __global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kerne
   constexpr int LLAST = LC > 0 ? fft::LastPassLogh<(LC > 0 ? LC : 1), 4, false>::value : 0;
   constexpr bool FUSED = PATFFT_ROW_FUSED && LC > 0 && LLAST > 0;
   if constexpr (LC > 0 && PATFFT_LAT_ROWPTR) {
-    fft::fft_ct_loaded_rows<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(
-        sm, p.tw, tid, fft::TileC<PLOG>(),
-        [&](int row, int q) -> const float2* {
+    fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(
+        sm, p.tw, tid, fft::TileC<PLOG>(), fft::rows_ld([&](int row, int q) -> const float2* {
           const int t = t0 + q;
           return t < p.t_end ? p.Y + ((size_t)row * p.ny + j1) * T + t : nullptr;
-        },
-        (size_t)p.ny * T);
+        }, (size_t)p.ny * T));
   } else if constexpr (LC > 0) {
     fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
   } else {
@@ -230,7 +226,13 @@ __global__ void __launch_bounds__(inv_lb_threads(PLOG, LC), inv_lb_minb(PLOG, LC
     const int t = t0 + q;
     if (t < T) z[((size_t)row * p.N1uh + j1) * T + t] = v;
   };
-  if constexpr (LC > 4 && PATFFT_INVCOL_STORED) {
+  if constexpr (LC > 4 && PATFFT_INVCOL_STORED && PATFFT_LAT_ROWPTR) {
+    const size_t rs = (size_t)p.N1uh * T;
+    auto rp = [&](int row, int q) -> float2* { return t0 + q < T ? z + (size_t)row * rs + j1 * (size_t)T + t0 + q : nullptr; };
+    fft::fft_ct_loaded_stored<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(
+        sm, p.tw, tid, fft::TileC<PLOG>(),
+        fft::rows_ld<false>([&](int row, int q) -> const float2* { return rp(row, q); }, rs), fft::rows_st(rp, rs));
+  } else if constexpr (LC > 4 && PATFFT_INVCOL_STORED) {
     fft::fft_ct_loaded_stored<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld, st);
   } else if constexpr (LC > 0) {
     fft::fft_ct_loaded<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
@@ -280,7 +282,15 @@ __global__ void __launch_bounds__(inv_lb_threads(PLOG, LC), inv_lb_minb(PLOG, LC
       const float2 o = lo ? make_float2(v.x - v.w, v.y + v.z) : make_float2(v.x + v.w, v.z - v.y);
       return t < T ? o : make_float2(0.f, 0.f);
     };
-    fft::fft_ct_loaded_stored<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld, st);
+    if constexpr (PATFFT_LAT_ROWPTR) {
+      fft::fft_ct_loaded_stored<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(
+          sm, p.tw, tid, fft::TileC<PLOG>(), ld, fft::rows_st([&](int row, int q) -> float2* {
+            const int t = t0 + 2 * q;
+            return t < T ? reinterpret_cast<float2*>(out + (size_t)row * T + t) : nullptr;
+          }, (size_t)(T / 2)));
+    } else {
+      fft::fft_ct_loaded_stored<true, LC, 4, false, PLOG, nth_for(LC, PLOG)>(sm, p.tw, tid, fft::TileC<PLOG>(), ld, st);
+    }
     return;
   }
   fft::staged_copy<8, float4>(
