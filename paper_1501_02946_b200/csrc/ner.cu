@@ -367,6 +367,9 @@ __device__ __forceinline__ void last_pass_inplace(float2* __restrict__ buf, cons
 #ifndef PATFFT_NER_DCT_DIV
 #define PATFFT_NER_DCT_DIV 8  // threads per CTA = T / 8 (measured: 4 and 16 slower)
 #endif
+#ifndef PATFFT_NER_EXTLOAD
+#define PATFFT_NER_EXTLOAD 1  // first pass: running pointers into gh and pre[] (NerExtLoad)
+#endif
 #ifndef PATFFT_NER_DIRECT
 #define PATFFT_NER_DIRECT 0  // 1: targets stored straight to a second buffer, loop not unrolled (kernel code
                              // 3672 -> 2152 instructions) -- measured 0.567 vs 0.560 ms, so not the bound
@@ -382,6 +385,48 @@ constexpr int ner_dct_threads(int logt) {
 #define PATFFT_NER_DCT_REGS 64  // 8 CTAs of 128 threads per SM (measured best; 48, 56, 72, 80, 96 slower)
 #endif
 constexpr int ner_dct_minb(int logt) { return (65536 / PATFFT_NER_DCT_REGS) / ner_dct_threads(logt); }
+
+// First-pass operand of the DCT-form NER: element n of the 2T-point input is
+// gh[|n - T|] (the even extension folded about T) times pre[n], zero at n = 0
+// and n = T.  For an item's elements n = nat0 + k S (S = 2^(L-R)), k < 2^(R-1)
+// read gh[T - nat0 - k S] and the rest gh[nat0 + (k - 2^(R-1)) S]: two base
+// pointers with running offsets (single-GPU rows are contiguous in time; the
+// sharded layout keeps the general addressing).
+struct NerExtLoad {
+  const float2* g;
+  const float2* pre;
+  int T;
+  bool flat;
+  size_t gstride;
+  int tshift, tmask;
+  __device__ __forceinline__ float2 at(int t) const {
+    return __ldcs(flat ? &g[t] : &g[(t >> tshift) * gstride + (t & tmask)]);
+  }
+};
+template <int R, int L>
+__device__ __forceinline__ void load_items(float2 (&e)[1 << R], int nat0, int, const NerExtLoad& ld) {
+  constexpr int KH = 1 << (R - 1);
+  constexpr int S = 1 << (L - R);
+  const float2* pr = ld.pre + nat0;
+  if (ld.flat) {
+    const float2* ga = ld.g + (ld.T - nat0);
+    const float2* gb = ld.g + nat0;
+#pragma unroll
+    for (int k = 0; k < (1 << R); ++k) {
+      const float2 v = k < KH ? ((k == 0 && nat0 == 0) ? make_float2(0.f, 0.f) : __ldcs(ga - k * S))
+                              : __ldcs(gb + (k - KH) * S);
+      e[fft::brev_c(k, R)] = fft::cmul(v, __ldg(pr + k * S));
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < (1 << R); ++k) {
+      const int n = nat0 + k * S;
+      const float2 v = (k == 0 && nat0 == 0) ? make_float2(0.f, 0.f) : ld.at(k < KH ? ld.T - n : n - ld.T);
+      e[fft::brev_c(k, R)] = fft::cmul(v, __ldg(pr + k * S));
+    }
+  }
+  if (nat0 == 0) e[fft::brev_c(KH, R)] = make_float2(0.f, 0.f);  // n = T
+}
 
 template <int K2, int D, int LOGT>
 __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner_dct_kernel(const NerParams p) {
@@ -409,11 +454,16 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   // the last pass stores D'[q] in natural order (Makhoul output permutation
   // Z[n] -> D'[n < 2T/2 ? 2n : 4T-1-2n]) into the same swizzled buffer
   const fft::SwzC<L> ad;
+#if PATFFT_NER_EXTLOAD
+  fft::fft_ct_loaded<true, L, PATFFT_NER_DCT_MAXR, true, 0, NTH, true>(
+      sbuf, p.tw, tid, ad, NerExtLoad{g, p.pre, T, flat_in, gstride, p.in_tshift, p.in_tmask});
+#else
   fft::fft_ct_loaded<true, L, PATFFT_NER_DCT_MAXR, true, 0, NTH, true>(sbuf, p.tw, tid, ad, [&](int n, int) {
     if (n == 0 || n == T) return make_float2(0.f, 0.f);
     const float2 gv = gload(n < T ? T - n : n - T);
     return fft::cmul(gv, __ldg(&p.pre[n]));
   });
+#endif
   {
     constexpr int LH = fft::LastPassLogh<L, PATFFT_NER_DCT_MAXR, true>::value;
     last_pass_inplace<L - LH, true, L, LH, NTH>(sbuf, p.tw, tid, ad, [&](int n, float2 v) {
