@@ -428,6 +428,29 @@ __device__ __forceinline__ void load_items(float2 (&e)[1 << R], int nat0, int, c
   if (nat0 == 0) e[fft::brev_c(KH, R)] = make_float2(0.f, 0.f);  // n = T
 }
 
+// Last-pass store of the depth IFFT into the z row: contiguous on one GPU,
+// [time chunk][row][t] in the sharded layout.
+struct NerZStore {
+  float2* z0;
+  bool flat;
+  size_t zstride;
+  int tshift, tmask;
+};
+template <int R, int H>
+__device__ __forceinline__ void store_items(const float2 (&e)[1 << R], int base, int, const NerZStore& st) {
+  if (st.flat) {
+    float2* b = st.z0 + base;
+#pragma unroll
+    for (int m = 0; m < (1 << R); ++m) b[m * H] = e[m];
+  } else {
+#pragma unroll
+    for (int m = 0; m < (1 << R); ++m) {
+      const int i = base + m * H;
+      st.z0[(i >> st.tshift) * st.zstride + (i & st.tmask)] = e[m];
+    }
+  }
+}
+
 template <int K2, int D, int LOGT>
 __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner_dct_kernel(const NerParams p) {
   constexpr int T = 1 << LOGT;
@@ -584,10 +607,15 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   const size_t zstride = (size_t)p.rows_out * tco;
   float2* __restrict__ z0 = p.z + (size_t)(r - p.out_row0) * tco;
   const bool flat_out = p.out_tshift >= 31;
+#if PATFFT_NER_EXTLOAD
+  fft::fft_ct_stored<true, LOGT, PATFFT_NER_INV_MAXR, true, 0, NTH>(
+      ibuf, p.tw, tid, fft::SwzC<LOGT>(), NerZStore{z0, flat_out, zstride, p.out_tshift, p.out_tmask});
+#else
   fft::fft_ct_stored<true, LOGT, PATFFT_NER_INV_MAXR, true, 0, NTH>(
       ibuf, p.tw, tid, fft::SwzC<LOGT>(), [&](int i, int, float2 v) {
         z0[flat_out ? (size_t)i : (i >> p.out_tshift) * zstride + (i & p.out_tmask)] = v;
       });
+#endif
 }
 
 }  // namespace
