@@ -29,6 +29,25 @@ import time
 
 import numpy as np
 
+# The driver parses stdout as one JSON line: libraries that print at init
+# (NCCL's version banner, cuFFT/driver notes) are sent to stderr by pointing
+# fd 1 there for the whole run; emit() writes the result line to the real stdout.
+_STDOUT_FD = None
+
+
+def _quiet_stdout():
+    global _STDOUT_FD
+    if _STDOUT_FD is None:
+        sys.stdout.flush()
+        _STDOUT_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    text = json.dumps(line) + "\n"
+    sys.stdout.flush()
+    os.write(_STDOUT_FD if _STDOUT_FD is not None else 1, text.encode())
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -206,7 +225,7 @@ def run_reference_arm(args):
                          "sample": _sample_desc(args.config, frac)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
@@ -312,7 +331,7 @@ def run_sharded_arm(args):
             "gpu_launches": 7 * args.steps, "gpu_launches_note": "per rank per step: spread, colfft, rowfft, ner, "
             "inv_col, inv_c2r (+1 flush outside the events); 2 NCCL all-to-alls",
         }
-        print(json.dumps(line))
+        emit(line)
     dist.destroy_process_group()
     return 0
 
@@ -530,7 +549,7 @@ def run_gpu_arm(args):
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": own_launches * args.steps * nframes,
         "gpu_launches_note": f"own sm_100a kernels per step: {own_launches}; library (cuFFT) kernels per step: {lib_launches}",
     }
-    print(json.dumps(line))
+    emit(line)
     if dist is not None:
         dist.destroy_process_group()
     return 0
@@ -545,6 +564,7 @@ def _traffic_from_profiles(cfg, kernel):
 
 
 def main():
+    _quiet_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
