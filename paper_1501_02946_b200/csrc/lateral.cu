@@ -120,15 +120,19 @@ __global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kerne
     return;
   }
   float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * T;
-  for (int i = tid; i < p.ny * P; i += nth) {
-    const int k = i >> PLOG, q = i & (P - 1);
-    const int t = t0 + 2 * q;
-    if (t >= p.t_end) continue;
+  // each thread keeps one packed time pair q (nth is a multiple of P) and walks the bins k
+  const int q = tid & (P - 1);
+  const int t = t0 + 2 * q;
+  if (t >= p.t_end) return;
+  const int kstep = nth >> PLOG;
+  const size_t ostep = (size_t)kstep * T;
+  float2* __restrict__ o = dst + (size_t)(tid >> PLOG) * T + t;
+  for (int k = tid >> PLOG; k < p.ny; k += kstep, o += ostep) {
     const float2 zk = zat(k, q);
     const float2 zm = fft::conjf2(zat((n - k) & (n - 1), q));
     const float2 d = fft::csub(zk, zm);
-    const float4 o = make_float4(0.5f * (zk.x + zm.x), 0.5f * (zk.y + zm.y), 0.5f * d.y, -0.5f * d.x);
-    *reinterpret_cast<float4*>(dst + (size_t)k * T + t) = o;
+    *reinterpret_cast<float4*>(o) =
+        make_float4(0.5f * (zk.x + zm.x), 0.5f * (zk.y + zm.y), 0.5f * d.y, -0.5f * d.x);
   }
 }
 
@@ -187,10 +191,14 @@ __global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kerne
     return;
   }
   const bool nyq1 = (j1 == p.N1 / 2);
-  for (int i = tid; i < N0 * P; i += nth) {
-    const int j0w = i >> PLOG, q = i & (P - 1);
-    const int t = t0 + q;
-    if (t >= p.t_end) continue;
+  // each thread keeps one time sample q (nth is a multiple of P) and walks the rows j0w
+  const int q = tid & (P - 1);
+  const int t = t0 + q;
+  if (t >= p.t_end) return;
+  const int kstep = nth >> PLOG;
+  const size_t gstep = (size_t)kstep * p.ny * T;
+  float2* __restrict__ gp = p.gh + ((size_t)(tid >> PLOG) * p.ny + j1) * T + t;
+  for (int j0w = tid >> PLOG; j0w < N0; j0w += kstep, gp += gstep) {
     const int a = (N0 > 1) ? (j0w < N0 / 2 ? j0w : j0w - N0) : 0;
     const bool nyq0 = (N0 > 1) && (a == -(N0 / 2));
     float2 v;
@@ -203,7 +211,7 @@ __global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kerne
     } else {
       v = zat(a & mask, q);
     }
-    p.gh[((size_t)j0w * p.ny + j1) * T + t] = fft::cscale(v, p.dp0[j0w] * dp1);
+    *gp = fft::cscale(v, __ldg(&p.dp0[j0w]) * dp1);
   }
 }
 
