@@ -367,6 +367,9 @@ __device__ __forceinline__ void last_pass_inplace(float2* __restrict__ buf, cons
 #ifndef PATFFT_NER_DCT_DIV
 #define PATFFT_NER_DCT_DIV 8  // threads per CTA = T / 8 (measured: 4 and 16 slower)
 #endif
+#ifndef PATFFT_NER_POLY_SCALAR
+#define PATFFT_NER_POLY_SCALAR 1  // DCT kernel: tap polynomials as scalar FFMAs on constant-bank coefficients
+#endif
 #ifndef PATFFT_NER_EXTLOAD
 #define PATFFT_NER_EXTLOAD 1  // first pass: running pointers into gh and pre[] (NerExtLoad)
 #endif
@@ -524,12 +527,26 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
     for (int j = 0; j < K; ++j) {
       constexpr int DE = D % 2 ? D - 1 : D;
       constexpr int DO = D % 2 ? D : D - 1;
+#if PATFFT_NER_POLY_SCALAR
+      // scalar Horner chains: each FFMA takes its coefficient straight from the
+      // constant bank (the packed form needs the pair in registers: LDC + MOV)
+      float ev = p.poly[j][DE], ov = p.poly[j][DO];
+#pragma unroll
+      for (int s2 = 1; s2 <= DO / 2; ++s2) {
+        ev = fmaf(ev, z2, p.poly[j][DE - 2 * s2]);
+        ov = fmaf(ov, z2, p.poly[j][DO - 2 * s2]);
+      }
+#pragma unroll
+      for (int d = DE - 2 * (DO / 2) - 2; d >= 0; d -= 2) ev = fmaf(ev, z2, p.poly[j][d]);
+      const float2 eo = make_float2(ev, ov);
+#else
       float2 eo = make_float2(p.poly[j][DE], p.poly[j][DO]);
 #pragma unroll
       for (int s2 = 1; s2 <= DO / 2; ++s2)
         eo = fft::f2fma(eo, make_float2(z2, z2), make_float2(p.poly[j][DE - 2 * s2], p.poly[j][DO - 2 * s2]));
 #pragma unroll
       for (int d = DE - 2 * (DO / 2) - 2; d >= 0; d -= 2) eo.x = fmaf(eo.x, z2, p.poly[j][d]);
+#endif
       const float wa = fmaf(z, eo.y, eo.x);
       const float wb = fmaf(-z, eo.y, eo.x);
       const float2 Fa = at(j);
