@@ -328,8 +328,9 @@ def run_sharded_arm(args):
             "clocks": clk,
             "e2e": {"value": vox / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * host_slice.size * world,
                     "d2h_bytes_per_step": 8 * int(np.prod(pin_out.shape)) * world, "ms_per_step": 1e3 * e2e_s},
-            "gpu_launches": 7 * args.steps, "gpu_launches_note": "per rank per step: spread, colfft, rowfft, ner, "
-            "inv_col, inv_c2r (+1 flush outside the events); 2 NCCL all-to-alls",
+            "gpu_launches": 7 * args.steps, "gpu_launches_note": "per rank per step: absmax (sample scale of the fp16 "
+            "gridding), spread, colfft, rowfft, ner, inv_col, inv_c2r (+1 flush outside the events); 2 NCCL "
+            "all-to-alls",
         }
         emit(line)
     dist.destroy_process_group()

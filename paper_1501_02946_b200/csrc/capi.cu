@@ -1565,6 +1565,7 @@ int patfft_nedner_stage_bytes(const patfft_nedner_plan* P, double* bytes, int n)
 int patfft_nedner_launches_per_execute(const patfft_nedner_plan* P, int* own, int* library) {
   if (!P) return fail(PATFFT_ERR_PARAMETER, "null plan");
   int o = 4;  // spread, colfft, rowfft, ner
+  if (P->tc_ntiles > 0 && P->tc_f16) o += 1;  // absmax_kernel (sample scale of the fp16 gridding)
   int lib = 0;
   if (P->custom_inverse) o += (P->N0u > 1 ? 2 : 1);
   else lib += 1;  // cuFFT C2R (may be several kernels)
