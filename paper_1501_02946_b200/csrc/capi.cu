@@ -304,18 +304,33 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // An explicit alpha/beta fixes the window in frequency units; the GPU grids
   // are powers of two, so when its effective oversampling differs from the
   // reference's (even 11-smooth length) the same (alpha, beta, K) can cover a
-  // different part of the window.  Probe the accuracy at the GPU sizes and
-  // refuse loudly instead of returning a silently different answer.
+  // different part of the window.  Probe the accuracy at the GPU sizes.  If it
+  // is lost there but the window is accurate at the reference's own length,
+  // the reference's result is the exact transform to within that accuracy, so
+  // the GPU computes the same transform with the window resolved for its own
+  // oversampling (same K, alpha/beta as nufft.py:139-149 would pick) -- checked
+  // as accurate too.  Otherwise refuse loudly instead of returning a silently
+  // different answer.
   if ((mode == 0 || mode == 3) && (!std::isnan(d->spec_alpha) || !std::isnan(d->spec_beta))) {
-    struct Probe { const Window* w; int n, n_over, n_over_ref; };
+    struct Probe { Window* w; int n, n_over, n_over_ref; };
     std::vector<Probe> probes;
     for (int a = 0; a < d->n_lat; ++a)
       probes.push_back({&P->win_lat[a], d->out_dims[a], n_over_lat[a], even_fast_len(c * d->out_dims[a])});
     if (mode != 3) probes.push_back({&P->win_t, n_ext, P->n_over_t, even_fast_len(c * n_ext)});
+    constexpr double kWinTol = 1e-6;
     for (const Probe& pr : probes) {
       if (pr.n_over == pr.n_over_ref || pr.n_over > 8192) continue;
-      const double e = window_relative_error(*pr.w, pr.n, pr.n_over);
-      if (!(e <= 1e-6)) {
+      double e = window_relative_error(*pr.w, pr.n, pr.n_over);
+      Window wref, wsub;
+      if (!(e <= kWinTol) && pr.n_over_ref <= 8192 &&
+          resolve_window(c, K, d->spec_alpha, d->spec_beta, double(pr.n_over_ref) / pr.n, &wref, &err) &&
+          window_relative_error(wref, pr.n, pr.n_over_ref) <= kWinTol &&
+          resolve_window(c, K, NAN, NAN, double(pr.n_over) / pr.n, &wsub, &err) &&
+          window_relative_error(wsub, pr.n, pr.n_over) <= kWinTol) {
+        *pr.w = wsub;
+        e = 0.0;
+      }
+      if (!(e <= kWinTol)) {
         char buf[320];
         std::snprintf(buf, sizeof buf,
                       "window (c=%g, K=%d, alpha=%g, beta=%g) loses accuracy at the GPU's power-of-two oversampled "
