@@ -457,12 +457,27 @@ def run_gpu_arm(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         host_cvt = os.environ.get("PATFFT_HOST_CONVERT", "1") != "0"
-        wb = 4 if host_cvt else 8  # bytes per value that cross PCIe
-        e2e = {"value": vox * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": wb * nsamp,
-               "d2h_bytes_per_step": wb * nout, "ms_per_step": 1e3 * e2e_s,
+        if host_cvt:
+            # bytes that cross PCIe, as the plan splits them (capi.cu execute_host_staged): with a
+            # pinned caller buffer >= 4 MiB, sensor rows [0, direct_in * M) go as float64 by DMA
+            # and the rest as float32; voxels [0, direct_out * n) likewise on the way back
+            def _frac(name, default):
+                v = os.environ.get(name, os.environ.get("PATFFT_HOST_DIRECT", default))
+                return min(1.0, max(0.0, float(v)))
+            m_rows, t_len = rec.samples.shape
+            md = int(_frac("PATFFT_HOST_DIRECT_IN", "0.25") * m_rows) if 8 * nsamp >= (4 << 20) else 0
+            od = int(_frac("PATFFT_HOST_DIRECT_OUT", "0") * nout) // 256 * 256 if 8 * nout >= (4 << 20) else 0
+            h2d_b = 8 * md * t_len + 4 * (nsamp - md * t_len)
+            d2h_b = 8 * od + 4 * (nout - od)
+        else:
+            h2d_b, d2h_b = 8 * nsamp, 8 * nout
+        e2e = {"value": vox * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d_b,
+               "d2h_bytes_per_step": d2h_b, "ms_per_step": 1e3 * e2e_s,
                "path": ("patfft_nedner_execute (C ABI): f64 host samples narrowed to f32 by the host cores into pinned "
-                        "staging, uploaded in blocks overlapped with the narrowing and with the spread + lateral FFTs "
-                        "of earlier time chunks; f32 volume downloaded in blocks widened into the f64 host buffer"
+                        "staging (the caller buffer is pinned: a direct_in share of the sensor rows crosses as f64 by "
+                        "DMA and is narrowed on the device), uploaded in blocks overlapped with the narrowing and with "
+                        "the spread + lateral FFTs of earlier time chunks; f32 volume downloaded in blocks widened into "
+                        "the f64 host buffer"
                         if host_cvt else
                         "patfft_nedner_execute (C ABI): pinned f64 host -> device (time chunks, H2D overlapped with "
                         "spread + lateral FFTs) -> pinned f64 host")}

@@ -59,6 +59,15 @@ using fft::TileAddr;
 #define PATFFT_LB_INV_MINB256 5  // inverse kernels with <= 256 threads: 5 CTAs/SM (48 regs); measured 4 / 6 slower
 #endif
 
+// Grid order of the tiled lateral kernels: 1 = time tiles fastest (CTAs
+// launched together read neighbouring time segments of the same rows, i.e.
+// the same DRAM pages), 0 = rows / columns fastest.
+#ifndef PATFFT_LAT_TFAST
+#define PATFFT_LAT_TFAST 1
+#endif
+__device__ __forceinline__ int lat_line() { return PATFFT_LAT_TFAST ? blockIdx.y : blockIdx.x; }
+__device__ __forceinline__ int lat_ttile() { return PATFFT_LAT_TFAST ? blockIdx.x : blockIdx.y; }
+
 constexpr int nth_for(int L, int PLOG) {
   return ((L >= 4 ? (1 << (L - 4)) : 1) << PLOG) < 64 ? 64
          : (((L >= 4 ? (1 << (L - 4)) : 1) << PLOG) > 512 ? 512 : ((L >= 4 ? (1 << (L - 4)) : 1) << PLOG));
@@ -71,8 +80,8 @@ template <int PLOG, int LC>
 __global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
-  const int u0 = blockIdx.x;
-  const int t0 = p.t_begin + blockIdx.y * 2 * P;
+  const int u0 = lat_line();
+  const int t0 = p.t_begin + lat_ttile() * 2 * P;
   const int tid = threadIdx.x;
   const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.T, n = p.ncols;
@@ -140,8 +149,8 @@ template <int PLOG, int LC>
 __global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
-  const int j1 = blockIdx.x;
-  const int t0 = p.t_begin + blockIdx.y * P;
+  const int j1 = lat_line();
+  const int t0 = p.t_begin + lat_ttile() * P;
   const int tid = threadIdx.x;
   const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.T, nr = p.nrows;
@@ -219,8 +228,8 @@ template <int PLOG, int LC>
 __global__ void __launch_bounds__(inv_lb_threads(PLOG, LC), inv_lb_minb(PLOG, LC)) inv_col_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
-  const int j1 = blockIdx.x;
-  const int t0 = blockIdx.y * P;
+  const int j1 = lat_line();
+  const int t0 = lat_ttile() * P;
   const int tid = threadIdx.x;
   const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.Tu, n = p.N0u;
@@ -260,8 +269,8 @@ template <int PLOG, int LC>
 __global__ void __launch_bounds__(inv_lb_threads(PLOG, LC), inv_lb_minb(PLOG, LC)) inv_c2r_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
   constexpr int P = 1 << PLOG;
-  const int n0 = blockIdx.x;
-  const int t0 = blockIdx.y * 2 * P;
+  const int n0 = lat_line();
+  const int t0 = lat_ttile() * 2 * P;
   const int tid = threadIdx.x;
   const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.Tu, n = p.N1u, half = n / 2;
@@ -352,7 +361,8 @@ int threads_for(int len, int plog) {
     const int plog = plog_for(len);                                                                    \
     const size_t smem = ((size_t)len << plog) * sizeof(float2);                                        \
     const int thr = threads_for(len, plog);                                                            \
-    dim3 grid(grid_xy.x, (unsigned)((grid_xy.y + (tpack << plog) - 1) / (tpack << plog)));              \
+    const unsigned ntt = (unsigned)((grid_xy.y + (tpack << plog) - 1) / (tpack << plog));               \
+    const dim3 grid = PATFFT_LAT_TFAST ? dim3(ntt, grid_xy.x) : dim3(grid_xy.x, ntt);                  \
     cudaError_t err = cudaSuccess;                                                                     \
     auto run = [&](auto k) {                                                                           \
       err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
