@@ -454,6 +454,9 @@ __device__ __forceinline__ void store_items(const float2 (&e)[1 << R], int base,
   }
 }
 
+// float2 slots of the DCT kernel's D' array: bins [-16, 2T + 16) with one pad per 16
+__host__ __device__ constexpr int ner_dct_dwords(int T) { return (2 * T + 32) + (2 * T + 32) / 16; }
+
 template <int K2, int D, int LOGT>
 __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner_dct_kernel(const NerParams p) {
   constexpr int T = 1 << LOGT;
@@ -473,8 +476,11 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
     return __ldcs(flat_in ? &g[t] : &g[(t >> p.in_tshift) * gstride + (t & p.in_tmask)]);
   };
   // natural-order D' array (after the transform): one pad slot per 16, which
-  // keeps the stride-~4 tap gathers of neighbouring threads conflict-free
-  auto dpad = [](int q) { return q + (q >> 4); };
+  // keeps the stride-~4 tap gathers of neighbouring threads conflict-free.
+  // Bins q in [-16, 2T + 16): the folded bins D'[-1-q] = D'[q] and
+  // D'[4T-1-q] = D'[q] that taps at the band ends reach are stored too, so
+  // the gathers never fold (no per-tap branch).
+  auto dpad = [](int q) { return (q + 16) + ((q + 16) >> 4); };
 
   // 1. DCT-III of the windowed half extension via a 2T-point inverse FFT;
   // the last pass stores D'[q] in natural order (Makhoul output permutation
@@ -493,7 +499,10 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   {
     constexpr int LH = fft::LastPassLogh<L, PATFFT_NER_DCT_MAXR, true>::value;
     last_pass_inplace<L - LH, true, L, LH, NTH>(sbuf, p.tw, tid, ad, [&](int n, float2 v) {
-      sbuf[dpad(n < T ? 2 * n : 4 * T - 1 - 2 * n)] = v;
+      const int q = n < T ? 2 * n : 4 * T - 1 - 2 * n;
+      sbuf[dpad(q)] = v;
+      if (q < K) sbuf[dpad(-1 - q)] = v;
+      if (q >= N2 - K) sbuf[dpad(4 * T - 1 - q)] = v;
     });
   }
   __syncthreads();
@@ -514,14 +523,8 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
     // taps span at most two 16-blocks: tap t sits at base0 + t or base1 + t.
     // Targets at the ends of the band fold by D'[-1-q] = D'[q] = D'[4T-1-q].
     const int kb = k0 - K + 1;
-    const bool edge = kb < 0 || k0 + K >= N2;
-    const int base0 = dpad(kb), tb = 16 - (kb & 15);
-    auto at = [&](int t) {
-      if (!edge) return sbuf[(t < tb ? base0 : base0 + 1) + t];
-      int k = (kb + t) & (4 * T - 1);
-      k = k >= N2 ? (~k) & (4 * T - 1) : k;
-      return sbuf[dpad(k)];
-    };
+    const int base0 = dpad(kb), tb = 16 - (kb & 15);  // kb >= -K, kb + K2 <= 2T + K
+    auto at = [&](int t) { return sbuf[(t < tb ? base0 : base0 + 1) + t]; };
     float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -561,7 +564,7 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   // swizzled) behind the D' array: no per-target registers, and the target
   // loop is not unrolled (five inlined copies of the interpolation made the
   // kernel's code larger than the instruction cache)
-  float2* __restrict__ obuf = sbuf + (2 * T + 2 * T / 16);
+  float2* __restrict__ obuf = sbuf + ner_dct_dwords(T);
   const fft::SwzC<LOGT> iad;
 #else
   float2 valsP[kPairs], valsM[kPairs];
@@ -671,7 +674,7 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
   if (ct_ok && dct && p.pre) {
     // DCT form: 2T-point transform, half the shared memory
     threads = std::max(64, std::min(512, p.T / PATFFT_NER_DCT_DIV));
-    const size_t smem2 = (size_t)(2 * p.T + 2 * p.T / 16 + (PATFFT_NER_DIRECT ? p.T : 0)) * sizeof(float2);
+    const size_t smem2 = (size_t)(ner_dct_dwords(p.T) + (PATFFT_NER_DIRECT ? p.T : 0)) * sizeof(float2);
     auto go2 = [&](auto kern) {
       err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
       if (err != cudaSuccess) return;
