@@ -677,6 +677,16 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     if (fit_ner_poly(wt, 12, &q) > 1e-6)
       return fail(PATFFT_ERR_UNSUPPORTED, "window transform not representable by the tap polynomials");
   }
+  q.poly7 = 0;
+  if (P->poly_degree == 8) {
+    // degree 7 is below fp32 rounding for the default window (1.5e-8): one FFMA less per
+    // tap pair in the DCT kernel; the degree-8 kernels read a zero top coefficient
+    float p7[kMaxTaps / 2][kMaxPolyDegree + 1];
+    if (fit_ner_poly_into(wt, 7, p7) <= 4e-8) {
+      std::memcpy(q.poly, p7, sizeof p7);
+      q.poly7 = 1;
+    }
+  }
 
   // ---- device buffers -----------------------------------------------------
   int rc;

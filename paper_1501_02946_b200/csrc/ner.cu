@@ -681,6 +681,15 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
       kern<<<rows, threads, smem2, s>>>(p);
       err = cudaGetLastError();
     };
+    if (p.poly7) {
+      switch (p.log_n_over - 2) {
+        case 7: go2(ner_dct_kernel<12, 7, 7>); return err;
+        case 8: go2(ner_dct_kernel<12, 7, 8>); return err;
+        case 9: go2(ner_dct_kernel<12, 7, 9>); return err;
+        case 10: go2(ner_dct_kernel<12, 7, 10>); return err;
+        case 11: go2(ner_dct_kernel<12, 7, 11>); return err;
+      }
+    }
     switch (p.log_n_over - 2) {
       case 7: go2(ner_dct_kernel<12, 8, 7>); return err;
       case 8: go2(ner_dct_kernel<12, 8, 8>); return err;

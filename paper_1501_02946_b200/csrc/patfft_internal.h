@@ -103,6 +103,7 @@ struct NerParams {
   double c_eff;        // n_over / (2T)
   float scale;         // 1/(N0*N1*T): scipy ifftn normalisation * up^d
   float poly[kMaxTaps / 2][kMaxPolyDegree + 1];  // psihat((z + K-1/2-j)/c)/psihat(0), z in [-1/2,1/2]
+  int poly7;           // 1: poly has degree 7 (coefficient 8 zero): ner_dct_kernel<.., 7, ..>
 };
 
 // Kernel launchers

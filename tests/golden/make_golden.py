@@ -37,7 +37,14 @@ def _record(pos, w, samples, dt, c, dx, nl):
                                sound_speed=c, dx=dx, n_lateral=nl)
 
 
+ONLY = set(sys.argv[1:])  # optional fixture names: regenerate just those
+
+
 def _save(name, **arrays):
+    if ONLY and name not in ONLY:
+        return
+    if "samples" in arrays:  # a fixture whose data never reaches a sensor tests only zero -> zero
+        assert np.abs(arrays["samples"]).max() > 0, f"{name}: all-zero samples"
     path = os.path.join(HERE, f"{name}.npz")
     np.savez_compressed(path, **arrays)
     print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
@@ -90,7 +97,8 @@ def main():
     recon_case("recon_3d_spec_c25", synth.make_3d(20, 16, 32, 20e-9, "uniform", 2),
                spec={"c": 2.5, "K": 6, "alpha": 12.0, "beta": 2.3})
     # 10. upsample 3 (non-power-of-two depth and lateral inverse sizes)
-    recon_case("recon_3d_up3", synth.make_3d(21, 8, 16, 20e-9, "jittered", 1), upsample=3)
+    # (dt = 100 ns: the 16 samples reach the ball; at 20 ns every trace was zero)
+    recon_case("recon_3d_up3", synth.make_3d(21, 8, 16, 100e-9, "jittered", 1), upsample=3)
     # 11. every sensor exactly on the aperture corner / edges (wrap-around taps on both axes)
     rng = np.random.default_rng(22)
     n = 16
@@ -99,9 +107,10 @@ def main():
                            np.array([[-half, -half], [half, half], [-half, half], [half, -half],
                                      [0.0, half], [half, 0.0], [-half, 0.0], [0.0, -half]])])
     balls = [(0.2e-3, 0.1e-3, 2.0e-3, 0.6e-3, 1.0)]
-    samples = synth.ball_traces(edge, 32, 20e-9, synth.SOUND_SPEED, balls)
+    # (dt = 60 ns: the 32 samples reach the ball; at 20 ns every trace was zero)
+    samples = synth.ball_traces(edge, 32, 60e-9, synth.SOUND_SPEED, balls)
     w = np.full(edge.shape[0], (n * synth.PITCH) ** 2 / edge.shape[0])
-    recon_case("recon_3d_edges16", synth.SyntheticRecord(edge, w, samples, 20e-9, synth.SOUND_SPEED, synth.PITCH,
+    recon_case("recon_3d_edges16", synth.SyntheticRecord(edge, w, samples, 60e-9, synth.SOUND_SPEED, synth.PITCH,
                                                          (n, n)))
 
     # 12. complete grids: reconstruct_equispaced and reconstruct_interp_fft
