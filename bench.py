@@ -473,6 +473,7 @@ def run_gpu_arm(args):
             h2d_b, d2h_b = 8 * nsamp, 8 * nout
         e2e = {"value": vox * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d_b,
                "d2h_bytes_per_step": d2h_b, "ms_per_step": 1e3 * e2e_s,
+               "median_ms": 1e3 * float(np.median(et)), "max_ms": 1e3 * float(np.max(et)),
                "path": ("patfft_nedner_execute (C ABI): f64 host samples narrowed to f32 by the host cores into pinned "
                         "staging (the caller buffer is pinned: a direct_in share of the sensor rows crosses as f64 by "
                         "DMA and is narrowed on the device), uploaded in blocks overlapped with the narrowing and with "

@@ -416,8 +416,8 @@ __device__ __forceinline__ void load_items(float2 (&e)[1 << R], int nat0, int, c
     const float2* gb = ld.g + nat0;
 #pragma unroll
     for (int k = 0; k < (1 << R); ++k) {
-      const float2 v = k < KH ? ((k == 0 && nat0 == 0) ? make_float2(0.f, 0.f) : __ldcs(ga - k * S))
-                              : __ldcs(gb + (k - KH) * S);
+      const float2 v = k < KH ? ((k == 0 && nat0 == 0) ? make_float2(0.f, 0.f) : fft::ld_stream(ga - k * S))
+                              : fft::ld_stream(gb + (k - KH) * S);
       e[fft::brev_c(k, R)] = fft::cmul(v, __ldg(pr + k * S));
     }
   } else {
