@@ -291,7 +291,14 @@ __global__ void __launch_bounds__(inv_lb_threads(PLOG, LC), inv_lb_minb(PLOG, LC
       const bool lo = r <= half;
       const int k = lo ? r : n - r;
       // unconditional (clamped) load so the compiler issues all of an item's loads back to back
+#if PATFFT_INV_L2PF
+      float4 v;
+      asm volatile("ld.global.nc.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                   : "l"(reinterpret_cast<const float4*>(z + (size_t)k * T + min(t, T - 2))));
+#else
       float4 v = __ldg(reinterpret_cast<const float4*>(z + (size_t)k * T + min(t, T - 2)));
+#endif
       if (k == 0 || k == half) {  // C2R semantics: self-conjugate bins are real
         v.y = 0.f;
         v.w = 0.f;
