@@ -521,6 +521,9 @@ __device__ __forceinline__ void c16_next(Cursor16& u, const Item16* ring) {
 #ifndef PATFFT_TC16_NOBUILD
 #define PATFFT_TC16_NOBUILD 0
 #endif
+#ifndef PATFFT_TC16_BUILD_WARP0
+#define PATFFT_TC16_BUILD_WARP0 2  // first warp of the B build (0: all warps, tid < N; 2: spread 0.471 -> 0.461 ms; 1: 0.497, 3: 0.462)
+#endif
 #ifndef PATFFT_TC16_NOMMA
 #define PATFFT_TC16_NOMMA 0
 #endif
@@ -737,7 +740,27 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
     mbar_wait_tc(&ld_bar[sb], (g >> 1) & 1);                      // A + samples of stage g landed
     uint8_t* bo = b_ops + sb * B_SLOT;
     const float* sr = s_ring + sb * (S_SLOT / 4);
+#if PATFFT_TC16_BUILD_WARP0
+    // B built by warps PATFFT_TC16_BUILD_WARP0.. only: warp 0 (MMA issue, offset fetches,
+    // item claims) and warp 1 (bulk copies) reach the stage barrier without the build's latency
+    if (warp >= PATFFT_TC16_BUILD_WARP0 && !PATFFT_TC16_NOBUILD) {
+      constexpr int FT = 32 * PATFFT_TC16_BUILD_WARP0;
+#pragma unroll 1
+      for (int u = tid - FT; u < 2 * N; u += kThreadsTC - FT) {
+        const int n = u % N, kb = u / N;
+        float w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = sr[(8 * kb + j) * N + n];
+        uint4 bh, bl;
+        split_f16x8_scaled(w, s_scale, bh, bl);
+        *reinterpret_cast<uint4*>(bo + kb * B_LBO + n * 16) = bh;
+        *reinterpret_cast<uint4*>(bo + B_HALF + kb * B_LBO + n * 16) = bl;
+      }
+    }
+    if (false) {
+#else
     if (tid < N && !PATFFT_TC16_NOBUILD) {
+#endif
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int n = tq + h * NH;
