@@ -11,9 +11,16 @@ inside the timed region).  ``--impl reference`` times the CPU oracle (the
 restated reference algorithm, float64 numpy/scipy) on a bounded sample of
 the same workload.
 
-For N > 1 (torchrun) every rank reconstructs its own record (independent
-volumes, "replicas"; no collective on the data path) and ``value`` is the
-total voxels of all ranks over the max per-rank device time.
+For N > 1 one record is reconstructed by all N ranks together (strong
+scaling, paper_1501_02946_b200/parallel.py): each rank spreads and
+lateral-FFTs its own time slice, an NCCL all-to-all hands every rank its
+lateral-frequency rows, each rank runs the fused NER on its rows, and a
+second all-to-all returns depth slices for the lateral inverse.  ``value`` is
+the record's voxels over the max per-rank device time.  Launched by the
+driver under torchrun (RANK / WORLD_SIZE / LOCAL_RANK from the environment);
+``python bench.py --gpus N`` without a launcher re-executes itself under
+``torch.distributed.run`` with N local ranks.  cfg5 (independent frames)
+runs as replicas: every rank reconstructs its own 64 frames.
 """
 
 from __future__ import annotations
@@ -128,7 +135,7 @@ def make_workload(name, rank=0):
     from paper_1501_02946_b200 import synth
 
     if name == "cfg5":
-        frames = list(synth.make_frames(seed=5 + 1000 * rank, frames=8))
+        frames = list(synth.make_frames(seed=5 + 1000 * rank, frames=64))
         return frames
     seed = {"cfg1": 1, "cfg2": 2, "cfg3": 3, "cfg4": 4}[name] + 1000 * rank
     return [synth.CONFIGS[name](seed)]
@@ -200,31 +207,109 @@ def cpu_sample_seconds(rec, frac):
     return full, measured
 
 
+def _reference_module():
+    """The unmodified reference package, installed once into baseline/_ref with
+    ``python -m pip install --no-index --no-build-isolation --no-deps --target
+    baseline/_ref <copy of /root/reference/pkg>``.  Pure
+    Python, so the install travels to the GPU box with the repo snapshot."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "patfft")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    sys.dont_write_bytecode = True
+    try:
+        import patfft.recon as R
+    except Exception:
+        return None
+    return R
+
+
 def run_reference_arm(args):
+    """CPU reference on this host's cores, on the GPU arm's config and metric.
+
+    With ``baseline/_ref`` installed: the reference's own public call
+    ``patfft.recon.reconstruct_nedner`` (recon.py:358-379) on the full record,
+    repeated until ``--steps`` runs are done or the next run would exceed the
+    arm's time budget (``--ref-budget``, default 240 s; one cfg4 run takes
+    ~100 s), so the line's ``steps`` / ``ms_per_step`` are what actually ran.
+    cfg5 times whole frames and scales to the 64-frame step.  The oracle
+    port's 1/16-sample extrapolation is reported beside it.  Without the
+    install, the oracle port's sample is the value (``kind`` "port").
+    """
     rank, world, _ = _env_rank()
     if rank != 0:
         return 0
     os.environ.setdefault("PAT_THREADS", str(os.cpu_count() or 1))
+    cores = int(os.environ["PAT_THREADS"])
     recs = make_workload(args.config)
     rec = recs[0]
-    vox = _voxels(rec)
+    n_frames = len(recs)
+    vox = _voxels(rec) * n_frames
     frac = args.cpu_frac or 1.0 / 16
-    vals = []
-    for i in range(args.warmup + args.steps):
+    R = _reference_module()
+    extra = {}
+    if R is not None:
+        budget = args.ref_budget
+        times = []
+        t_start = time.perf_counter()
+        k = 0
+        while True:
+            r = recs[k % n_frames]
+            rr = R.SensorRecord(positions=r.positions, weights=r.weights, samples=r.samples, dt=r.dt,
+                                sound_speed=r.sound_speed, dx=r.dx, n_lateral=r.n_lateral)
+            t0 = time.perf_counter()
+            R.reconstruct_nedner(rr)
+            times.append(time.perf_counter() - t0)
+            k += 1
+            done = len(times) >= max(1, args.steps) * (n_frames if n_frames > 1 else 1)
+            if n_frames > 1:
+                done = done or len(times) >= 2 and time.perf_counter() - t_start + times[-1] > budget
+            else:
+                done = done or time.perf_counter() - t_start + times[-1] > budget
+            if done:
+                break
+        per_rec = float(np.mean(times))
+        step_s = per_rec * n_frames
+        value = vox / step_s
+        steps = max(1, len(times) // n_frames) if n_frames > 1 else len(times)
+        kind = "reference"
+        sample = (f"{args.config}: the reference package itself (baseline/_ref, patfft.recon.reconstruct_nedner, "
+                  f"float64 numpy/scipy, PAT_THREADS={cores} for its FFTs, the rest single-threaded as written), "
+                  f"{len(times)} full {'frame' if n_frames > 1 else 'reconstruction'}"
+                  f"{'s' if len(times) != 1 else ''} of {per_rec:.1f} s each"
+                  + (f", scaled to the {n_frames}-frame step" if n_frames > 1 else ""))
+        extra["reference_runs_s"] = times
+        extra["requested"] = {"steps": args.steps, "warmup": args.warmup}
+        if len(times) < args.steps * (n_frames if n_frames > 1 else 1):
+            extra["deviation"] = (f"ran {len(times)} full reference {'frames' if n_frames > 1 else 'reconstructions'} "
+                                  f"instead of {args.steps} steps: each takes {per_rec:.0f} s and the arm's budget is "
+                                  f"{budget:.0f} s; no warm-up (nothing to warm in numpy/scipy)")
         full, meas = cpu_sample_seconds(rec, frac)
-        if i >= args.warmup:
-            vals.append(vox / full)
-    value = statistics.median(vals)
-    cores = int(os.environ["PAT_THREADS"])
+        extra["port_sample_extrapolation"] = {"value": _voxels(rec) / full, "unit": UNIT,
+                                              "sample": _sample_desc(args.config, frac), "measured_s": meas,
+                                              "extrapolated_full_s": full}
+    else:
+        vals = []
+        for i in range(args.warmup + args.steps):
+            full, meas = cpu_sample_seconds(rec, frac)
+            if i >= args.warmup:
+                vals.append(_voxels(rec) / full)
+        value = statistics.median(vals)
+        step_s = vox / value
+        steps = args.steps
+        kind = "port"
+        sample = _sample_desc(args.config, frac)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * vox / value,
+        "steps": steps, "warmup": 0 if kind == "reference" else args.warmup, "ms_per_step": 1e3 * step_s,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": _config_json(args, rec),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": _sample_desc(args.config, frac)},
+        "data": "synthetic (seeded, BASELINE config shapes)", "config": _config_json(args, rec, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                         "os_cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0))},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    line.update(extra)
     emit(line)
     return 0
 
@@ -239,7 +324,7 @@ def _voxels(rec):
     return int(np.prod(rec.n_lateral)) * rec.samples.shape[1]
 
 
-def _config_json(args, rec):
+def _config_json(args, rec, world=1):
     from paper_1501_02946_b200 import synth
 
     return {"workload": f"{args.config}: {synth.DESCRIPTIONS[args.config]}",
@@ -247,7 +332,8 @@ def _config_json(args, rec):
             "out_shape": list(rec.n_lateral) + [int(rec.samples.shape[1])],
             "window": "Kaiser-Bessel c=2 K=6 (reference default)",
             "l2": "inputs (>=268 MB at cfg4) exceed L2 and a 512 MB scratch write flushes L2 between steps",
-            "parallelism": "replicas" if args.gpus > 1 else "single-gpu"}
+            "parallelism": ("single-gpu" if world == 1 else
+                            f"replicas x{world}" if args.config == "cfg5" else f"sharded x{world}")}
 
 
 # ---------------------------------------------------------------------------
@@ -562,7 +648,7 @@ def run_gpu_arm(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32/c64", "data": "synthetic (seeded, BASELINE config shapes)",
-        "config": _config_json(args, rec), "clocks": clk, "roofline": roof, "stages": stage_report,
+        "config": _config_json(args, rec, world), "clocks": clk, "roofline": roof, "stages": stage_report,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": own_launches * args.steps * nframes,
         "gpu_launches_note": f"own sm_100a kernels per step: {own_launches}; library (cuFFT) kernels per step: {lib_launches}",
     }
@@ -580,7 +666,30 @@ def _traffic_from_profiles(cfg, kernel):
         return None
 
 
+def _spawn_ranks(n):
+    """``--gpus N`` without a launcher: re-run this command under torchrun, N local ranks."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
+    if "WORLD_SIZE" not in os.environ:
+        gi = [a for a in sys.argv[1:] if a.startswith("--gpus")]
+        n = 1
+        if gi:
+            v = gi[0].split("=", 1)[1] if "=" in gi[0] else sys.argv[sys.argv.index(gi[0]) + 1]
+            n = int(v)
+        if n > 1:
+            _spawn_ranks(n)
     _quiet_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -592,6 +701,8 @@ def main():
                     help="fraction of the workload the CPU sample runs (default: 1/4 for the cpu_baseline leg "
                          "(~10-15 s), 1/16 per step for --impl reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=240.0,
+                    help="--impl reference: seconds of full reference runs (at least one run)")
     ap.add_argument("--sharded", action="store_true", help="use the sharded multi-GPU path even at N=1")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -166,8 +166,11 @@ def reconstruct_frames_file(plan, in_path, out_path, frames: slice | None = None
             cur = nxt[0]
             th = threading.Thread(target=fetch, args=(order[i + 1] if i + 1 < len(order) else None,))
             th.start()
-            plan.execute(cur, out=out)
+            _, _, nonfinite = plan.execute_checked(cur, out=out)
             th.join()
+            if nonfinite:  # the ScalarField finiteness rule (recon.py:62-63), per frame
+                raise DataValidationError(f"frame {order[i]}: field values must be finite "
+                                          f"({nonfinite} non-finite voxels)")
             f.write(np.ascontiguousarray(out, dtype="<f8").tobytes(order="C"))
     oh.data_offset = _PREFIX.size + len(js)
     return oh

@@ -507,17 +507,31 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   }
   __syncthreads();
 
-  // 2. targets (as ner_kernel)
+  // 2. targets.  kappa(j, l) = sqrt(j2 + l^2) in float32 pairs: j2 (float64,
+  // recon.py:210-214 summation order) splits into hi + lo floats once per
+  // row, l^2 is exact, and one Newton step on rsqrt gives kappa = y + yl to
+  // ~1e-12 absolute -- the bin k0 and the offset z of c kappa_e - 1/2 =
+  // 4 kappa - 1/2 (c_eff = 2) then follow without float64 arithmetic (the
+  // fp64 DSQRT / FRND / F2F chain was a quarter of the target phase).  The
+  // band test of recon.py:289 (j2 + l^2 <= (T/2)^2 in float64) is a prefix
+  // l <= lmax, decided once per row in float64 exactly as the reference does.
   const int j0w = r / p.N1h;
   const int j1 = r - j0w * p.N1h;
   const double j2 = p.jt0[j0w] + p.jt1[j1];  // recon.py:210-214 summation order
   constexpr double halfT = (double)T / 2.0;
   constexpr double band_r2 = halfT * halfT;
-  auto interp_D = [&](double ke) {
-    const double xi = __dmul_rn(p.c_eff, ke) - 0.5;  // half-bin grid
-    const double k0d = floor(xi);
-    const int k0 = (int)k0d;
-    const float z = (float)(xi - k0d) - 0.5f;
+  int lmax;
+  {
+    const double rem = band_r2 - j2;
+    int c0 = rem > 0.0 ? (int)sqrt(rem) : 0;
+    if (c0 > T / 2) c0 = T / 2;
+    while (c0 < T / 2 && j2 + (double)(c0 + 1) * (c0 + 1) <= band_r2) ++c0;
+    while (c0 > 0 && !(j2 + (double)c0 * c0 <= band_r2)) --c0;
+    lmax = c0;  // targets lh = 1 .. lmax are on the band
+  }
+  const float j2h = (float)j2;
+  const float j2l = (float)(j2 - (double)j2h);
+  auto interp_D = [&](int k0, float z) {
     const float z2 = z * z;
     // taps k0-K+1 .. k0+K of D' (natural order, padded).  Inside the band the
     // taps span at most two 16-blocks: tap t sits at base0 + t or base1 + t.
@@ -530,7 +544,6 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
     for (int j = 0; j < K; ++j) {
       constexpr int DE = D % 2 ? D - 1 : D;
       constexpr int DO = D % 2 ? D : D - 1;
-#if PATFFT_NER_POLY_SCALAR
       // scalar Horner chains: each FFMA takes its coefficient straight from the
       // constant bank (the packed form needs the pair in registers: LDC + MOV)
       float ev = p.poly[j][DE], ov = p.poly[j][DO];
@@ -541,17 +554,8 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
       }
 #pragma unroll
       for (int d = DE - 2 * (DO / 2) - 2; d >= 0; d -= 2) ev = fmaf(ev, z2, p.poly[j][d]);
-      const float2 eo = make_float2(ev, ov);
-#else
-      float2 eo = make_float2(p.poly[j][DE], p.poly[j][DO]);
-#pragma unroll
-      for (int s2 = 1; s2 <= DO / 2; ++s2)
-        eo = fft::f2fma(eo, make_float2(z2, z2), make_float2(p.poly[j][DE - 2 * s2], p.poly[j][DO - 2 * s2]));
-#pragma unroll
-      for (int d = DE - 2 * (DO / 2) - 2; d >= 0; d -= 2) eo.x = fmaf(eo.x, z2, p.poly[j][d]);
-#endif
-      const float wa = fmaf(z, eo.y, eo.x);
-      const float wb = fmaf(-z, eo.y, eo.x);
+      const float wa = fmaf(z, ov, ev);
+      const float wb = fmaf(-z, ov, ev);
       const float2 Fa = at(j);
       const float2 Fb = at(K2 - 1 - j);
       acc = fft::f2fma(Fa, make_float2(wa, wa), fft::f2fma(Fb, make_float2(wb, wb), acc));
@@ -578,21 +582,36 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   for (int it = 0; it < kPairs; ++it) {
     const int lh = tid + it * NTH;
     float2 vp = make_float2(0.f, 0.f), vm = make_float2(0.f, 0.f);
-    if (lh <= T / 2 && lh > 0) {
-      const double lv = __dmul_rn(__dmul_rn((double)lh, 1.0 / (double)T), (double)T);  // fftfreq(T)*T
-      const double r2 = __dadd_rn(j2, __dmul_rn(lv, lv));
-      if (r2 <= band_r2) {
-        const double kap = sqrt(r2);
-        const double ke = 2.0 * kap;
-        const float2 Dv = interp_D(ke);
-        const double red = ke - 2.0 * floor(0.5 * ke + 0.5);
-        const float2 cs = cospi_sinpi((float)red);  // (cos, sin)(pi kappa_e)
-        const float amp = __fdividef(2.f * (float)lv, (float)kap);
-        const float a = 0.5f * amp * p.scale;
-        const float rx = Dv.x * cs.x, ry = Dv.y * cs.x, sx = Dv.x * cs.y, sy = Dv.y * cs.y;
-        vp = make_float2(a * (rx + sy + g0.x), a * (ry - sx + g0.y));  // e^{-i pi ke} D + g0
-        vm = make_float2(a * (rx - sy + g0.x), a * (ry + sx + g0.y));  // e^{+i pi ke} D + g0
+    if (lh <= lmax && lh > 0) {
+      // r2 = lh^2 + j2 as an unevaluated float pair (s, rl): TwoSum
+      const float l2 = (float)(lh * lh);  // exact (lh <= 2^10)
+      const float s = l2 + j2h;
+      const float bb = s - l2;
+      const float rl = ((l2 - (s - bb)) + (j2h - bb)) + j2l;
+      // kappa = sqrt(s + rl) = y + yl (one Newton step from the rsqrt estimate)
+      const float rs = rsqrtf(s);
+      const float y = s * rs;
+      const float yl = (fmaf(-y, y, s) + rl) * (0.5f * rs);
+      // c kappa_e - 1/2 = 4 y - 1/2 + 4 yl; 4 y - 1/2 is exact in float32
+      const float xh = fmaf(4.f, y, -0.5f);
+      float kf = floorf(xh);
+      float z = ((xh - kf) - 0.5f) + 4.f * yl;  // in [-1/2, 1/2) up to the yl correction
+      if (z < -0.5f) {
+        z += 1.f;
+        kf -= 1.f;
+      } else if (z >= 0.5f) {
+        z -= 1.f;
+        kf += 1.f;
       }
+      const float2 Dv = interp_D((int)kf, z);
+      // exp(-+ i pi kappa_e), kappa_e = 2 kappa reduced mod 2: 2 (y - rint(y)) is exact
+      const float red = fmaf(2.f, y - rintf(y), 2.f * yl);
+      const float2 cs = cospi_sinpi(red);  // (cos, sin)(pi kappa_e)
+      const float amp = __fdividef(2.f * (float)lh, y);  // 2 l / kappa (recon.py:290)
+      const float a = 0.5f * amp * p.scale;
+      const float rx = Dv.x * cs.x, ry = Dv.y * cs.x, sx = Dv.x * cs.y, sy = Dv.y * cs.y;
+      vp = make_float2(a * (rx + sy + g0.x), a * (ry - sx + g0.y));  // e^{-i pi ke} D + g0
+      vm = make_float2(a * (rx - sy + g0.x), a * (ry + sx + g0.y));  // e^{+i pi ke} D + g0
     }
 #if PATFFT_NER_DIRECT
     if (lh <= T / 2) {
@@ -665,7 +684,7 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
   };
   // compile-time variant for the default window (2K = 12, degree 8), c_eff = 2,
   // upsample 1 and T = 2^7 .. 2^11
-  const bool ct_ok = K2 == 12 && degree == 8 && p.fused_ifft && p.up == 1 && p.n_over == 4 * p.T &&
+  const bool ct_ok = (K2 == 12 || K2 == 8) && degree == 8 && p.fused_ifft && p.up == 1 && p.n_over == 4 * p.T &&
                      p.Tu == p.T && p.log_n_over >= 9 && p.log_n_over <= 13;
   static const bool dct = [] {
     const char* e = std::getenv("PATFFT_NER_DCT");
@@ -681,24 +700,24 @@ cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
       kern<<<rows, threads, smem2, s>>>(p);
       err = cudaGetLastError();
     };
-    if (p.poly7) {
-      switch (p.log_n_over - 2) {
-        case 7: go2(ner_dct_kernel<12, 7, 7>); return err;
-        case 8: go2(ner_dct_kernel<12, 7, 8>); return err;
-        case 9: go2(ner_dct_kernel<12, 7, 9>); return err;
-        case 10: go2(ner_dct_kernel<12, 7, 10>); return err;
-        case 11: go2(ner_dct_kernel<12, 7, 11>); return err;
-      }
-    }
-    switch (p.log_n_over - 2) {
-      case 7: go2(ner_dct_kernel<12, 8, 7>); return err;
-      case 8: go2(ner_dct_kernel<12, 8, 8>); return err;
-      case 9: go2(ner_dct_kernel<12, 8, 9>); return err;
-      case 10: go2(ner_dct_kernel<12, 8, 10>); return err;
-      case 11: go2(ner_dct_kernel<12, 8, 11>); return err;
-    }
+#define PATFFT_NER_DCT_SWITCH(k2, d)                         \
+  switch (p.log_n_over - 2) {                                 \
+    case 7: go2(ner_dct_kernel<k2, d, 7>); return err;        \
+    case 8: go2(ner_dct_kernel<k2, d, 8>); return err;        \
+    case 9: go2(ner_dct_kernel<k2, d, 9>); return err;        \
+    case 10: go2(ner_dct_kernel<k2, d, 10>); return err;      \
+    case 11: go2(ner_dct_kernel<k2, d, 11>); return err;      \
   }
-  if (ct_ok) {
+    if (K2 == 8) {
+      if (p.poly7) PATFFT_NER_DCT_SWITCH(8, 7)
+      PATFFT_NER_DCT_SWITCH(8, 8)
+    } else {
+      if (p.poly7) PATFFT_NER_DCT_SWITCH(12, 7)
+      PATFFT_NER_DCT_SWITCH(12, 8)
+    }
+#undef PATFFT_NER_DCT_SWITCH
+  }
+  if (ct_ok && K2 == 12) {
     threads = ner_threads(p.n_over);
     switch (p.log_n_over - 2) {
       case 7: go(ner_kernel<12, 8, 7>); return err;

@@ -179,7 +179,7 @@ struct patfft_nedner_plan {
   int n_lat = 2, N0 = 1, N1 = 0, T = 0, up = 1, M = 0;
   int nrows = 1, ncols = 0, N1h = 0;
   int N0u = 1, N1u = 0, N1uh = 0, Tu = 0;
-  int n_over_t = 0, K2 = 12, poly_degree = 8;
+  int n_over_t = 0, K2 = 12, K2t = 12, poly_degree = 8;  // K2: lateral taps, K2t: NER taps
   int R = 4, ngroups = 0, nblk = 0;
   int64_t n_records = 0;
   bool fused_ifft = true;

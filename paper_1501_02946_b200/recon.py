@@ -19,8 +19,8 @@ from __future__ import annotations
 
 import ctypes
 import math
-import sys
 import threading
+import weakref
 from collections import OrderedDict
 from dataclasses import dataclass, field
 
@@ -212,6 +212,18 @@ def _out_dims(n_lateral, out_dims):
     return dims
 
 
+class _Lease:
+    """One hand-out of a pooled output buffer (see ``NedNerPlan._fresh_out``)."""
+
+    __slots__ = ("_buf", "__weakref__")
+
+    def __init__(self, buf: np.ndarray):
+        self._buf = buf
+
+    def __buffer__(self, flags):
+        return memoryview(self._buf)
+
+
 class NedNerPlan:
     """Device plan for one sensor layout (positions, weights, grid, window).
 
@@ -301,22 +313,31 @@ class NedNerPlan:
         return out, resid.value, int(bad.value)
 
     # Output volumes handed to callers are recycled once the caller has dropped
-    # every reference (the array, its views and the ScalarField holding it):
-    # a fresh 0.5 GB numpy array costs more in first-touch page faults than the
-    # reconstruction's whole PCIe transfer.  Only arrays this plan allocated and
-    # nobody else references are reused; anything still referenced is left alone.
+    # every reference to them (the array, any view of it, the ScalarField
+    # holding it): a fresh 0.5 GB numpy array costs more in first-touch page
+    # faults than the reconstruction's whole PCIe transfer.  Each volume handed
+    # out is a numpy array over a per-call ``_Lease`` object that exports the
+    # pooled buffer; numpy keeps that lease alive as the base of the array and
+    # of every view derived from it, and a ``weakref.finalize`` on the lease
+    # returns the buffer to the pool only when the last of them is gone.  No
+    # reference counting heuristics: a result that is still reachable is never
+    # handed out again.
     _OUT_POOL_SIZE = 2
 
     def _fresh_out(self) -> np.ndarray:
-        pool = self.__dict__.setdefault("_out_pool", [])
-        for a in pool:
-            # references: the pool list, the loop variable and getrefcount's argument
-            if sys.getrefcount(a) == 3:
-                return a
-        a = np.empty(self.out_shape, dtype=np.float64)
-        if len(pool) < self._OUT_POOL_SIZE:
-            pool.append(a)
-        return a
+        pool = self.__dict__.setdefault("_out_pool", [])  # [backing array, busy flag]
+        for slot in pool:
+            if not slot[1]:
+                break
+        else:
+            slot = [np.empty(self.out_shape, dtype=np.float64), False]
+            if len(pool) >= self._OUT_POOL_SIZE:
+                return slot[0]  # pool full of live results: an unpooled array
+            pool.append(slot)
+        slot[1] = True
+        lease = _Lease(slot[0])
+        weakref.finalize(lease, slot.__setitem__, 1, False)
+        return np.frombuffer(lease, dtype=np.float64).reshape(self.out_shape)
 
     def execute_device(self, samples_ptr: int, image_ptr: int, stream: int = 0) -> None:
         """Device float32 pointers; enqueued on ``stream`` (0 = plan stream)."""

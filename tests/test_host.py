@@ -131,3 +131,40 @@ def test_desc_struct_layout_matches_header():
     assert d.spec_K.offset == 48
     assert d.spec_alpha.offset == 56
     assert ctypes.sizeof(d) == 72
+
+
+def test_output_pool_never_hands_out_a_reachable_volume():
+    """NedNerPlan._fresh_out recycles an output buffer only after the caller
+    dropped the array AND every view of it (lease lifetime via weakref.finalize,
+    no reference-count heuristics)."""
+    import gc
+
+    from paper_1501_02946_b200.recon import NedNerPlan
+
+    class FakePlan:
+        out_shape = (3, 4, 5)
+        _OUT_POOL_SIZE = 2
+
+    p = FakePlan()
+    fresh = NedNerPlan._fresh_out.__get__(p)
+    a = fresh()
+    assert a.flags.writeable and a.flags.c_contiguous and a.shape == p.out_shape
+    a[...] = 1.0
+    view = a[1]                      # a view keeps the buffer reachable
+    del a
+    gc.collect()
+    b = fresh()
+    c = fresh()                      # pool full of live results: an unpooled array
+    for x in (b, c):
+        assert not np.shares_memory(x, view)
+    b[...] = 2.0
+    assert np.all(view == 1.0)
+    held = {"field": pb.ScalarField(b, (1.0, 1.0, 1.0))}  # a ScalarField holding the result also counts
+    del b
+    gc.collect()
+    d = fresh()
+    assert not np.shares_memory(d, held["field"].values) and not np.shares_memory(d, view)
+    del d, view, c
+    gc.collect()
+    e = fresh()                      # everything dropped: a pooled buffer comes back
+    assert any(np.shares_memory(e, s[0]) for s in p._out_pool)
