@@ -710,11 +710,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     const double th = 2.0 * M_PI * i / n_ext - M_PI;  // nufft.py:281
     iw[i] = (float)(psh0 * norm_t / kb_psi(wt, th));
   }
-  std::vector<float2> tw(1 << 14);
-  for (int k = 0; k < (1 << 14); ++k) {
-    const double a = -2.0 * M_PI * k / (1 << 14);
-    tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
-  }
+  const std::vector<float2> tw = make_twiddles();
   NerParams& q = P->ner;
   // tap polynomials: the lowest of degree 7 (one FFMA less per tap pair, the
   // DCT kernel's <.., 7, ..> variants), 8 or 12 whose fit stays at float32

@@ -20,6 +20,16 @@ namespace patfft {
 namespace fft {
 
 constexpr int kLogTwiddles = 14;  // table length 16384
+// Per-pass twiddle tables behind the main table (host: make_twiddles): for a
+// pass at half-length H = 2^LOGH (1 <= LOGH <= kPassTwMaxLog), item offset k
+// reads its R <= 4 stage twiddles W_{H 2^(i+1)}^k, i = 0..3, as 4 consecutive
+// float2 at kPassTwOffset(LOGH) + 4k.  Neighbouring items (lanes) then read
+// neighbouring 32-byte blocks instead of gathering single float2 at a stride
+// of 2^(14-LOGH-i-1) -- in the single-transform NER passes those strided
+// gathers were 60% of the L1 data-pipe wavefronts.
+constexpr int kPassTwMaxLog = 12;
+__host__ __device__ constexpr int kPassTwOffset(int logh) { return (1 << kLogTwiddles) + 4 * ((1 << logh) - 2); }
+constexpr int kTwiddleTableLen = kPassTwOffset(kPassTwMaxLog + 1);
 
 // Packed FP32 (sm_100a FADD2 / FMUL2 / FFMA2): one issue slot per complex
 // add, two per complex multiply.  The compiler folds broadcast scalars,
@@ -192,11 +202,24 @@ struct XorLinear<Addr, std::void_t<decltype(Addr::kXorLinear)>> : std::bool_cons
 template <int R, bool INV, int LOGH>
 __device__ __forceinline__ void pass_butterflies(float2 (&e)[1 << R], int k, const float2* __restrict__ tw) {
   constexpr int PR = 1 << R;
+  float2 wst[4];
+  if constexpr (LOGH > 0 && LOGH <= kPassTwMaxLog) {
+    const float4* pt = reinterpret_cast<const float4*>(tw + kPassTwOffset(LOGH) + 4 * k);
+    const float4 a = __ldg(pt);
+    wst[0] = make_float2(a.x, a.y);
+    wst[1] = make_float2(a.z, a.w);
+    if constexpr (R > 2) {
+      const float4 b = __ldg(pt + 1);
+      wst[2] = make_float2(b.x, b.y);
+      wst[3] = make_float2(b.z, b.w);
+    }
+  }
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     float2 wi = make_float2(1.f, 0.f);
     if constexpr (LOGH > 0) {
-      wi = __ldg(&tw[k << (kLogTwiddles - LOGH - i - 1)]);  // W_{H 2^{i+1}}^k
+      if constexpr (LOGH <= kPassTwMaxLog) wi = wst[i];
+      else wi = __ldg(&tw[k << (kLogTwiddles - LOGH - i - 1)]);  // W_{H 2^{i+1}}^k
       if (INV) wi.y = -wi.y;
     }
 #pragma unroll

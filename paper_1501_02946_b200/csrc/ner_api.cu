@@ -378,11 +378,7 @@ int patfft_ner_plan_create(int n, double c, int K, double alpha, double beta, in
   const double s0 = kb_psihat(P->win, 0.0), norm = 1.0 / (2.0 * M_PI * P->win.c_eff);
   std::vector<float> iw(n);
   for (int k = 0; k < n; ++k) iw[k] = (float)(s0 * norm / kb_psi(P->win, 2.0 * M_PI * k / n - M_PI));
-  std::vector<float2> tw(1 << 14);
-  for (int k = 0; k < (1 << 14); ++k) {
-    const double a = -2.0 * M_PI * k / (1 << 14);
-    tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
-  }
+  const std::vector<float2> tw = make_twiddles();
   P->degree = 8;
   if (fit_ner_poly_public(P->win, 8, P->prm.poly) > 2e-8) {
     P->degree = 12;

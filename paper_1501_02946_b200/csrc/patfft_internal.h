@@ -34,7 +34,11 @@ double bessel_i0(double x);                   // scipy.special.i0 equivalent
 double kb_psi(const Window& w, double th);    // window_eval (nufft.py:159-165)
 double kb_psihat(const Window& w, double x);  // window_ft_eval (nufft.py:168-187)
 int even_fast_len(double target);             // next_even_fast_len (nufft.py:83-89)
-double window_relative_error(const Window& w, int n, int n_over);  // accuracy probe (window.cpp)
+double window_relative_error(const Window& w, int n, int n_over);
+// FFT twiddle table of the shared-memory transforms (fft_smem.cuh): the
+// 2^14-point table exp(-2 pi i k / 2^14) followed by the per-pass tables
+// (kPassTwOffset); float2 pairs, float64-accurate (window.cpp)
+std::vector<float2> make_twiddles();  // accuracy probe (window.cpp)
 
 // ---------------------------------------------------------------------------
 // Device-side parameter blocks

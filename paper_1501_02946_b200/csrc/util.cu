@@ -2,6 +2,7 @@
 // path, and a fill used to flush L2 between timed iterations.
 #include <cuda_runtime.h>
 
+#include "fft_smem.cuh"
 #include "patfft_internal.h"
 
 namespace patfft {
@@ -85,6 +86,27 @@ cudaError_t launch_gather_rows(const float* samples, const int* gidx, float* gri
 cudaError_t launch_fill(float* dst, size_t n, float v, cudaStream_t s) {
   fill_kernel<<<grid_for(n), 256, 0, s>>>(dst, n, v);
   return cudaGetLastError();
+}
+
+}  // namespace patfft
+
+namespace patfft {
+
+std::vector<float2> make_twiddles() {
+  std::vector<float2> tw(fft::kTwiddleTableLen);
+  for (int k = 0; k < (1 << fft::kLogTwiddles); ++k) {
+    const double a = -2.0 * M_PI * k / (1 << fft::kLogTwiddles);
+    tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  for (int logh = 1; logh <= fft::kPassTwMaxLog; ++logh) {
+    const int H = 1 << logh;
+    for (int k = 0; k < H; ++k)
+      for (int i = 0; i < 4; ++i) {
+        const double a = -2.0 * M_PI * k / ((double)H * (2 << i));  // W_{H 2^(i+1)}^k
+        tw[fft::kPassTwOffset(logh) + 4 * k + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+      }
+  }
+  return tw;
 }
 
 }  // namespace patfft
