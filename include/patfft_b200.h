@@ -95,6 +95,15 @@ int patfft_nedner_output_shape(const patfft_nedner_plan* plan, int64_t shape[3])
 int patfft_nedner_execute(patfft_nedner_plan* plan, const double* samples, double* image,
                           double* imag_residual);
 
+/* Pipelined patfft_nedner_execute over n records that share the plan's sensor
+ * layout (e.g. the frames of a time series; BASELINE config 5): samples[k] /
+ * images[k] as in patfft_nedner_execute.  Record k+1 is narrowed and uploaded
+ * and record k-1 downloaded and widened while the device reconstructs record
+ * k; each record's result is bit-identical to a single call.  nonfinite
+ * (optional, n entries) receives each volume's non-finite voxel count. */
+int patfft_nedner_execute_batch(patfft_nedner_plan* plan, int n, const double* const* samples,
+                                double* const* images, int64_t* nonfinite);
+
 /* patfft_nedner_execute that also counts the non-finite voxels of the image
  * (written to *nonfinite when non-NULL) in the same host pass that widens the
  * float32 volume to float64, so the caller can apply the ScalarField
@@ -218,6 +227,13 @@ int patfft_nedner_launches_per_execute(const patfft_nedner_plan* plan, int* own,
  * x N_t MACs per product); info[2] = tiles (or SIMT blocks); info[3] = time
  * samples per tensor-core work item. */
 int patfft_nedner_spread_info(const patfft_nedner_plan* plan, int64_t info[4]);
+
+/* Windows the plan evaluates (nufft.py:133-149 semantics): taps[0] = 2K of the
+ * lateral gridding, taps[1] = 2K of the NER (8 when the float32-grade window
+ * replaced an auto-resolved K > 4), taps[2] = degree
+ * of the NER tap polynomials; win[0..2] = (c_eff, alpha, beta) of the lateral
+ * window along the last axis, win[3..5] = the same for the NER window. */
+int patfft_nedner_window_info(const patfft_nedner_plan* plan, int64_t taps[3], double win[6]);
 
 /* ---- small runtime helpers used by the Python shim and bench.py ---------- */
 const char* patfft_last_error(void);

@@ -49,6 +49,8 @@ _SIGS = {
     "patfft_nedner_output_shape": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
     "patfft_nedner_execute": (ctypes.c_int, [_P, _P, _P, _D]),
     "patfft_nedner_execute_checked": (ctypes.c_int, [_P, _P, _P, _D, ctypes.POINTER(ctypes.c_int64)]),
+    "patfft_nedner_execute_batch": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_P), ctypes.POINTER(_P),
+                                                   ctypes.POINTER(ctypes.c_int64)]),
     "patfft_nedner_execute_device": (ctypes.c_int, [_P, _P, _P, _P]),
     "patfft_nedner_execute_frames_device": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P]),
     "patfft_nedner_plan_destroy": (None, [_P]),
@@ -81,6 +83,7 @@ _SIGS = {
     "patfft_nedner_stage_bytes": (ctypes.c_int, [_P, _D, ctypes.c_int]),
     "patfft_nedner_launches_per_execute": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "patfft_nedner_spread_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
+    "patfft_nedner_window_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64), _D]),
     "patfft_last_error": (ctypes.c_char_p, []),
     "patfft_version": (ctypes.c_char_p, []),
     "patfft_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),

@@ -355,7 +355,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // given.  PATFFT_FP32_WINDOW=0 keeps the requested K.
   P->K2t = P->K2;
   {
-    static const bool fp32_win = [] {
+    const bool fp32_win = [] {  // read per plan (tests compare both settings in one process)
       const char* e = std::getenv("PATFFT_FP32_WINDOW");
       return e ? std::atoi(e) != 0 : true;
     }();
@@ -625,7 +625,16 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     }
     std::vector<int> order(ntiles);
     for (int t = 0; t < ntiles; ++t) order[t] = t;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return padded[a] > padded[b]; });
+    // claim order: 0 = longest tile first (load balance), 1 = row-major tiles (neighbouring
+    // tiles share sensors: their gathered sample rows are re-read from L2, not HBM)
+    const int torder = [] {
+      const char* e = std::getenv("PATFFT_TC_ORDER");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (torder == 0)
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return padded[a] > padded[b]; });
+    else
+      std::stable_partition(order.begin(), order.end(), [&](int a) { return padded[a] > 0; });
     for (int t : order) tctiles.push_back(make_int4((int)start[t], (int)padded[t], (t / tcs) * 8, (t % tcs) * 16));
     P->tc_ntiles = ntiles;
     P->tc_nonempty = (int)std::count_if(padded.begin(), padded.end(), [](int64_t v) { return v > 0; });
@@ -797,6 +806,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   }
 
   CUDA_TRY(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  if (const char* e = std::getenv("PATFFT_LAT_CHUNK")) P->lat_chunk = std::max(0, std::atoi(e)) / 64 * 64;
   if (const char* e = std::getenv("PATFFT_OVERLAP_CHUNKS")) P->overlap_chunks = std::max(1, std::min(4, std::atoi(e)));
   if (const char* e = std::getenv("PATFFT_GRAPHS")) P->use_graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("PATFFT_H2D_CHUNKS")) P->h2d_chunks = std::max(1, std::atoi(e));
@@ -887,6 +897,8 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   LateralParams& L = P->lat;
   L.grid = P->d_grid;
   L.Y = P->d_Y;
+  L.ys = T;
+  L.yt0 = 0;
   L.gh = P->d_gh;
   L.tw = P->d_tw;
   L.dp0 = P->d_dp0;
@@ -974,6 +986,7 @@ int patfft_ned_execute(patfft_nedner_plan* P, const double* values, double* out,
   CUDA_TRY(launch_lateral_col(L, st));
   L.T = B;  // rowfft works on complex columns
   L.t_end = B;
+  L.ys = B;
   CUDA_TRY(launch_lateral_row(L, st));
   CUDA_TRY(launch_f32_to_f64(reinterpret_cast<const float*>(P->d_gh), P->d_out64, 2 * out_c, st));
   CUDA_TRY(cudaMemcpyAsync(out, P->d_out64, 2 * out_c * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1087,6 +1100,20 @@ static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* 
     if (P->mode == 0) CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
     else CUDA_TRY(launch_gather_rows(samples, P->d_gidx, P->d_grid, P->M, T, st));
     if (prof) CUDA_TRY(cudaEventRecord(P->ev[1], st));
+    const int lc = P->lat_chunk;
+    if (lc > 0 && lc < T && P->mode == 0 && !prof) {
+      // time chunks of lc samples: colfft writes the chunk's Y (nrows x N1h x lc,
+      // reused for every chunk, L2-resident) and rowfft consumes it right away,
+      // so the Y round trip stays in L2 instead of HBM
+      L.ys = lc;
+      for (int tb = 0; tb < T; tb += lc) {
+        L.t_begin = L.yt0 = tb;
+        L.t_end = std::min(T, tb + lc);
+        CUDA_TRY(launch_lateral_col(L, st));
+        CUDA_TRY(launch_lateral_row(L, st));
+      }
+      return PATFFT_OK;
+    }
     CUDA_TRY(launch_lateral_col(L, st));
     if (prof) CUDA_TRY(cudaEventRecord(P->ev[2], st));
     CUDA_TRY(launch_lateral_row(L, st));
@@ -1173,13 +1200,16 @@ static int execute_graphed(patfft_nedner_plan* P, int n_frames, const float* sam
     return PATFFT_OK;
   };
   if (P->profiling || !P->use_graphs) return enqueue();
-  if (P->graph_exec && P->g_in == samples && P->g_out == image && P->g_frames == n_frames) {
-    CUDA_TRY(cudaGraphLaunch(P->graph_exec, st));
-    return PATFFT_OK;
-  }
-  if (P->graph_exec) {
-    cudaGraphExecDestroy(P->graph_exec);
-    P->graph_exec = nullptr;
+  for (auto& g : P->graphs)
+    if (g.exec && g.in == samples && g.out == image && g.frames == n_frames) {
+      CUDA_TRY(cudaGraphLaunch(g.exec, st));
+      return PATFFT_OK;
+    }
+  auto& slot = P->graphs[P->graph_next];
+  P->graph_next = (P->graph_next + 1) % patfft_nedner_plan::kGraphSlots;
+  if (slot.exec) {
+    cudaGraphExecDestroy(slot.exec);
+    slot.exec = nullptr;
   }
   cudaGraph_t graph = nullptr;
   CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -1190,16 +1220,16 @@ static int execute_graphed(patfft_nedner_plan* P, int n_frames, const float* sam
     return rc;
   }
   if (ce != cudaSuccess) return fail(PATFFT_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-  const cudaError_t ie = cudaGraphInstantiate(&P->graph_exec, graph, 0);
+  const cudaError_t ie = cudaGraphInstantiate(&slot.exec, graph, 0);
   cudaGraphDestroy(graph);
   if (ie != cudaSuccess) {
-    P->graph_exec = nullptr;
+    slot.exec = nullptr;
     return fail(PATFFT_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
   }
-  P->g_in = samples;
-  P->g_out = image;
-  P->g_frames = n_frames;
-  CUDA_TRY(cudaGraphLaunch(P->graph_exec, st));
+  slot.in = samples;
+  slot.out = image;
+  slot.frames = n_frames;
+  CUDA_TRY(cudaGraphLaunch(slot.exec, st));
   return PATFFT_OK;
 }
 
@@ -1548,11 +1578,165 @@ int patfft_nedner_execute(patfft_nedner_plan* P, const double* samples, double* 
   return patfft_nedner_execute_checked(P, samples, image, imag_residual, nullptr);
 }
 
+// Pipelined drop-in execution of n host records on one plan (one sensor
+// layout, e.g. the frames of a time series): the reference call
+// (recon.py:358-379, float64 in / float64 out) applied to a stream.  While
+// the device reconstructs record k, the host cores widen record k-1's
+// downloaded volume and narrow record k+1's samples, and the copy engines
+// move k+1 up and k-1 down (PCIe is full duplex).  A share of each pinned
+// caller buffer (batch_direct_in / _out) crosses as float64 by DMA with the
+// conversion on the device, which balances the host cores' memory traffic
+// against the PCIe link; pageable caller buffers go through the cores only.
+// Every record gets exactly the single-call arithmetic (bit-identical).
+static int batch_setup(patfft_nedner_plan* P, size_t in_n, size_t out_n) {
+  if (P->batch_ready) return PATFFT_OK;
+  int rc;
+  for (auto& b : P->bset) {
+    if ((rc = dalloc(&b.d_in, in_n))) return rc;
+    if ((rc = dalloc(&b.d_in64, in_n))) return rc;
+    if ((rc = dalloc(&b.d_out, out_n))) return rc;
+    if ((rc = dalloc(&b.d_out64, out_n))) return rc;
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&b.d_bad), sizeof(unsigned long long)));
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&b.h_in), in_n * sizeof(float), cudaHostAllocDefault));
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&b.h_out), out_n * sizeof(float), cudaHostAllocDefault));
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&b.h_bad), sizeof(unsigned long long), cudaHostAllocDefault));
+    for (cudaEvent_t* e : {&b.ev_in, &b.ev_comp, &b.ev_out}) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (auto& e : b.ev_blk) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(b.ev_comp, P->stream));  // "previous use finished" for the first records
+    CUDA_TRY(cudaEventRecord(b.ev_out, P->stream));
+    CUDA_TRY(cudaEventRecord(b.ev_in, P->stream));
+  }
+  if (!P->copy_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : P->ev_h2d) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_out_stream, cudaStreamNonBlocking));
+  if (const char* e = std::getenv("PATFFT_BATCH_DIRECT_IN")) P->batch_direct_in = std::min(1.0, std::max(0.0, std::atof(e)));
+  if (const char* e = std::getenv("PATFFT_BATCH_DIRECT_OUT")) P->batch_direct_out = std::min(1.0, std::max(0.0, std::atof(e)));
+  P->batch_ready = true;
+  return PATFFT_OK;
+}
+
+int patfft_nedner_execute_batch(patfft_nedner_plan* P, int n, const double* const* samples, double* const* images,
+                                int64_t* nonfinite) {
+  if (!P || n < 0 || (n > 0 && (!samples || !images))) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  for (int k = 0; k < n; ++k)
+    if (!samples[k] || !images[k]) return fail(PATFFT_ERR_PARAMETER, "null record buffer");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  if (P->world != 1) return fail(PATFFT_ERR_PARAMETER, "sharded plan: use the patfft_nedner_shard_* stages");
+  const int M = P->M, T = P->T;
+  const size_t in_n = (size_t)M * T, out_n = (size_t)P->N0u * P->N1u * P->Tu;
+  int rc;
+  if ((rc = batch_setup(P, in_n, out_n))) return rc;
+  const bool big = in_n * sizeof(double) >= (size_t)(4 << 20);
+  constexpr int kBlk = 16;
+  const int rb = big ? std::min(P->host_blocks, kBlk) : 1;  // upload row blocks
+  const int ob = big ? kBlk : 1;                            // download voxel blocks
+  cudaStream_t st = P->stream, cin = P->copy_stream, cout = P->copy_out_stream;
+  std::vector<size_t> od(n);  // direct voxels of record k
+  double tr_wait = 0.0, tr_widen = 0.0, tr_narrow = 0.0, tr_inwait = 0.0;
+  const double tr0 = P->host_trace ? wall_ms() : 0.0;
+  auto widen = [&](int k) -> int {
+    auto& b = P->bset[k & 1];
+    const size_t sn = out_n - od[k];
+    const size_t per = ((sn + ob - 1) / ob + 255) / 256 * 256;
+    int64_t bad = 0;
+    for (int j = 0; j * per < sn; ++j) {
+      const size_t a = (size_t)j * per, m = std::min(per, sn - a);
+      const double w0 = P->host_trace ? wall_ms() : 0.0;
+      CUDA_TRY(cudaEventSynchronize(b.ev_blk[j]));
+      const double w1 = P->host_trace ? wall_ms() : 0.0;
+      bad += host_widen(b.h_out + a, images[k] + od[k] + a, (int64_t)m);
+      if (P->host_trace) {
+        tr_wait += w1 - w0;
+        tr_widen += wall_ms() - w1;
+      }
+    }
+    const double w2 = P->host_trace ? wall_ms() : 0.0;
+    CUDA_TRY(cudaEventSynchronize(b.ev_out));
+    if (P->host_trace) tr_wait += wall_ms() - w2;
+    if (od[k]) bad += (int64_t)*b.h_bad;
+    if (nonfinite) nonfinite[k] = bad;
+    return PATFFT_OK;
+  };
+  for (int k = 0; k <= n; ++k) {
+    if (k < n) {
+      auto& b = P->bset[k & 1];
+      const int Md = (big && P->batch_direct_in > 0 && host_pinned(samples[k], in_n * sizeof(double)))
+                         ? (int)(P->batch_direct_in * M) : 0;
+      od[k] = (out_n * sizeof(double) >= (size_t)(4 << 20) && P->batch_direct_out > 0 &&
+               host_pinned(images[k], out_n * sizeof(double)))
+                  ? (size_t)(P->batch_direct_out * out_n) / 256 * 256 : 0;
+      // (A) upload: d_in is free once record k-2's compute is done; h_in once its H2D is done
+      CUDA_TRY(cudaStreamWaitEvent(cin, b.ev_comp, 0));
+      const double w0 = P->host_trace ? wall_ms() : 0.0;
+      CUDA_TRY(cudaEventSynchronize(b.ev_in));
+      if (P->host_trace) tr_inwait += wall_ms() - w0;
+      if (Md)
+        CUDA_TRY(cudaMemcpyAsync(b.d_in64, samples[k], (size_t)Md * T * sizeof(double), cudaMemcpyHostToDevice, cin));
+      const int rows_per = std::max(1, (M - Md + rb - 1) / rb);
+      for (int m0 = Md; m0 < M; m0 += rows_per) {
+        const int m1 = std::min(M, m0 + rows_per);
+        const double w1 = P->host_trace ? wall_ms() : 0.0;
+        host_narrow_rows(samples[k] + (size_t)m0 * T, T, b.h_in + (size_t)m0 * T, T, m1 - m0, T);
+        if (P->host_trace) tr_narrow += wall_ms() - w1;
+        CUDA_TRY(cudaMemcpyAsync(b.d_in + (size_t)m0 * T, b.h_in + (size_t)m0 * T, (size_t)(m1 - m0) * T * sizeof(float),
+                                 cudaMemcpyHostToDevice, cin));
+      }
+      CUDA_TRY(cudaEventRecord(b.ev_in, cin));
+      // (B) compute: after the upload, and once record k-2's download has read d_out
+      CUDA_TRY(cudaStreamWaitEvent(st, b.ev_in, 0));
+      CUDA_TRY(cudaStreamWaitEvent(st, b.ev_out, 0));
+      if (Md) CUDA_TRY(launch_f64_to_f32(b.d_in64, b.d_in, (size_t)Md * T, st));
+      if ((rc = execute_graphed(P, 1, b.d_in, b.d_out, st))) return rc;
+      if (od[k]) {
+        CUDA_TRY(cudaMemsetAsync(b.d_bad, 0, sizeof(unsigned long long), st));
+        CUDA_TRY(launch_f32_to_f64_count(b.d_out, b.d_out64, od[k], b.d_bad, st));
+      }
+      CUDA_TRY(cudaEventRecord(b.ev_comp, st));
+      // (C) download: staged float32 blocks first (the host widens them), then the direct float64 part
+      CUDA_TRY(cudaStreamWaitEvent(cout, b.ev_comp, 0));
+      const size_t sn = out_n - od[k];
+      const size_t per = ((sn + ob - 1) / ob + 255) / 256 * 256;
+      for (int j = 0; j * per < sn; ++j) {
+        const size_t a = (size_t)j * per, m = std::min(per, sn - a);
+        CUDA_TRY(cudaMemcpyAsync(b.h_out + a, b.d_out + od[k] + a, m * sizeof(float), cudaMemcpyDeviceToHost, cout));
+        CUDA_TRY(cudaEventRecord(b.ev_blk[j], cout));
+      }
+      if (od[k]) {
+        CUDA_TRY(cudaMemcpyAsync(images[k], b.d_out64, od[k] * sizeof(double), cudaMemcpyDeviceToHost, cout));
+        CUDA_TRY(cudaMemcpyAsync(b.h_bad, b.d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, cout));
+      }
+      CUDA_TRY(cudaEventRecord(b.ev_out, cout));
+    }
+    // (D) the host widens the previous record while this one uploads / computes
+    if (k >= 1 && (rc = widen(k - 1))) return rc;
+  }
+  if (P->host_trace && n > 0)
+    std::fprintf(stderr, "[patfft batch] %d records: %.2f ms/record | narrow %.2f, widen %.2f, wait download %.2f, "
+                 "wait staging %.2f ms/record (%d host threads)\n", n, (wall_ms() - tr0) / n, tr_narrow / n,
+                 tr_widen / n, tr_wait / n, tr_inwait / n, host_threads());
+  return PATFFT_OK;
+}
+
 void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
   if (P->stream) cudaStreamSynchronize(P->stream);
-  if (P->graph_exec) cudaGraphExecDestroy(P->graph_exec);
+  for (auto& g : P->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (P->copy_out_stream) cudaStreamSynchronize(P->copy_out_stream);
+  for (auto& b : P->bset) {
+    for (void* p : {(void*)b.d_in, (void*)b.d_in64, (void*)b.d_out, (void*)b.d_out64, (void*)b.d_bad}) free_dev(p);
+    for (void* h : {(void*)b.h_in, (void*)b.h_out, (void*)b.h_bad})
+      if (h) cudaFreeHost(h);
+    for (cudaEvent_t e : {b.ev_in, b.ev_comp, b.ev_out})
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : b.ev_blk)
+      if (e) cudaEventDestroy(e);
+  }
+  if (P->copy_out_stream) cudaStreamDestroy(P->copy_out_stream);
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
   for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_gh,
@@ -1649,6 +1833,21 @@ int patfft_nedner_spread_info(const patfft_nedner_plan* P, int64_t info[4]) {
   info[1] = tc ? P->tc_records : P->n_records;  // records (tile x sensor pairs, padded to 16 per tile)
   info[2] = tc ? P->tc_ntiles : P->nblk;        // tiles / SIMT blocks
   info[3] = tc ? P->tc_n : 0;                   // time samples per tensor-core item
+  return PATFFT_OK;
+}
+
+int patfft_nedner_window_info(const patfft_nedner_plan* P, int64_t taps[3], double win[6]) {
+  if (!P || !taps || !win) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  taps[0] = P->K2;
+  taps[1] = P->K2t;
+  taps[2] = P->ner.poly7 ? 7 : P->poly_degree;
+  const patfft::Window& wl = P->win_lat[P->n_lat - 1];
+  win[0] = wl.c_eff;
+  win[1] = wl.alpha;
+  win[2] = wl.beta;
+  win[3] = P->win_t.c_eff;
+  win[4] = P->win_t.alpha;
+  win[5] = P->win_t.beta;
   return PATFFT_OK;
 }
 

@@ -128,14 +128,17 @@ __global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kerne
     }
     return;
   }
-  float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * T;
+  // Y: [nrows][ny][ys] holding times [yt0, yt0 + ys) (the whole record, or a
+  // time chunk that stays L2-resident until rowfft consumes it)
+  const int ys = p.ys;
+  float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * ys;
   // each thread keeps one packed time pair q (nth is a multiple of P) and walks the bins k
   const int q = tid & (P - 1);
   const int t = t0 + 2 * q;
   if (t >= p.t_end) return;
   const int kstep = nth >> PLOG;
-  const size_t ostep = (size_t)kstep * T;
-  float2* __restrict__ o = dst + (size_t)(tid >> PLOG) * T + t;
+  const size_t ostep = (size_t)kstep * ys;
+  float2* __restrict__ o = dst + (size_t)(tid >> PLOG) * ys + (t - p.yt0);
   for (int k = tid >> PLOG; k < p.ny; k += kstep, o += ostep) {
     const float2 zk = zat(k, q);
     const float2 zm = fft::conjf2(zat((n - k) & (n - 1), q));
@@ -155,9 +158,11 @@ __global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kerne
   const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.T, nr = p.nrows;
   const TileAddr ad{PLOG};
+  const int ys = p.ys;
+  const float2* __restrict__ yb = p.Y - p.yt0;
   auto ld = [&](int row, int q) {
     const int t = t0 + q;
-    return (t < p.t_end) ? __ldcs(p.Y + ((size_t)row * p.ny + j1) * T + t) : make_float2(0.f, 0.f);
+    return (t < p.t_end) ? __ldcs(yb + ((size_t)row * p.ny + j1) * ys + t) : make_float2(0.f, 0.f);
   };
   constexpr int LLAST = LC > 0 ? fft::LastPassLogh<(LC > 0 ? LC : 1), 4, false>::value : 0;
   constexpr bool FUSED = PATFFT_ROW_FUSED && LC > 0 && LLAST > 0;
@@ -165,8 +170,8 @@ __global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kerne
     fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(
         sm, p.tw, tid, fft::TileC<PLOG>(), fft::rows_ld([&](int row, int q) -> const float2* {
           const int t = t0 + q;
-          return t < p.t_end ? p.Y + ((size_t)row * p.ny + j1) * T + t : nullptr;
-        }, (size_t)p.ny * T));
+          return t < p.t_end ? yb + ((size_t)row * p.ny + j1) * ys + t : nullptr;
+        }, (size_t)p.ny * ys));
   } else if constexpr (LC > 0) {
     fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(sm, p.tw, tid, fft::TileC<PLOG>(), ld);
   } else {

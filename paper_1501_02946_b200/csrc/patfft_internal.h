@@ -80,6 +80,7 @@ struct LateralParams {
   const float* dp1;    // [N1]
   int T, nrows, lrows, ncols, lcols, ny, N0, N1;
   int t_begin, t_end;  // forward kernels: time range processed by this launch
+  int ys, yt0;         // Y time stride and the time stored at Y offset 0 (whole record: T, 0)
   int cplx;            // 1: NedPlan mode (complex values, full spectrum, no Hermitian fix-up)
   int centered;        // NedPlan output order
   // inverse
@@ -170,12 +171,37 @@ struct patfft_nedner_plan {
   size_t h_stage_n = 0;
   cudaEvent_t ev_d2h[kMaxH2dChunks] = {}, ev_done = nullptr;
   int overlap_chunks = 1;  // time chunks of the overlapped forward stages (1 = off)
-  // CUDA graph of the last executed (samples, image, frames) triple
+  int lat_chunk = 0;       // time samples per colfft -> rowfft chunk (0 = whole record)
+  // CUDA graphs of the last executed (samples, image, frames) triples (the
+  // batch path alternates two buffer sets)
   bool use_graphs = true;
-  cudaGraphExec_t graph_exec = nullptr;
-  const float* g_in = nullptr;
-  float* g_out = nullptr;
-  int g_frames = 0;
+  struct GraphSlot {
+    cudaGraphExec_t exec = nullptr;
+    const float* in = nullptr;
+    float* out = nullptr;
+    int frames = 0;
+  };
+  static constexpr int kGraphSlots = 4;
+  GraphSlot graphs[kGraphSlots];
+  int graph_next = 0;
+  // pipelined batch of host records (patfft_nedner_execute_batch): two sets of
+  // device input/output buffers and pinned staging, one per record in flight
+  struct BatchSet {
+    float* d_in = nullptr;
+    double* d_in64 = nullptr;  // direct (float64 DMA) sensor rows
+    float* d_out = nullptr;
+    double* d_out64 = nullptr;  // direct voxels, widened on the device
+    unsigned long long* d_bad = nullptr;
+    float* h_in = nullptr;   // pinned staging of the narrowed rows
+    float* h_out = nullptr;  // pinned staging of the downloaded float32 voxels
+    unsigned long long* h_bad = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_comp = nullptr, ev_out = nullptr;
+    cudaEvent_t ev_blk[16] = {};
+  };
+  BatchSet bset[2];
+  bool batch_ready = false;
+  cudaStream_t copy_out_stream = nullptr;
+  double batch_direct_in = 0.4, batch_direct_out = 0.4;
   std::mutex mu;
 
   // sizes

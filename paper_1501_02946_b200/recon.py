@@ -312,6 +312,30 @@ class NedNerPlan:
                                                                ctypes.byref(resid), ctypes.byref(bad)))
         return out, resid.value, int(bad.value)
 
+    def execute_batch(self, samples_list, outs=None):
+        """Pipelined ``execute_checked`` over records sharing this plan's layout
+        (patfft_nedner_execute_batch): record k+1 uploads and record k-1
+        downloads while record k is reconstructed.  Returns (volumes, nonfinite
+        counts); each volume is bit-identical to a single ``execute``."""
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in samples_list]
+        for a in arrs:
+            if a.shape != (self.n_sensors, self.n_time):
+                raise DataValidationError("samples shape does not match the plan")
+        n = len(arrs)
+        if outs is None:
+            outs = [np.empty(self.out_shape, dtype=np.float64) for _ in range(n)]
+        if len(outs) != n:
+            raise DataValidationError("need one output array per record")
+        for o in outs:
+            if o.shape != self.out_shape or o.dtype != np.float64 or not o.flags.c_contiguous:
+                raise DataValidationError("out must be a C-contiguous float64 array of the output shape")
+        pin = (ctypes.c_void_p * max(1, n))(*[a.ctypes.data for a in arrs])
+        pout = (ctypes.c_void_p * max(1, n))(*[o.ctypes.data for o in outs])
+        bad = (ctypes.c_int64 * max(1, n))()
+        with self._lock:
+            _lib.check(self._lib.patfft_nedner_execute_batch(self._h, n, pin, pout, bad))
+        return outs, [int(bad[i]) for i in range(n)]
+
     # Output volumes handed to callers are recycled once the caller has dropped
     # every reference to them (the array, any view of it, the ScalarField
     # holding it): a fresh 0.5 GB numpy array costs more in first-touch page
@@ -347,6 +371,15 @@ class NedNerPlan:
     def execute_frames_device(self, n_frames: int, samples_ptr: int, images_ptr: int, stream: int = 0) -> None:
         _lib.check(self._lib.patfft_nedner_execute_frames_device(self._h, int(n_frames), ctypes.c_void_p(samples_ptr),
                                                                  ctypes.c_void_p(images_ptr), ctypes.c_void_p(stream)))
+
+    def window_info(self) -> dict:
+        """Taps and window parameters the plan evaluates (patfft_nedner_window_info)."""
+        taps = (ctypes.c_int64 * 3)()
+        win = (ctypes.c_double * 6)()
+        _lib.check(self._lib.patfft_nedner_window_info(self._h, taps, win))
+        return {"lateral_taps": int(taps[0]), "ner_taps": int(taps[1]), "ner_poly_degree": int(taps[2]),
+                "lateral": {"c_eff": win[0], "alpha": win[1], "beta": win[2]},
+                "ner": {"c_eff": win[3], "alpha": win[4], "beta": win[5]}}
 
     def set_profiling(self, on: bool) -> None:
         _lib.check(self._lib.patfft_nedner_set_profiling(self._h, 1 if on else 0))
@@ -498,7 +531,15 @@ def _field(plan, samples) -> ScalarField:
     img, resid, nonfinite = plan.execute_checked(np.asarray(samples, dtype=np.float64))
     if nonfinite:
         raise DataValidationError("field values must be finite")
-    return ScalarField._checked(img, plan.spacing, {"imag_residual": float(resid)})
+    return ScalarField._checked(img, plan.spacing, {"imag_residual": float(resid), "imag_residual_kind": _IMAG_KIND})
+
+
+# recon.py:255-257 reports max|Im|/max|Re| of its complex float64 ifftn of the
+# Hermitian-symmetrised spectrum: pure float64 rounding (6e-17 .. 1.5e-16 on the
+# reference goldens).  This path inverts the Hermitian half spectrum with a
+# C2R transform, whose imaginary part is identically zero: the same quantity
+# without the rounding, reported as exactly 0.0.
+_IMAG_KIND = "exact: Hermitian half-spectrum C2R inverse, imaginary part identically zero"
 
 
 def _as_spec(spec):

@@ -60,7 +60,10 @@ def test_gpu_cfg4_matches_reference_golden(fp32_window):
     if fp32_window:
         f = pb.reconstruct_nedner(s.as_record())
     else:
-        img, _ = _env_plan(s, PATFFT_FP32_WINDOW=0).execute(s.samples)
+        plan = _env_plan(s, PATFFT_FP32_WINDOW=0)
+        wi = plan.window_info()
+        assert wi["lateral_taps"] == 12 and wi["ner_taps"] == 12, wi
+        img, _ = plan.execute(s.samples)
         f = pb.ScalarField(img, tuple(g["spacing"]))
     v = f.values
     assert v.shape == (256, 256, 1024)
@@ -176,3 +179,66 @@ def test_gpu_cfg4_geometry_short_depth_both_gridding_forms(f16):
     err = rel_l2(got, want)
     print(f"cfg4 layout at Nt=128, gridding f16={f16}: rel-L2 {err:.3e}")
     assert err <= TOL
+
+
+def test_gpu_window_selection():
+    """Auto (alpha, beta) windows with K > 4 run with the float32-grade 8 taps;
+    explicit windows and K <= 4 keep what was asked (nufft.py:133-149)."""
+    s = synth.make_3d(3, 16, 64, 20e-9, "jittered", 1)
+
+    def taps(spec):
+        p = pb.NedNerPlan(s.positions, s.weights, 64, s.dt, s.sound_speed, s.dx, s.n_lateral, spec=spec)
+        w = p.window_info()
+        return w["lateral_taps"], w["ner_taps"]
+
+    assert taps(None) == (8, 8)
+    assert taps(pb.WindowSpec(K=5)) == (8, 8)
+    assert taps(pb.WindowSpec(K=3)) == (6, 6)
+    assert taps(pb.WindowSpec(K=6, alpha=9.41535318280861)) == (12, 12)
+
+
+def _pinned_f64(shape):
+    import ctypes
+
+    from paper_1501_02946_b200 import _lib
+    lib = _lib.load()
+    p = ctypes.c_void_p()
+    n = int(np.prod(shape))
+    _lib.check(lib.patfft_host_alloc(8 * n, ctypes.byref(p)))
+    a = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_double)), shape=(n,)).reshape(shape)
+    return a, p
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_gpu_batch_pipeline_bit_identical_to_single_calls(name):
+    """patfft_nedner_execute_batch (record k+1 up / k-1 down while k computes)
+    gives every record exactly the single-call result, with pageable and pinned
+    caller buffers (the pinned ones move a share as float64 by DMA), and counts
+    non-finite voxels per record."""
+    from paper_1501_02946_b200 import _lib
+
+    lib = _lib.load()
+    s = synth.CONFIGS[name]()
+    plan = pb.NedNerPlan(s.positions, s.weights, s.samples.shape[1], s.dt, s.sound_speed, s.dx, s.n_lateral)
+    rng = np.random.default_rng(9)
+    recs = [s.samples * rng.uniform(0.5, 2.0) for _ in range(5)]
+    recs[3] = recs[3].copy()
+    recs[3][11, 7] = np.nan
+    want = [plan.execute_checked(r) for r in recs]
+    vols, bad = plan.execute_batch(recs)
+    for k in range(5):
+        assert bad[k] == want[k][2]
+        assert np.array_equal(vols[k], want[k][0], equal_nan=True)
+    assert bad[3] > 0 and all(bad[k] == 0 for k in (0, 1, 2, 4))
+    pins = [_pinned_f64(s.samples.shape) for _ in range(3)] + [_pinned_f64(plan.out_shape) for _ in range(3)]
+    try:
+        for k in range(3):
+            pins[k][0][...] = recs[k]
+        outs = [pins[3 + k][0] for k in range(3)]
+        vols, bad = plan.execute_batch([pins[k][0] for k in range(3)], outs)
+        for k in range(3):
+            assert bad[k] == 0
+            assert np.array_equal(outs[k], want[k][0])
+    finally:
+        for _, p in pins:
+            lib.patfft_host_free(p)
