@@ -409,14 +409,17 @@ def run_sharded_arm(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32/c64", "data": "synthetic (seeded, BASELINE config shapes)",
-            "config": dict(_config_json(args, rec), parallelism=f"sharded x{world}: time-sliced NED, "
-                           "all-to-all, row-sliced NER, all-to-all, time-sliced lateral inverse"),
+            "config": dict(_config_json(args, rec, world), parallelism=f"sharded x{world}: time-sliced NED, "
+                           "pipelined all-to-all, row-sliced NER, pipelined all-to-all, time-sliced lateral inverse"),
             "clocks": clk,
             "e2e": {"value": vox / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * host_slice.size * world,
                     "d2h_bytes_per_step": 8 * int(np.prod(pin_out.shape)) * world, "ms_per_step": 1e3 * e2e_s},
-            "gpu_launches": 7 * args.steps, "gpu_launches_note": "per rank per step: absmax (sample scale of the fp16 "
-            "gridding), spread, colfft, rowfft, ner, inv_col, inv_c2r (+1 flush outside the events); 2 NCCL "
-            "all-to-alls",
+            "gpu_launches": (4 + 2 * sh.C + sh.B) * args.steps,
+            "gpu_launches_note": (f"per rank per step: absmax (sample scale of the fp16 gridding) + spread, colfft + "
+                                  f"rowfft per time piece ({sh.C} pieces), ner per row block ({sh.B} blocks), inv_col "
+                                  f"+ inv_c2r (+1 flush outside the events); grouped NCCL send/recv per piece and per "
+                                  f"block (none at world 1)"),
+            "pipeline": {"time_pieces": sh.C, "row_blocks": sh.B},
         }
         emit(line)
     dist.destroy_process_group()

@@ -175,6 +175,18 @@ int patfft_nedner_shard_rows(const patfft_nedner_plan* plan, int64_t* row_starts
 int patfft_nedner_shard_forward(patfft_nedner_plan* plan, const float* samples_slice, void* gh_send, void* stream);
 int patfft_nedner_shard_ner(patfft_nedner_plan* plan, const void* gh_recv, void* z_send, void* stream);
 int patfft_nedner_shard_inverse(patfft_nedner_plan* plan, const void* z_recv, float* image_slice, void* stream);
+/* Pipelined variants (paper_1501_02946_b200/parallel.py overlaps each exchange
+ * with the next piece of compute):
+ *  spread: gridding of the whole local time slice into the plan's grid;
+ *  lateral: lateral FFTs of local times [t_begin, t_end) (multiples of 32) of
+ *    that grid into gh_chunk = [rows_total][t_end - t_begin];
+ *  ner_rows: NER + depth IFFT of the rank's local rows [row_begin, row_end)
+ *    from gh_recv laid out [t / in_tchunk][rows_mine][in_tchunk] (in_tchunk a
+ *    power of two) into z_block = [dst rank][row_end - row_begin][N_t / world]. */
+int patfft_nedner_shard_spread(patfft_nedner_plan* plan, const float* samples_slice, void* stream);
+int patfft_nedner_shard_lateral(patfft_nedner_plan* plan, int t_begin, int t_end, void* gh_chunk, void* stream);
+int patfft_nedner_shard_ner_rows(patfft_nedner_plan* plan, const void* gh_recv, int in_tchunk, int row_begin,
+                                 int row_end, void* z_block, void* stream);
 
 /* ---- forward model: the reference's forward_fourier (forward.py:105-166) --
  * Full-grid sensor traces of an initial pressure field on an

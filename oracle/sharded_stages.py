@@ -7,12 +7,12 @@ stage produces exactly what the matching ``patfft_nedner_shard_*`` CUDA stage
 produces (same layout, same sign conventions), computed with the oracle's
 restatement of the reference (nedner_oracle.py):
 
-* forward : NED of the time slice (nufft.py:400-418), Hermitian part on
+* forward : (spread + lateral) NED of the time slice (nufft.py:400-418), Hermitian part on
             the lateral Nyquist planes (recon.py:218-222), half spectrum in
             j1, multiplied by (-1)^(j0+j1) (the GPU grids on a centred
             oversampled plane and skips the output fftshift -- the two signs
             cancel);
-* ner     : warped NER + amplitude/band (recon.py:274-308), scaled by
+* ner     : (ner_rows) warped NER + amplitude/band (recon.py:274-308), scaled by
             1/(N0 N1 T) and inverse-FFT'd along depth;
 * inverse : lateral inverse FFT (C2R along j1).
 """
@@ -60,7 +60,27 @@ class NumpyStages:
     def _put(t, arr):
         t.copy_(t.new_tensor(np.ascontiguousarray(arr, dtype=np.complex64).view(np.float32).ravel()))
 
+    # pipelined stages (ShardedNedNer): spread keeps the slice's spectrum, lateral
+    # hands out time pieces of it, ner_rows works on a block of the rank's rows
+    def spread(self, samples_slice, stream=0):
+        self._half = self._forward_half(samples_slice)
+
+    def lateral(self, t_begin, t_end, gh_chunk, stream=0):
+        self._put(gh_chunk, self._half[:, t_begin:t_end])
+
+    def ner_rows(self, gh_recv, in_tchunk, row_begin, row_end, z_block, stream=0):
+        rm = self.row_starts[self.rank + 1] - self.row_starts[self.rank]
+        chunks = self._c(gh_recv).reshape(self.T // in_tchunk, rm, in_tchunk)
+        rows = np.concatenate(list(chunks), axis=1)[row_begin:row_end]  # (rows, T), time chunk k = t // in_tchunk
+        r0 = self.row_starts[self.rank] + row_begin
+        fh = O.fhat_rows(rows.astype(np.complex128), self.j2[r0:r0 + row_end - row_begin], self.T, self.spec)
+        z = np.fft.ifft(fh, axis=-1) * self.T / (self.N0 * self.N1 * self.T)
+        self._put(z_block, np.stack([z[:, q * self.Tr:(q + 1) * self.Tr] for q in range(self.world)]))
+
     def forward(self, samples_slice, gh_send, stream=0):
+        self._put(gh_send, self._forward_half(samples_slice))
+
+    def _forward_half(self, samples_slice):
         s = samples_slice.detach().cpu().numpy().astype(np.float64) * self.scale[:, None]
         gh = O.NedOracle(self.dims, *self.spec).execute(self.gpos, s.astype(np.complex128), wrapped=True)
         b = gh
@@ -69,8 +89,7 @@ class NumpyStages:
         sym = 0.5 * (gh + np.conj(b))
         if self.nlat == 1:
             sym = sym[None]
-        half = sym[:, : self.N1h, :].reshape(self.rows_total, self.Tr) * self.sign[:, None]
-        self._put(gh_send, half)
+        return sym[:, : self.N1h, :].reshape(self.rows_total, self.Tr) * self.sign[:, None]
 
     def ner(self, gh_recv, z_send, stream=0):
         rm = self.row_starts[self.rank + 1] - self.row_starts[self.rank]

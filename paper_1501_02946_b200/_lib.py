@@ -61,6 +61,9 @@ _SIGS = {
     "patfft_nedner_shard_forward": (ctypes.c_int, [_P, _P, _P, _P]),
     "patfft_nedner_shard_ner": (ctypes.c_int, [_P, _P, _P, _P]),
     "patfft_nedner_shard_inverse": (ctypes.c_int, [_P, _P, _P, _P]),
+    "patfft_nedner_shard_spread": (ctypes.c_int, [_P, _P, _P]),
+    "patfft_nedner_shard_lateral": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, _P]),
+    "patfft_nedner_shard_ner_rows": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P]),
     "patfft_ner_plan_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                               ctypes.c_double, ctypes.c_int, ctypes.POINTER(_P)]),
     "patfft_ner_plan_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),

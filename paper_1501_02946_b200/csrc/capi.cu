@@ -899,6 +899,8 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   L.Y = P->d_Y;
   L.ys = T;
   L.yt0 = 0;
+  L.gs = T;
+  L.gt0 = 0;
   L.gh = P->d_gh;
   L.tw = P->d_tw;
   L.dp0 = P->d_dp0;
@@ -1030,6 +1032,70 @@ int patfft_nedner_shard_forward(patfft_nedner_plan* P, const float* samples_slic
   CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
   return enqueue_forward(P, samples_slice, static_cast<float2*>(gh_send), st, true, false);
+}
+
+int patfft_nedner_shard_spread(patfft_nedner_plan* P, const float* samples_slice, void* stream) {
+  if (!P || !samples_slice) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  if (P->mode != 0) return fail(PATFFT_ERR_PARAMETER, "not a NEDNER plan");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+  SpreadParams sp;
+  sp.samples = samples_slice;
+  sp.recs = P->d_recs;
+  sp.blk = P->d_blk;
+  sp.blk_grp = P->d_blkgrp;
+  set_tc(P, sp);
+  sp.grid = P->d_grid;
+  sp.T = P->Tr;
+  sp.ncols = P->ncols;
+  sp.nrows = P->nrows;
+  sp.t_begin = 0;
+  sp.t_end = P->Tr;
+  CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
+  return PATFFT_OK;
+}
+
+int patfft_nedner_shard_lateral(patfft_nedner_plan* P, int t_begin, int t_end, void* gh_chunk, void* stream) {
+  if (!P || !gh_chunk) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  if (t_begin < 0 || t_end > P->Tr || t_begin >= t_end || (t_begin % 32) || ((t_end - t_begin) % 32 && t_end != P->Tr))
+    return fail(PATFFT_ERR_PARAMETER, "time range must be a non-empty multiple of 32 samples inside the local slice");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+  LateralParams L = P->lat;
+  L.gh = static_cast<float2*>(gh_chunk);
+  L.gs = t_end - t_begin;
+  L.gt0 = t_begin;
+  L.t_begin = t_begin;
+  L.t_end = t_end;
+  CUDA_TRY(launch_lateral_col(L, st));
+  CUDA_TRY(launch_lateral_row(L, st));
+  return PATFFT_OK;
+}
+
+int patfft_nedner_shard_ner_rows(patfft_nedner_plan* P, const void* gh_recv, int in_tchunk, int row_begin,
+                                 int row_end, void* z_block, void* stream) {
+  if (!P || !gh_recv || !z_block) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  if (row_begin < 0 || row_end > P->rows_mine || row_begin >= row_end)
+    return fail(PATFFT_ERR_PARAMETER, "row range outside the rank's rows");
+  if (in_tchunk < 1 || (in_tchunk & (in_tchunk - 1)) || P->T % in_tchunk)
+    return fail(PATFFT_ERR_PARAMETER, "input time chunk must be a power of two dividing N_t");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+  NerParams q = P->ner;
+  q.gh = static_cast<const float2*>(gh_recv);
+  q.z = static_cast<float2*>(z_block);
+  q.in_tchunk = in_tchunk;
+  q.in_tshift = in_tchunk == P->T && P->world == 1 ? 31 : ilog2(in_tchunk);
+  q.in_tmask = in_tchunk == P->T && P->world == 1 ? 0x7fffffff : in_tchunk - 1;
+  q.in_row_off = row_begin;
+  q.rows_launch = row_end - row_begin;
+  q.out_row0 = P->row_begin + row_begin;
+  q.rows_out = row_end - row_begin;
+  CUDA_TRY(launch_ner(q, P->K2t, P->poly_degree, st));
+  return PATFFT_OK;
 }
 
 int patfft_nedner_shard_ner(patfft_nedner_plan* P, const void* gh_recv, void* z_send, void* stream) {

@@ -209,9 +209,11 @@ __global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kerne
   const int q = tid & (P - 1);
   const int t = t0 + q;
   if (t >= p.t_end) return;
+  // gh: [N0][ny][gs] holding times [gt0, gt0 + gs) (the whole slice, or the
+  // time chunk one pipelined exchange of the sharded path sends)
   const int kstep = nth >> PLOG;
-  const size_t gstep = (size_t)kstep * p.ny * T;
-  float2* __restrict__ gp = p.gh + ((size_t)(tid >> PLOG) * p.ny + j1) * T + t;
+  const size_t gstep = (size_t)kstep * p.ny * p.gs;
+  float2* __restrict__ gp = p.gh + ((size_t)(tid >> PLOG) * p.ny + j1) * p.gs + (t - p.gt0);
   for (int j0w = tid >> PLOG; j0w < N0; j0w += kstep, gp += gstep) {
     const int a = (N0 > 1) ? (j0w < N0 / 2 ? j0w : j0w - N0) : 0;
     const bool nyq0 = (N0 > 1) && (a == -(N0 / 2));

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(ner_ct_threads(LOGT), ner_ct_minb(LOGT)) ner_k
   constexpr int CT_NTH = CT ? ner_ct_threads(LOGT) : 1;
   extern __shared__ float2 sbuf[];
   constexpr int K = K2 / 2;
-  const int rl = blockIdx.x;         // local row of the input array
+  const int rl = blockIdx.x + p.in_row_off;  // local row of the input array
   const int r = p.row0 + rl;         // global gh row: j0w * N1h + j1
   const int tid = threadIdx.x;
   const int nth = CT ? CT_NTH : (int)blockDim.x;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(ner_dct_threads(LOGT), ner_dct_minb(LOGT)) ner
   constexpr int N2 = 2 * T;
   constexpr int K = K2 / 2;
   extern __shared__ float2 sbuf[];
-  const int rl = blockIdx.x;
+  const int rl = blockIdx.x + p.in_row_off;
   const int r = p.row0 + rl;
   const int tid = threadIdx.x;
   const int tci = p.in_tchunk;
@@ -674,7 +674,7 @@ int ner_threads(int n_over) {
 cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
   int threads = ner_threads(p.n_over);
   const size_t smem = ner_smem_bytes(p.n_over, p.fused_ifft ? p.Tu : 0);
-  const unsigned rows = (unsigned)p.rows_local;
+  const unsigned rows = (unsigned)(p.rows_launch > 0 ? p.rows_launch : p.rows_local);
   cudaError_t err = cudaSuccess;
   auto go = [&](auto kern) {
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

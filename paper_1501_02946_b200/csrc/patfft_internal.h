@@ -81,6 +81,7 @@ struct LateralParams {
   int T, nrows, lrows, ncols, lcols, ny, N0, N1;
   int t_begin, t_end;  // forward kernels: time range processed by this launch
   int ys, yt0;         // Y time stride and the time stored at Y offset 0 (whole record: T, 0)
+  int gs, gt0;         // the same for gh
   int cplx;            // 1: NedPlan mode (complex values, full spectrum, no Hermitian fix-up)
   int centered;        // NedPlan output order
   // inverse
@@ -104,6 +105,7 @@ struct NerParams {
   // row / time layout (single GPU: row0 = out_row0 = 0, rows_local = N0*N1h,
   // rows_out = N0u*N1uh, in_tchunk = T, out_tchunk = Tu)
   int row0, rows_local, in_tchunk, in_tshift, in_tmask;
+  int in_row_off, rows_launch;  // rows [in_row_off, in_row_off + rows_launch) of the input (0, 0: all)
   int out_row0, rows_out, out_tchunk, out_tshift, out_tmask;
   double c_eff;        // n_over / (2T)
   float scale;         // 1/(N0*N1*T): scipy ifftn normalisation * up^d

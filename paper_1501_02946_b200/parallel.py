@@ -112,6 +112,19 @@ class GpuStages:
         _lib.check(self._lib.patfft_nedner_shard_inverse(self._h, ctypes.c_void_p(z_recv.data_ptr()),
                                                          ctypes.c_void_p(image_slice.data_ptr()), self._stream(stream)))
 
+    def spread(self, samples_slice, stream=0):
+        _lib.check(self._lib.patfft_nedner_shard_spread(self._h, ctypes.c_void_p(samples_slice.data_ptr()),
+                                                        self._stream(stream)))
+
+    def lateral(self, t_begin, t_end, gh_chunk, stream=0):
+        _lib.check(self._lib.patfft_nedner_shard_lateral(self._h, int(t_begin), int(t_end),
+                                                         ctypes.c_void_p(gh_chunk.data_ptr()), self._stream(stream)))
+
+    def ner_rows(self, gh_recv, in_tchunk, row_begin, row_end, z_block, stream=0):
+        _lib.check(self._lib.patfft_nedner_shard_ner_rows(self._h, ctypes.c_void_p(gh_recv.data_ptr()), int(in_tchunk),
+                                                          int(row_begin), int(row_end),
+                                                          ctypes.c_void_p(z_block.data_ptr()), self._stream(stream)))
+
     def close(self):
         if getattr(self, "_h", None):
             self._lib.patfft_nedner_plan_destroy(self._h)
@@ -124,17 +137,46 @@ class GpuStages:
             pass
 
 
+def _pow2_at_most(n, cap):
+    c = 1
+    while c * 2 <= min(n, cap):
+        c *= 2
+    return c
+
+
 class ShardedNedNer:
     """Reconstruct one record across all ranks of a torch.distributed group.
 
     Every rank builds the plan from the same sensor layout; ``run`` takes the
     rank's time slice ``samples[:, rank*Tr:(rank+1)*Tr]`` (a device tensor,
     float32) and returns the rank's depth slice of the image
-    ``image[..., rank*Tr:(rank+1)*Tr]``.
+    ``image[..., rank*Tr:(rank+1)*Tr]``.  The returned tensor is this object's
+    output buffer and is overwritten by the next ``run`` (pass ``out=`` to
+    keep results apart).
+
+    Schedule per rank (each exchange overlaps the compute that follows it):
+
+    1. spread the whole slice (one gridding launch: the tensor-core kernel
+       wants long time blocks);
+    2. lateral FFTs in ``time_chunks`` pieces of Tr / C samples; the
+       exchange of piece c (rows of every destination, one grouped NCCL
+       send/recv) runs while piece c + 1 is transformed;
+    3. NER in ``row_blocks`` blocks of the rank's rows; the exchange of block
+       b (its depth slices back to their owners) runs while block b + 1 is
+       interpolated;
+    4. lateral inverse of the rank's depth slice.
+
+    Receive buffers are laid out so that nothing is repacked: piece c from
+    rank q lands as time chunk q*C + c of ``[chunk][rows_mine][Tr/C]``, which
+    the NER kernel reads directly, and block b of rank q lands at its global
+    rows of ``[rows_total][Tr]``, which the inverse reads directly.  At world
+    size 1 there is no exchange and the buffers alias (the single-GPU
+    pipeline with three launches).
     """
 
     def __init__(self, positions, weights, n_time, dt, sound_speed, dx, n_lateral, out_dims=None,
-                 spec: WindowSpec | None = None, group=None, device=None, stages=None, torch_device=None):
+                 spec: WindowSpec | None = None, group=None, device=None, stages=None, torch_device=None,
+                 time_chunks=None, row_blocks=None):
         import torch
         import torch.distributed as dist
 
@@ -157,44 +199,112 @@ class ShardedNedNer:
             stages = GpuStages(positions, weights, n_time, dt, sound_speed, dx, n_lateral, dims, spec, self.rank,
                                self.world, torch_device.index)
         self.stages = stages
+        P = self.world
+        # pieces of Tr / C >= 32 samples (lateral kernels' time tile); none at world 1
+        self.C = C = (1 if P == 1 else _pow2_at_most(max(1, L.Tr // 32), 4)) if time_chunks is None else int(time_chunks)
+        if C < 1 or L.Tr % C or (C > 1 and (L.Tr // C) % 32) or (L.Tr // C) & (L.Tr // C - 1):
+            raise ValueError("time_chunks must split N_t / world into power-of-two pieces of >= 32 samples")
+        self.Trc = Trc = L.Tr // C
+        self.B = B = (1 if P == 1 else 4) if row_blocks is None else int(row_blocks)
         f32 = dict(dtype=torch.float32, device=torch_device)
         rm = L.rows(self.rank)
-        self.gh_send = torch.empty(L.rows_total * L.Tr * 2, **f32)
-        self.gh_recv = torch.empty(self.world * rm * L.Tr * 2, **f32)
-        self.z_send = torch.empty(self.world * rm * L.Tr * 2, **f32)
-        self.z_recv = torch.empty(L.rows_total * L.Tr * 2, **f32)
+        self.rm = rm
+        # a block partition every rank computes the same way for every rank's rows
+        self.bounds = [[b * L.rows(q) // B for b in range(B + 1)] for q in range(P)]
+        if min(self.bounds[self.rank][b + 1] - self.bounds[self.rank][b] for b in range(B)) < 1:
+            raise ValueError("more row blocks than rows on a rank")
+        self.gh_send = torch.empty(C * L.rows_total * Trc * 2, **f32)       # [c][rows_total][Trc]
+        self.gh_recv = self.gh_send if P == 1 else torch.empty(P * C * rm * Trc * 2, **f32)  # [q*C+c][rm][Trc]
+        self.z_send = torch.empty(P * rm * L.Tr * 2, **f32)                 # per block b: [q][rows_b][Tr]
+        self.z_recv = self.z_send if (P == 1 and B == 1) else torch.empty(L.rows_total * L.Tr * 2, **f32)
         self.image = torch.empty(L.image_slice_shape(), **f32)
-        self.send1 = [L.rows(q) * L.Tr * 2 for q in range(self.world)]
-        self.recv1 = [rm * L.Tr * 2] * self.world
-        self.send2 = self.recv1
-        self.recv2 = self.send1
         # A dedicated (non-default) stream: the C stages treat a NULL stream as
         # "the plan's own stream", which would not be ordered with torch's
         # legacy default stream.
         self.cuda_stream = torch.cuda.Stream(device=torch_device) if torch_device.type == "cuda" else None
 
-    def run(self, samples_slice):
+    # ---- buffer views ----------------------------------------------------
+    def _gh_send_chunk(self, c):
+        n = self.layout.rows_total * self.Trc * 2
+        return self.gh_send[c * n:(c + 1) * n]
+
+    def _gh_send_rows(self, c, q):
+        L, w = self.layout, self.Trc * 2
+        return self._gh_send_chunk(c)[L.row_starts[q] * w:L.row_starts[q + 1] * w]
+
+    def _gh_recv_piece(self, q, c):
+        n = self.rm * self.Trc * 2
+        k = q * self.C + c
+        return self.gh_recv[k * n:(k + 1) * n]
+
+    def _z_block(self, b):
+        L = self.layout
+        b0 = self.bounds[self.rank][b]
+        return self.z_send[self.world * b0 * L.Tr * 2:self.world * self.bounds[self.rank][b + 1] * L.Tr * 2]
+
+    def _z_block_dst(self, b, q):
+        L = self.layout
+        nb = self.bounds[self.rank][b + 1] - self.bounds[self.rank][b]
+        return self._z_block(b)[q * nb * L.Tr * 2:(q + 1) * nb * L.Tr * 2]
+
+    def _z_recv_rows(self, b, q):
+        L = self.layout
+        r0 = L.row_starts[q] + self.bounds[q][b]
+        r1 = L.row_starts[q] + self.bounds[q][b + 1]
+        return self.z_recv[r0 * L.Tr * 2:r1 * L.Tr * 2]
+
+    def _exchange(self, pairs):
+        """One grouped exchange: pairs[q] = (send view to rank q, recv view from rank q)."""
+        dist = self.dist
+        snd, rcv = pairs[self.rank]
+        rcv.copy_(snd)  # own share: a device copy on the compute stream
+        ops = []
+        for q, (sv, rv) in enumerate(pairs):
+            if q == self.rank:
+                continue
+            ops.append(dist.P2POp(dist.isend, sv, q, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, rv, q, group=self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    # ---- one reconstruction ----------------------------------------------
+    def run(self, samples_slice, out=None):
         """Enqueue one sharded reconstruction; returns this rank's image slice.
 
         Work is ordered after everything already queued on the caller's current
         stream and the caller's stream waits for the result.
         """
         if self.cuda_stream is None:
-            return self._run(samples_slice, 0)
-        torch = self.torch
-        cur = torch.cuda.current_stream(self.tdev)
-        self.cuda_stream.wait_stream(cur)
-        with torch.cuda.stream(self.cuda_stream):
-            out = self._run(samples_slice, self.cuda_stream.cuda_stream)
-        cur.wait_stream(self.cuda_stream)
-        return out
+            img = self._run(samples_slice, 0)
+        else:
+            torch = self.torch
+            cur = torch.cuda.current_stream(self.tdev)
+            self.cuda_stream.wait_stream(cur)
+            with torch.cuda.stream(self.cuda_stream):
+                img = self._run(samples_slice, self.cuda_stream.cuda_stream)
+            cur.wait_stream(self.cuda_stream)
+        if out is not None:
+            out.copy_(img)
+            return out
+        return img
 
     def _run(self, samples_slice, s):
-        self.stages.forward(samples_slice, self.gh_send, s)
-        self.dist.all_to_all_single(self.gh_recv, self.gh_send, output_split_sizes=self.recv1,
-                                    input_split_sizes=self.send1, group=self.group)
-        self.stages.ner(self.gh_recv, self.z_send, s)
-        self.dist.all_to_all_single(self.z_recv, self.z_send, output_split_sizes=self.recv2,
-                                    input_split_sizes=self.send2, group=self.group)
-        self.stages.inverse(self.z_recv, self.image, s)
+        L, P, C, B = self.layout, self.world, self.C, self.B
+        st = self.stages
+        st.spread(samples_slice, s)
+        works = []
+        for c in range(C):
+            st.lateral(c * self.Trc, (c + 1) * self.Trc, self._gh_send_chunk(c), s)
+            if P > 1:  # piece c to every row owner while piece c + 1 is transformed
+                works += self._exchange([(self._gh_send_rows(c, q), self._gh_recv_piece(q, c)) for q in range(P)])
+        for w in works:
+            w.wait()
+        works = []
+        for b in range(B):
+            b0, b1 = self.bounds[self.rank][b], self.bounds[self.rank][b + 1]
+            st.ner_rows(self.gh_recv, self.Trc, b0, b1, self._z_block(b), s)
+            if self.z_recv is not self.z_send:  # block b back to the depth owners while b + 1 runs
+                works += self._exchange([(self._z_block_dst(b, q), self._z_recv_rows(b, q)) for q in range(P)])
+        for w in works:
+            w.wait()
+        st.inverse(self.z_recv, self.image, s)
         return self.image

@@ -63,3 +63,57 @@ def test_sharded_plan_rejects_unsupported_shapes():
     with pytest.raises(pb.DeviceError):
         GpuStages(rec.positions, rec.weights, 96, rec.dt, rec.sound_speed, rec.dx, (16, 16), (16, 16),
                   pb.WindowSpec(), 0, 4, 0)
+
+
+@pytest.mark.parametrize("world,chunks,blocks", [(2, 2, 3), (4, 2, 4), (8, 1, 2)])
+def test_pipelined_shard_stages_match_single_gpu(world, chunks, blocks):
+    """The pipelined stage entry points (whole-slice spread, lateral FFTs in time
+    pieces, NER in row blocks) with the exchange layouts of parallel.ShardedNedNer,
+    ranks emulated one after another on one GPU: bit-identical to one GPU."""
+    import torch
+
+    from paper_1501_02946_b200.parallel import GpuStages, ShardLayout
+
+    rec = synth.make_3d(50 + world, 64, 256, 20e-9, "clustered", 3, sigma=2e-3)
+    want = pb.reconstruct_nedner(rec.as_record()).values
+    nl = tuple(rec.n_lateral)
+    T = rec.samples.shape[1]
+    L = ShardLayout(2, nl, T, world)
+    C, Trc = chunks, L.Tr // chunks
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    s = stream.cuda_stream
+    stages = [GpuStages(rec.positions, rec.weights, T, rec.dt, rec.sound_speed, rec.dx, nl, nl, pb.WindowSpec(), q,
+                        world, 0) for q in range(world)]
+    samples = torch.tensor(rec.samples, dtype=torch.float32, device=dev)
+    f32 = dict(dtype=torch.float32, device=dev)
+    rs = L.row_starts
+    # rank p: pieces gh_send[p][c] = [rows_total][Trc]
+    gh_send = [[torch.empty(L.rows_total * Trc * 2, **f32) for _ in range(C)] for _ in range(world)]
+    for p in range(world):
+        stages[p].spread(samples[:, p * L.Tr:(p + 1) * L.Tr].contiguous(), s)
+        for c in range(C):
+            stages[p].lateral(c * Trc, (c + 1) * Trc, gh_send[p][c], s)
+    # rank q receives piece c of rank p as time chunk p*C + c of [chunk][rows_q][Trc]
+    gh_recv = [torch.cat([gh_send[p][c].view(L.rows_total, Trc * 2)[rs[q]:rs[q + 1]].reshape(-1)
+                          for p in range(world) for c in range(C)]) for q in range(world)]
+    bounds = [[b * L.rows(q) // blocks for b in range(blocks + 1)] for q in range(world)]
+    z_recv = [torch.empty(L.rows_total * L.Tr * 2, **f32) for _ in range(world)]
+    for p in range(world):
+        for b in range(blocks):
+            b0, b1 = bounds[p][b], bounds[p][b + 1]
+            zb = torch.empty(world * (b1 - b0) * L.Tr * 2, **f32)
+            stages[p].ner_rows(gh_recv[p], Trc, b0, b1, zb, s)
+            for q in range(world):  # block b of rank p -> its global rows on rank q
+                r0, r1 = rs[p] + b0, rs[p] + b1
+                z_recv[q][r0 * L.Tr * 2:r1 * L.Tr * 2].copy_(zb.view(world, -1)[q])
+    imgs = [torch.empty(L.image_slice_shape(), **f32) for _ in range(world)]
+    for q in range(world):
+        stages[q].inverse(z_recv[q], imgs[q], s)
+    torch.cuda.synchronize()
+    got = torch.cat(imgs, dim=-1).double().cpu().numpy()
+    torch.cuda.set_stream(torch.cuda.default_stream(dev))
+    err = rel_l2(got, want)
+    print(f"pipelined world {world} (pieces {C}, row blocks {blocks}): rel-L2 vs single GPU {err:.2e}")
+    assert err <= 1e-6

@@ -26,7 +26,17 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, outdir):
+def _case(case):
+    from paper_1501_02946_b200 import synth
+
+    if case == "3d":
+        return synth.make_3d(31, 16, 32, 20e-9, "uniform", 2)
+    if case == "3d_long":  # N_t / world = 128: four 32-sample pieces per exchange
+        return synth.make_3d(33, 16, 256, 20e-9, "jittered", 2)
+    return synth.make_2d(seed=32, n=32, nt=256)
+
+
+def _worker(rank, world, port, case, outdir, chunks=None, blocks=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -36,12 +46,13 @@ def _worker(rank, world, port, case, outdir):
         from paper_1501_02946_b200.parallel import ShardedNedNer
         from paper_1501_02946_b200 import synth
 
-        rec = synth.make_3d(31, 16, 32, 20e-9, "uniform", 2) if case == "3d" else synth.make_2d(seed=32, n=32, nt=256)
+        rec = _case(case)
         spec = WindowSpec()
         stages = NumpyStages(rec.positions, rec.weights, rec.samples.shape[1], rec.dt, rec.sound_speed, rec.dx,
                              rec.n_lateral, tuple(rec.n_lateral), spec, rank, world)
         sh = ShardedNedNer(rec.positions, rec.weights, rec.samples.shape[1], rec.dt, rec.sound_speed, rec.dx,
-                           rec.n_lateral, stages=stages, torch_device=torch.device("cpu"))
+                           rec.n_lateral, stages=stages, torch_device=torch.device("cpu"), time_chunks=chunks,
+                           row_blocks=blocks)
         tr = sh.layout.Tr
         sl = torch.tensor(np.ascontiguousarray(rec.samples[:, rank * tr:(rank + 1) * tr]), dtype=torch.float32)
         img = sh.run(sl)
@@ -50,14 +61,20 @@ def _worker(rank, world, port, case, outdir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,case", [(2, "3d"), (4, "3d"), (2, "2d")])
-def test_sharded_pipeline_gloo_matches_oracle(tmp_path, world, case):
+@pytest.mark.parametrize("world,case,chunks,blocks", [(2, "3d", None, None), (4, "3d", None, None),
+                                                     (8, "3d", None, None), (2, "2d", None, None),
+                                                     (1, "3d", None, None), (2, "3d", 1, 1), (4, "3d", 1, 3),
+                                                     (2, "3d_long", None, None), (2, "3d_long", 2, 5)])
+def test_sharded_pipeline_gloo_matches_oracle(tmp_path, world, case, chunks, blocks):
+    """The pipelined schedule (time pieces exchanged while the next piece is
+    transformed, NER row blocks exchanged while the next block runs) over real
+    gloo processes; every (pieces, blocks) split gives the oracle volume."""
     from oracle import nedner_oracle as O
     from paper_1501_02946_b200 import synth
 
-    mp.spawn(_worker, args=(world, _free_port(), case, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), case, str(tmp_path), chunks, blocks), nprocs=world, join=True)
     got = np.concatenate([np.load(tmp_path / f"slice{r}.npy") for r in range(world)], axis=-1)
-    rec = synth.make_3d(31, 16, 32, 20e-9, "uniform", 2) if case == "3d" else synth.make_2d(seed=32, n=32, nt=256)
+    rec = _case(case)
     want, _ = O.reconstruct_nedner(rec.positions, rec.weights, rec.samples, rec.dt, rec.sound_speed, rec.dx,
                                    rec.n_lateral)
     assert got.shape == want.shape
