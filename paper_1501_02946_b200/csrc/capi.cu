@@ -800,6 +800,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     }
   }
   if ((rc = dalloc(&P->d_Y, (size_t)nrows * P->N1h * T))) return rc;
+  if ((rc = dalloc(&P->d_lat_flags, 2 * ((size_t)T / 32 + 2)))) return rc;
   if (world == 1) {
     if ((rc = dalloc(&P->d_gh, (size_t)P->N0 * P->N1h * T))) return rc;
     if ((rc = dalloc(&P->d_z, (size_t)P->N0u * P->N1uh * P->Tu))) return rc;
@@ -897,6 +898,9 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   LateralParams& L = P->lat;
   L.grid = P->d_grid;
   L.Y = P->d_Y;
+  L.f_flags = P->d_lat_flags;
+  L.f_chunks = L.f_slots = 0;
+  L.y_capacity = T;
   L.ys = T;
   L.yt0 = 0;
   L.gs = T;
@@ -1069,8 +1073,7 @@ int patfft_nedner_shard_lateral(patfft_nedner_plan* P, int t_begin, int t_end, v
   L.gt0 = t_begin;
   L.t_begin = t_begin;
   L.t_end = t_end;
-  CUDA_TRY(launch_lateral_col(L, st));
-  CUDA_TRY(launch_lateral_row(L, st));
+  CUDA_TRY(launch_lateral_forward(L, st));
   return PATFFT_OK;
 }
 
@@ -1175,14 +1178,18 @@ static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* 
       for (int tb = 0; tb < T; tb += lc) {
         L.t_begin = L.yt0 = tb;
         L.t_end = std::min(T, tb + lc);
-        CUDA_TRY(launch_lateral_col(L, st));
-        CUDA_TRY(launch_lateral_row(L, st));
+        CUDA_TRY(launch_lateral_forward(L, st));
       }
       return PATFFT_OK;
     }
-    CUDA_TRY(launch_lateral_col(L, st));
-    if (prof) CUDA_TRY(cudaEventRecord(P->ev[2], st));
-    CUDA_TRY(launch_lateral_row(L, st));
+    if (lateral_fused_supported(L)) {  // one launch: its time is reported as lateral_col, lateral_row = 0
+      CUDA_TRY(launch_lateral_forward(L, st));
+      if (prof) CUDA_TRY(cudaEventRecord(P->ev[2], st));
+    } else {
+      CUDA_TRY(launch_lateral_col(L, st));
+      if (prof) CUDA_TRY(cudaEventRecord(P->ev[2], st));
+      CUDA_TRY(launch_lateral_row(L, st));
+    }
     if (prof) CUDA_TRY(cudaEventRecord(P->ev[3], st));
     return PATFFT_OK;
   }
@@ -1203,8 +1210,7 @@ static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* 
     L.t_begin = k * chunk;
     L.t_end = std::min(T, L.t_begin + chunk);
     CUDA_TRY(cudaStreamWaitEvent(P->stream2, P->ev_chunk[k], 0));
-    CUDA_TRY(launch_lateral_col(L, P->stream2));
-    CUDA_TRY(launch_lateral_row(L, P->stream2));
+    CUDA_TRY(launch_lateral_forward(L, P->stream2));
   }
   CUDA_TRY(cudaEventRecord(P->ev_join, P->stream2));
   CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
@@ -1381,8 +1387,7 @@ static int execute_host_devconvert(patfft_nedner_plan* P, const double* samples,
       sp.t_begin = L.t_begin = tb;
       sp.t_end = L.t_end = te;
       CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
-      CUDA_TRY(launch_lateral_col(L, st));
-      CUDA_TRY(launch_lateral_row(L, st));
+      CUDA_TRY(launch_lateral_forward(L, st));
     }
     L.t_begin = 0;
     L.t_end = T;
@@ -1428,8 +1433,7 @@ static int enqueue_forward_chunk(patfft_nedner_plan* P, int tb, int te, cudaStre
   L.t_begin = tb;
   L.t_end = te;
   CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
-  CUDA_TRY(launch_lateral_col(L, st));
-  CUDA_TRY(launch_lateral_row(L, st));
+  CUDA_TRY(launch_lateral_forward(L, st));
   return PATFFT_OK;
 }
 
@@ -1805,7 +1809,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->copy_out_stream) cudaStreamDestroy(P->copy_out_stream);
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
-  for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_gh,
+  for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_lat_flags, (void*)P->d_gh,
                   (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_tc_recs, (void*)P->d_tc_tiles, (void*)P->d_tc_counter, (void*)P->d_tc_a16, (void*)P->d_tc_off, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_pre, (void*)P->d_tw, (void*)P->d_jt0,
                   (void*)P->d_jt1})

@@ -340,7 +340,10 @@ __device__ __forceinline__ float2 last_pass_output(const float2* __restrict__ bu
 // `stride` float2 apart.  The first pass then loads an item's radix-2^R
 // elements, and the last pass stores them, from one base pointer with a
 // running offset instead of recomputing every address.
-template <class F, bool STREAM>
+// MODE: 0 = default caching, 1 = streaming (evict-first, 256-byte L2 prefetch),
+// 2 = L2-coherent (bypasses L1: rows another CTA of the same launch has just
+// written), 3 = streaming with a 128-byte L2 prefetch
+template <class F, int MODE>
 struct RowsLd {
   F ptr;
   size_t stride;
@@ -350,8 +353,8 @@ struct RowsSt {
   F ptr;
   size_t stride;
 };
-template <bool STREAM = true, class F>
-__device__ __forceinline__ RowsLd<F, STREAM> rows_ld(F f, size_t stride) {
+template <int MODE = 1, class F>
+__device__ __forceinline__ RowsLd<F, MODE> rows_ld(F f, size_t stride) {
   return {f, stride};
 }
 template <class F>
@@ -393,13 +396,23 @@ __device__ __forceinline__ float2 ld_keep(const float2* a) {
   return *a;
 #endif
 }
-template <int R, int L, class F, bool STREAM>
-__device__ __forceinline__ void load_items(float2 (&e)[1 << R], int nat0, int p, const RowsLd<F, STREAM>& rl) {
+__device__ __forceinline__ float2 ld_stream128(const float2* a) {
+  float2 v;
+  asm volatile("ld.global.cs.L2::128B.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+  return v;
+}
+__device__ __forceinline__ float2 ld_l2(const float2* a) {
+  float2 v;
+  asm volatile("ld.global.cg.L2::256B.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+  return v;
+}
+template <int R, int L, class F, int MODE>
+__device__ __forceinline__ void load_items(float2 (&e)[1 << R], int nat0, int p, const RowsLd<F, MODE>& rl) {
   const float2* b = rl.ptr(nat0, p);
   const size_t st = rl.stride << (L - R);
   if (b) {
 #pragma unroll
-    for (int k = 0; k < (1 << R); ++k) e[brev_c(k, R)] = STREAM ? ld_stream(b + k * st) : ld_keep(b + k * st);
+    for (int k = 0; k < (1 << R); ++k) e[brev_c(k, R)] = MODE == 3 ? ld_stream128(b + k * st) : MODE == 2 ? ld_l2(b + k * st) : MODE == 1 ? ld_stream(b + k * st) : ld_keep(b + k * st);
   } else {
 #pragma unroll
     for (int k = 0; k < (1 << R); ++k) e[k] = make_float2(0.f, 0.f);

@@ -75,13 +75,30 @@ constexpr int nth_for(int L, int PLOG) {
 constexpr int inv_lb_threads(int PLOG, int LC) { return LC > 0 ? nth_for(LC, PLOG) : 512; }
 constexpr int inv_lb_minb(int PLOG, int LC) { return inv_lb_threads(PLOG, LC) <= 256 ? PATFFT_LB_INV_MINB256 : 2; }
 
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// One column-FFT tile: grid row u0, packed time pairs [t0, t0 + 2P) -> Y (time
+// stride ys, time yt0 at offset 0).  `before_store` runs (all threads) between
+// the transform and the first write to Y.
 // LC > 0: compile-time transform length 2^LC (launched with nth_for(LC, PLOG) threads)
-template <int PLOG, int LC>
-__global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kernel(const LateralParams p) {
-  extern __shared__ float2 sm[];
+#ifndef PATFFT_FUSED_NOGRID
+#define PATFFT_FUSED_NOGRID 0  // diagnosis: the fused kernel's column tiles transform zeros instead of reading the grid
+#endif
+#ifndef PATFFT_FUSED_GRIDLD
+#define PATFFT_FUSED_GRIDLD 3  // fused kernel: grid row loads (fft::RowsLd mode)
+#endif
+#ifndef PATFFT_FUSED_FENCEALL
+#define PATFFT_FUSED_FENCEALL 0
+#endif
+#ifndef PATFFT_FUSED_GHCS
+#define PATFFT_FUSED_GHCS 1    // fused kernel: gh stored with the streaming (evict-first) hint
+#endif
+template <int PLOG, int LC, int GMODE = 1, class Hook>
+__device__ __forceinline__ void colfft_body(const LateralParams& p, float2* __restrict__ sm, int u0, int t0,
+                                            float2* __restrict__ Y, int ys, int yt0, Hook before_store) {
   constexpr int P = 1 << PLOG;
-  const int u0 = lat_line();
-  const int t0 = p.t_begin + lat_ttile() * 2 * P;
   const int tid = threadIdx.x;
   const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.T, n = p.ncols;
@@ -95,8 +112,9 @@ __global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kerne
   constexpr bool FUSED = PATFFT_LAT_FUSED && LC > 0 && LLAST > 0;
   if constexpr (LC > 0 && PATFFT_LAT_ROWPTR) {
     fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(
-        sm, p.tw, tid, fft::TileC<PLOG>(), fft::rows_ld([&](int row, int q) -> const float2* {
+        sm, p.tw, tid, fft::TileC<PLOG>(), fft::rows_ld<GMODE>([&](int row, int q) -> const float2* {
           const int t = t0 + 2 * q;
+          if (PATFFT_FUSED_NOGRID && GMODE != 1) return nullptr;
           return t < p.t_end ? reinterpret_cast<const float2*>(src + (size_t)row * T + t) : nullptr;
         }, (size_t)(T / 2)));
   } else if constexpr (LC > 0) {
@@ -114,11 +132,12 @@ __global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kerne
         sm, p.tw, fft::TileC<PLOG>(), k, q);
     else return sm[ad(k, q)];
   };
+  before_store();
   if (p.cplx) {
     // complex values (NedPlan): the packed pair IS one complex sample; keep
     // the full cropped spectrum j1 in [-N1/2, N1/2) in wrapped order
     const int Tc = T / 2;
-    float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * Tc;
+    float2* __restrict__ dst = Y + (size_t)u0 * p.ny * Tc;
     for (int i = tid; i < p.ny * P; i += nth) {
       const int k = i >> PLOG, q = i & (P - 1);
       const int t = t0 + 2 * q;
@@ -130,15 +149,14 @@ __global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kerne
   }
   // Y: [nrows][ny][ys] holding times [yt0, yt0 + ys) (the whole record, or a
   // time chunk that stays L2-resident until rowfft consumes it)
-  const int ys = p.ys;
-  float2* __restrict__ dst = p.Y + (size_t)u0 * p.ny * ys;
+  float2* __restrict__ dst = Y + (size_t)u0 * p.ny * ys;
   // each thread keeps one packed time pair q (nth is a multiple of P) and walks the bins k
   const int q = tid & (P - 1);
   const int t = t0 + 2 * q;
   if (t >= p.t_end) return;
   const int kstep = nth >> PLOG;
   const size_t ostep = (size_t)kstep * ys;
-  float2* __restrict__ o = dst + (size_t)(tid >> PLOG) * ys + (t - p.yt0);
+  float2* __restrict__ o = dst + (size_t)(tid >> PLOG) * ys + (t - yt0);
   for (int k = tid >> PLOG; k < p.ny; k += kstep, o += ostep) {
     const float2 zk = zat(k, q);
     const float2 zm = fft::conjf2(zat((n - k) & (n - 1), q));
@@ -149,17 +167,23 @@ __global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kerne
 }
 
 template <int PLOG, int LC>
-__global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kernel(const LateralParams p) {
+__global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) colfft_kernel(const LateralParams p) {
   extern __shared__ float2 sm[];
+  colfft_body<PLOG, LC>(p, sm, lat_line(), p.t_begin + lat_ttile() * (2 << PLOG), p.Y, p.ys, p.yt0, NoHook());
+}
+
+// One row-FFT tile: half-spectrum column j1, time samples [t0, t0 + P) of Y
+// (time stride ys, time yt0 at offset 0) -> gh.  YMODE: how Y is loaded
+// (fft::RowsLd; 2 when other CTAs of the same launch wrote it).
+template <int PLOG, int LC, int YMODE>
+__device__ __forceinline__ void rowfft_body(const LateralParams& p, float2* __restrict__ sm, int j1, int t0,
+                                            const float2* __restrict__ Y, int ys, int yt0) {
   constexpr int P = 1 << PLOG;
-  const int j1 = lat_line();
-  const int t0 = p.t_begin + lat_ttile() * P;
   const int tid = threadIdx.x;
   const int nth = LC > 0 ? nth_for(LC, PLOG) : (int)blockDim.x;
   const int T = p.T, nr = p.nrows;
   const TileAddr ad{PLOG};
-  const int ys = p.ys;
-  const float2* __restrict__ yb = p.Y - p.yt0;
+  const float2* __restrict__ yb = Y - yt0;
   auto ld = [&](int row, int q) {
     const int t = t0 + q;
     return (t < p.t_end) ? __ldcs(yb + ((size_t)row * p.ny + j1) * ys + t) : make_float2(0.f, 0.f);
@@ -168,7 +192,7 @@ __global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kerne
   constexpr bool FUSED = PATFFT_ROW_FUSED && LC > 0 && LLAST > 0;
   if constexpr (LC > 0 && PATFFT_LAT_ROWPTR) {
     fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(
-        sm, p.tw, tid, fft::TileC<PLOG>(), fft::rows_ld([&](int row, int q) -> const float2* {
+        sm, p.tw, tid, fft::TileC<PLOG>(), fft::rows_ld<YMODE>([&](int row, int q) -> const float2* {
           const int t = t0 + q;
           return t < p.t_end ? yb + ((size_t)row * p.ny + j1) * ys + t : nullptr;
         }, (size_t)p.ny * ys));
@@ -227,7 +251,72 @@ __global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kerne
     } else {
       v = zat(a & mask, q);
     }
-    *gp = fft::cscale(v, __ldg(&p.dp0[j0w]) * dp1);
+    const float2 g = fft::cscale(v, __ldg(&p.dp0[j0w]) * dp1);
+    if (YMODE == 2 && PATFFT_FUSED_GHCS) __stcs(gp, g);
+    else *gp = g;
+  }
+}
+
+template <int PLOG, int LC>
+__global__ void __launch_bounds__(PATFFT_LB_ROW_T, PATFFT_LB_ROW_B) rowfft_kernel(const LateralParams p) {
+  extern __shared__ float2 sm[];
+  rowfft_body<PLOG, LC, 1>(p, sm, lat_line(), p.t_begin + lat_ttile() * (1 << PLOG), p.Y, p.ys, p.yt0);
+}
+
+// ---------------------------------------------------------------------------
+// Column and row FFTs in ONE launch, so the column-transformed half spectrum Y
+// never travels to HBM: the time axis is cut into chunks of 2P samples (one
+// column-FFT tile); CTAs are laid out in rounds
+//   round r = [column tiles of chunk r (nrows CTAs)] [row tiles of chunk r - 1 (2 ny CTAs)]
+// and Y is a ring of kYSlots chunk buffers (nrows x ny x 2P each, 17 MB at
+// cfg4) that stays L2-resident.  A row tile waits until all column tiles of
+// its chunk have signalled; a column tile waits, just before it stores, until
+// the row tiles that read its ring slot kYSlots chunks earlier have finished.
+// Both dependencies point to CTAs with lower block indices -- dispatched
+// earlier, hence resident or complete -- so the waits cannot deadlock.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void lat_wait(const int* flag, int need) {
+  if (threadIdx.x == 0) {
+    int v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      if (v >= need) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+// (release by one thread after the CTA barrier: cumulative over the other threads' stores)
+__device__ __forceinline__ void lat_signal(int* flag) {
+#if PATFFT_FUSED_FENCEALL
+  __threadfence();
+#endif
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(flag) : "memory");
+}
+
+template <int PLOG, int L>
+__global__ void __launch_bounds__(PATFFT_LB_COL_T, PATFFT_LB_COL_B) latfused_kernel(const LateralParams p) {
+  extern __shared__ float2 sm[];
+  constexpr int P = 1 << PLOG;
+  const int nc = p.nrows, nr = 2 * p.ny, per = nc + nr;
+  const int round = blockIdx.x / per, idx = blockIdx.x - round * per;
+  const size_t slot = (size_t)p.nrows * p.ny * (2 * P);
+  if (idx < nc) {
+    const int c = round;
+    if (c >= p.f_chunks) return;
+    const int t0 = p.t_begin + c * 2 * P;
+    colfft_body<PLOG, L, PATFFT_FUSED_GRIDLD>(p, sm, idx, t0, p.Y + (size_t)(c % p.f_slots) * slot, 2 * P, t0, [&]() {
+      if (c >= p.f_slots) lat_wait(p.f_flags + p.f_chunks + (c - p.f_slots), nr);
+    });
+    lat_signal(p.f_flags + c);
+  } else {
+    const int c = round - 1;
+    if (c < 0) return;
+    const int tc = p.t_begin + c * 2 * P, i = idx - nc;
+    lat_wait(p.f_flags + c, nc);
+    rowfft_body<PLOG, L, 2>(p, sm, i >> 1, tc + (i & 1) * P, p.Y + (size_t)(c % p.f_slots) * slot, 2 * P, tc);
+    lat_signal(p.f_flags + p.f_chunks + c);
   }
 }
 
@@ -426,6 +515,54 @@ cudaError_t launch_lateral_col(const LateralParams& p, cudaStream_t s) {
 
 cudaError_t launch_lateral_row(const LateralParams& p, cudaStream_t s) {
   return launch_rowfft(p, p.nrows, dim3((unsigned)p.ny, (unsigned)(p.t_end - p.t_begin)), 1, s);
+}
+
+// Column + row FFTs of [t_begin, t_end): the two kernels with the whole Y in
+// between, or (opt-in, PATFFT_LAT_FUSED_SLOTS) the single-launch form
+// (latfused_kernel) for square oversampled planes of 128 / 256 / 512 points a side.
+namespace {
+// Ring slots of the single-launch form; 0 (default) = the two-kernel form.  Measured at cfg4
+// (DESIGN.md 4): the single launch keeps Y in L2 (DRAM traffic of the lateral stage 2.37 ->
+// 1.39 GB) but takes 0.606 ms against 0.532 ms -- both forms are bound by the latency of
+// their shared-memory passes at 2 CTAs per SM, not by HBM.  Read per launch (tests toggle it).
+int fused_slots() {
+  const char* e = std::getenv("PATFFT_LAT_FUSED_SLOTS");
+  return e ? std::max(0, std::min(16, std::atoi(e))) : 0;
+}
+}  // namespace
+
+bool lateral_fused_supported(const LateralParams& p) {
+  const int len = p.t_end - p.t_begin;
+  return fused_slots() > 0 && p.f_flags && !p.cplx && p.nrows == p.ncols &&
+         (p.nrows == 128 || p.nrows == 256 || p.nrows == 512) && plog_for(p.nrows) == 4 && len >= 64 &&
+         (int64_t)std::min(fused_slots(), (len + 31) / 32) * 32 <= (int64_t)p.y_capacity;
+}
+
+cudaError_t launch_lateral_forward(const LateralParams& p0, cudaStream_t s) {
+  if (!lateral_fused_supported(p0)) {
+    cudaError_t e = launch_lateral_col(p0, s);
+    return e != cudaSuccess ? e : launch_lateral_row(p0, s);
+  }
+  LateralParams p = p0;
+  p.f_chunks = (p.t_end - p.t_begin + 31) / 32;
+  p.f_slots = std::min(fused_slots(), p.f_chunks);
+  cudaError_t err = cudaMemsetAsync(p.f_flags, 0, sizeof(int) * 2 * (size_t)p.f_chunks, s);
+  if (err != cudaSuccess) return err;
+  const unsigned grid = (unsigned)((p.f_chunks + 1) * (p.nrows + 2 * p.ny));
+  const size_t smem = ((size_t)p.nrows << 4) * sizeof(float2);
+  auto run = [&](auto k, int thr) {
+    err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err == cudaSuccess) {
+      k<<<grid, thr, smem, s>>>(p);
+      err = cudaGetLastError();
+    }
+  };
+  switch (p.nrows) {
+    case 128: run(latfused_kernel<4, 7>, nth_for(7, 4)); break;
+    case 256: run(latfused_kernel<4, 8>, nth_for(8, 4)); break;
+    default: run(latfused_kernel<4, 9>, nth_for(9, 4)); break;
+  }
+  return err;
 }
 
 cudaError_t launch_lateral_inverse(const LateralParams& p, cudaStream_t s) {

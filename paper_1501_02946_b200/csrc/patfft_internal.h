@@ -82,6 +82,12 @@ struct LateralParams {
   int t_begin, t_end;  // forward kernels: time range processed by this launch
   int ys, yt0;         // Y time stride and the time stored at Y offset 0 (whole record: T, 0)
   int gs, gt0;         // the same for gh
+  // single-launch column + row FFTs (lateral.cu, latfused_kernel): Y is a ring of
+  // f_slots chunk buffers of 32 time samples; f_flags[c] counts the finished column
+  // tiles of chunk c, f_flags[f_chunks + c] its finished row tiles
+  int* f_flags;        // 2 * ceil(T / 32) ints (nullptr: two-kernel form only)
+  int f_chunks, f_slots;
+  int y_capacity;      // time samples per (row, bin) the Y allocation holds
   int cplx;            // 1: NedPlan mode (complex values, full spectrum, no Hermitian fix-up)
   int centered;        // NedPlan output order
   // inverse
@@ -126,6 +132,8 @@ bool spread_time_pairs(int R);
 int spread_time_chunks(int T, int R);
 cudaError_t launch_lateral_col(const LateralParams& p, cudaStream_t s);
 cudaError_t launch_lateral_row(const LateralParams& p, cudaStream_t s);
+bool lateral_fused_supported(const LateralParams& p);
+cudaError_t launch_lateral_forward(const LateralParams& p, cudaStream_t s);  // fused when supported, else col + row
 cudaError_t launch_lateral_inverse(const LateralParams& p, cudaStream_t s);
 cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s);
 size_t ner_smem_bytes(int n_over, int Tu);
@@ -224,6 +232,7 @@ struct patfft_nedner_plan {
   double* d_samples64 = nullptr;
   float* d_grid = nullptr;      // [nrows][ncols][T]
   float2* d_Y = nullptr;        // [nrows][N1h][T]
+  int* d_lat_flags = nullptr;   // progress counters of the single-launch lateral FFTs
   float2* d_gh = nullptr;       // [N0][N1h][T]
   float2* d_z = nullptr;        // [N0u][N1uh][Tu]
   float* d_out = nullptr;       // [N0u][N1u][Tu] f32 (host path staging)

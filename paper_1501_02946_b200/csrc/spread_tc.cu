@@ -530,6 +530,9 @@ __device__ __forceinline__ void c16_next(Cursor16& u, const Item16* ring) {
 #ifndef PATFFT_TC16_NOEPI
 #define PATFFT_TC16_NOEPI 0
 #endif
+#ifndef PATFFT_TC16_NOA
+#define PATFFT_TC16_NOA 0  // diagnosis: skip the A operand copies (wrong results; DRAM traffic of the sample gathers alone)
+#endif
 #ifndef PATFFT_TC16_MBAR
 #define PATFFT_TC16_MBAR 0  // B hand-off by an mbarrier only the MMA thread and load warp wait on (1): measured 0.504 vs 0.480 ms
 #endif
@@ -639,13 +642,13 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
     const int r = g % OFF_SLOTS;
     mbar_wait_tc(&off_bar[r], (g / OFF_SLOTS) & 1);
     uint64_t* bar = &ld_bar[g & 1];
-    if (lane == 0) mbar_expect(bar, A_SLOT + S_SLOT);
+    if (lane == 0) mbar_expect(bar, (PATFFT_TC16_NOA ? 0 : A_SLOT) + S_SLOT);
     __syncwarp();
     if (lane < kKC) {
       const int t0 = p.t_begin + u.it.tb * N;
       bulk_g2s(s_ring + (g & 1) * (S_SLOT / 4) + lane * N, p.samples + ((size_t)offbuf[r * kKC + lane] + t0), N * 4,
                bar);
-    } else if (lane == kKC) {
+    } else if (lane == kKC && !PATFFT_TC16_NOA) {
       bulk_g2s(a_ring + (g % A_SLOTS) * A_SLOT, p.tc_a16 + ((size_t)u.it.st0 + u.c) * (A_SLOT / 16), A_SLOT, bar);
     }
   };

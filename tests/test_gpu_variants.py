@@ -181,6 +181,29 @@ def test_gpu_cfg4_geometry_short_depth_both_gridding_forms(f16):
     assert err <= TOL
 
 
+@pytest.mark.parametrize("nl,nt,slots", [((64, 64), 128, 3), ((128, 128), 128, 2), ((256, 256), 256, 3)])
+def test_gpu_single_launch_lateral_matches_two_kernel_form(nl, nt, slots):
+    """PATFFT_LAT_FUSED_SLOTS > 0: column and row FFTs in one launch with Y as an
+    L2-resident ring (lateral.cu, latfused_kernel).  Same arithmetic per tile, so the
+    volume is bit-identical to the default two-kernel form; also checked vs the oracle."""
+    s = _rect_record(11 + nl[0], nl, nt, 20e-9, layout="jittered")
+    base = pb.NedNerPlan(s.positions, s.weights, nt, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    ref, _ = base.execute(s.samples)
+    ref = ref.copy()
+    os.environ["PATFFT_LAT_FUSED_SLOTS"] = str(slots)
+    try:
+        plan = pb.NedNerPlan(s.positions, s.weights, nt, s.dt, s.sound_speed, s.dx, s.n_lateral)
+        got, _ = plan.execute(s.samples)
+        got2, _ = plan.execute(s.samples)  # flags are re-zeroed per launch
+    finally:
+        os.environ.pop("PATFFT_LAT_FUSED_SLOTS", None)
+    assert np.array_equal(got, ref) and np.array_equal(got2, ref)
+    want, _ = O.reconstruct_nedner(s.positions, s.weights, s.samples, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    err = rel_l2(got, want)
+    print(f"single-launch lateral {nl} Nt={nt} slots={slots}: bit-identical to the two-kernel form, rel-L2 {err:.3e}")
+    assert err <= TOL
+
+
 def test_gpu_window_selection():
     """Auto (alpha, beta) windows with K > 4 run with the float32-grade 8 taps;
     explicit windows and K <= 4 keep what was asked (nufft.py:133-149)."""
