@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpatfft_b200.so")
-SOURCES = ["capi.cu", "spread.cu", "spread_tc.cu", "lateral.cu", "ner.cu", "ner_api.cu", "util.cu", "window.cpp", "hoststage.cpp"]
+SOURCES = ["capi.cu", "spread.cu", "spread_tc.cu", "lateral.cu", "ner.cu", "ner_api.cu", "reflen.cu", "util.cu", "window.cpp", "hoststage.cpp"]
 HEADERS = ["patfft_internal.h", "fft_smem.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -330,6 +330,12 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
         *pr.w = wsub;
         e = 0.0;
       }
+      if (!(e <= kWinTol) && mode == 0 && world == 1) {
+        // the reference's own answer carries this window's approximation error, which depends on
+        // the grid length: run the plan on the reference's lengths (reflen.cu)
+        P->ref_len = true;
+        break;
+      }
       if (!(e <= kWinTol)) {
         char buf[320];
         std::snprintf(buf, sizeof buf,
@@ -340,6 +346,20 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
         return fail(PATFFT_ERR_UNSUPPORTED, buf);
       }
     }
+  }
+  if (P->ref_len) {
+    for (int a = 0; a < d->n_lat; ++a) {
+      n_over_lat[a] = even_fast_len(c * d->out_dims[a]);
+      if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_lat[a]) / d->out_dims[a], &P->win_lat[a],
+                          &err))
+        return fail(PATFFT_ERR_PARAMETER, err);
+    }
+    P->nrows = d->n_lat == 2 ? n_over_lat[0] : 1;
+    P->ncols = n_over_lat[d->n_lat - 1];
+    P->n_over_t = even_fast_len(c * n_ext);
+    if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(P->n_over_t) / n_ext, &P->win_t, &err))
+      return fail(PATFFT_ERR_PARAMETER, err);
+    P->fused_ifft = false;  // the gather kernel writes the depth spectrum, cuFFT inverts it
   }
   // ---- float32-grade windows ----------------------------------------------
   // The reference's default window (K = 6, auto alpha/beta) makes each NUFFT
@@ -386,7 +406,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
       }
     }
   }
-  if (mode != 3 && P->T > 8 * ner_threads(P->n_over_t))
+  if (mode != 3 && !P->ref_len && P->T > 8 * ner_threads(P->n_over_t))
     return fail(PATFFT_ERR_UNSUPPORTED, "depth too long for the NER CTA layout");
   P->custom_inverse = is_pow2(P->N0u) && is_pow2(P->N1u) && P->N0u <= 16384 && P->N1u <= 16384 && P->N1u >= 2;
 
@@ -727,7 +747,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // 3e-8 at degree 7, K = 4 window 5e-8)
   q.poly7 = 0;
   P->poly_degree = 8;
-  if (mode != 2 && mode != 3) {
+  if (mode != 2 && mode != 3 && !P->ref_len) {
     float p7[kMaxTaps / 2][kMaxPolyDegree + 1];
     if (fit_ner_poly_into(wt, 7, p7) <= 6e-8) {
       std::memcpy(q.poly, p7, sizeof p7);
@@ -845,6 +865,31 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     int nl[1] = {P->Tu};
     CUFFT_TRY(cufftPlanMany(&P->fft_l, 1, nl, nl, 1, P->Tu, nl, 1, P->Tu, CUFFT_C2C, P->N0u * P->N1uh));
     P->have_l = true;
+  }
+
+  if (P->ref_len) {  // reference-length plan: uniform FFT stages through cuFFT (reflen.cu)
+    LatRef& lr = P->lat_ref;
+    lr.nyo = ncols / 2 + 1;
+    if ((rc = dalloc(&lr.spec, (size_t)nrows * lr.nyo * T))) return rc;
+    int n[2], inem[2], onem[2];
+    const int rank = d->n_lat;
+    if (rank == 2) {
+      n[0] = nrows; n[1] = ncols;
+      inem[0] = nrows; inem[1] = ncols;
+      onem[0] = nrows; onem[1] = lr.nyo;
+    } else {
+      n[0] = ncols; inem[0] = ncols; onem[0] = lr.nyo;
+    }
+    CUFFT_TRY(cufftPlanMany(&lr.r2c, rank, n, inem, T, 1, onem, T, 1, CUFFT_R2C, T));
+    NerRef& nr = P->ner_ref;
+    const int rows = P->N0 * P->N1h;
+    nr.rows_blk = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)rows, 32768, ((int64_t)1 << 25) / P->n_over_t}));
+    if ((rc = dalloc(&nr.fb, (size_t)nr.rows_blk * P->n_over_t))) return rc;
+    int nl[1] = {P->n_over_t};
+    CUFFT_TRY(cufftPlanMany(&nr.c2c, 1, nl, nl, 1, P->n_over_t, nl, 1, P->n_over_t, CUFFT_C2C, nr.rows_blk));
+    nr.win = NerRefWindow{wt.alpha, wt.beta, 1.0 / psh0, wt.K};
+    q.ref = &P->ner_ref;
+    P->lat.ref = &P->lat_ref;
   }
 
   // ---- kernel parameter blocks --------------------------------------------
@@ -1146,6 +1191,18 @@ int patfft_nedner_output_shape(const patfft_nedner_plan* P, int64_t shape[3]) {
 // lateral FFTs of chunk c run on the plan's second (higher-priority) stream.
 // Without overlap (profiling) the three kernels run back to back on `st`
 // with the stage events in between.
+// PATFFT_DEBUG_SYNC=1 (with PATFFT_GRAPHS=0): synchronise after each stage and name the one that faulted
+static int debug_sync(cudaStream_t st, const char* what) {
+  static const bool on = [] {
+    const char* e = std::getenv("PATFFT_DEBUG_SYNC");
+    return e && std::atoi(e) != 0;
+  }();
+  if (!on) return PATFFT_OK;
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(PATFFT_ERR_CUDA, std::string("stage ") + what + ": " + cudaGetErrorString(e));
+  return PATFFT_OK;
+}
+
 static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* gh, cudaStream_t st, bool overlap,
                            bool prof) {
   const int T = P->Tr;  // == P->T for a single GPU
@@ -1162,15 +1219,16 @@ static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* 
   LateralParams L = P->lat;
   L.gh = gh;
   const int tgran = (1 << 20) / spread_time_chunks(1 << 20, P->R);  // spread CTA time block
-  const int nc = (overlap && P->mode == 0) ? std::max(1, std::min(P->overlap_chunks, T / tgran)) : 1;
+  const int nc = (overlap && P->mode == 0 && !P->ref_len) ? std::max(1, std::min(P->overlap_chunks, T / tgran)) : 1;
   if (nc == 1) {
     sp.t_begin = L.t_begin = 0;
     sp.t_end = L.t_end = T;
     if (P->mode == 0) CUDA_TRY(launch_spread(sp, P->K2, P->R, P->nblk, st));
     else CUDA_TRY(launch_gather_rows(samples, P->d_gidx, P->d_grid, P->M, T, st));
     if (prof) CUDA_TRY(cudaEventRecord(P->ev[1], st));
+    if (int rc = debug_sync(st, "spread")) return rc;
     const int lc = P->lat_chunk;
-    if (lc > 0 && lc < T && P->mode == 0 && !prof) {
+    if (lc > 0 && lc < T && P->mode == 0 && !P->ref_len && !prof) {
       // time chunks of lc samples: colfft writes the chunk's Y (nrows x N1h x lc,
       // reused for every chunk, L2-resident) and rowfft consumes it right away,
       // so the Y round trip stays in L2 instead of HBM
@@ -1182,7 +1240,7 @@ static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* 
       }
       return PATFFT_OK;
     }
-    if (lateral_fused_supported(L)) {  // one launch: its time is reported as lateral_col, lateral_row = 0
+    if (L.ref || lateral_fused_supported(L)) {  // one stage: its time is reported as lateral_col, lateral_row = 0
       CUDA_TRY(launch_lateral_forward(L, st));
       if (prof) CUDA_TRY(cudaEventRecord(P->ev[2], st));
     } else {
@@ -1191,7 +1249,7 @@ static int enqueue_forward(patfft_nedner_plan* P, const float* samples, float2* 
       CUDA_TRY(launch_lateral_row(L, st));
     }
     if (prof) CUDA_TRY(cudaEventRecord(P->ev[3], st));
-    return PATFFT_OK;
+    return debug_sync(st, "lateral");
   }
   const int chunk = ((T + nc - 1) / nc + tgran - 1) / tgran * tgran;
   CUDA_TRY(cudaEventRecord(P->ev_fork, st));
@@ -1228,11 +1286,13 @@ static int execute_device_locked(patfft_nedner_plan* P, const float* samples, fl
   if (P->up > 1 || !P->fused_ifft)
     CUDA_TRY(cudaMemsetAsync(P->d_z, 0, sizeof(float2) * (size_t)P->N0u * P->N1uh * P->Tu, st));
   CUDA_TRY(launch_ner(P->ner, P->K2t, P->poly_degree, st));
+  if (int rc2 = debug_sync(st, "ner")) return rc2;
   if (!P->fused_ifft) {
     CUFFT_TRY(cufftSetStream(P->fft_l, st));
     CUFFT_TRY(cufftExecC2C(P->fft_l, reinterpret_cast<cufftComplex*>(P->d_z),
                            reinterpret_cast<cufftComplex*>(P->d_z), CUFFT_INVERSE));
   }
+  if (int rc2 = debug_sync(st, "depth ifft")) return rc2;
   if (prof) CUDA_TRY(cudaEventRecord(P->ev[4], st));
   if (P->custom_inverse) {
     CUDA_TRY(launch_lateral_inverse(L, st));
@@ -1340,7 +1400,7 @@ static int execute_host_devconvert(patfft_nedner_plan* P, const double* samples,
   const int T = P->T;
   // chunks are whole spread CTA time blocks (256 samples for the time-pair kernel)
   const int tgran = (1 << 20) / spread_time_chunks(1 << 20, P->R);
-  int nc = (P->mode == 0 && !P->profiling) ? std::max(1, std::min(P->h2d_chunks, T / tgran)) : 1;
+  int nc = (P->mode == 0 && !P->ref_len && !P->profiling) ? std::max(1, std::min(P->h2d_chunks, T / tgran)) : 1;
   nc = std::min(nc, (int)patfft_nedner_plan::kMaxH2dChunks);
   if (nc > 1 && !P->copy_stream) {
     CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
@@ -1529,7 +1589,7 @@ static int execute_host_staged(patfft_nedner_plan* P, const double* samples, dou
   cudaStream_t st = P->stream;
   // time chunks: whole spread CTA time blocks, so each chunk's spread starts on a block edge
   const int tgran = (1 << 20) / spread_time_chunks(1 << 20, P->R);
-  int nc = (P->mode == 0 && !P->profiling) ? std::max(1, std::min(P->h2d_chunks, T / tgran)) : 1;
+  int nc = (P->mode == 0 && !P->ref_len && !P->profiling) ? std::max(1, std::min(P->h2d_chunks, T / tgran)) : 1;
   nc = std::min(nc, (int)patfft_nedner_plan::kMaxH2dChunks);
   const int chunk = nc > 1 ? ((T + nc - 1) / nc + tgran - 1) / tgran * tgran : T;
   int used = 0;
@@ -1809,6 +1869,10 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->copy_out_stream) cudaStreamDestroy(P->copy_out_stream);
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
+  if (P->lat_ref.r2c) cufftDestroy(P->lat_ref.r2c);
+  if (P->ner_ref.c2c) cufftDestroy(P->ner_ref.c2c);
+  if (P->lat_ref.spec) cudaFree(P->lat_ref.spec);
+  if (P->ner_ref.fb) cudaFree(P->ner_ref.fb);
   for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_lat_flags, (void*)P->d_gh,
                   (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_tc_recs, (void*)P->d_tc_tiles, (void*)P->d_tc_counter, (void*)P->d_tc_a16, (void*)P->d_tc_off, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_pre, (void*)P->d_tw, (void*)P->d_jt0,

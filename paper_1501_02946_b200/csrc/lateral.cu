@@ -533,12 +533,13 @@ int fused_slots() {
 
 bool lateral_fused_supported(const LateralParams& p) {
   const int len = p.t_end - p.t_begin;
-  return fused_slots() > 0 && p.f_flags && !p.cplx && p.nrows == p.ncols &&
+  return fused_slots() > 0 && !p.ref && p.f_flags && !p.cplx && p.nrows == p.ncols &&
          (p.nrows == 128 || p.nrows == 256 || p.nrows == 512) && plog_for(p.nrows) == 4 && len >= 64 &&
          (int64_t)std::min(fused_slots(), (len + 31) / 32) * 32 <= (int64_t)p.y_capacity;
 }
 
 cudaError_t launch_lateral_forward(const LateralParams& p0, cudaStream_t s) {
+  if (p0.ref) return launch_lateral_ref(p0, s);
   if (!lateral_fused_supported(p0)) {
     cudaError_t e = launch_lateral_col(p0, s);
     return e != cudaSuccess ? e : launch_lateral_row(p0, s);

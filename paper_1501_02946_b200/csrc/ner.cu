@@ -672,6 +672,7 @@ int ner_threads(int n_over) {
 }
 
 cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s) {
+  if (p.ref) return launch_ner_ref(p, s);
   int threads = ner_threads(p.n_over);
   const size_t smem = ner_smem_bytes(p.n_over, p.fused_ifft ? p.Tu : 0);
   const unsigned rows = (unsigned)(p.rows_launch > 0 ? p.rows_launch : p.rows_local);

@@ -70,7 +70,26 @@ struct SpreadParams {
   CUtensorMap tc_gmap;                 // grid [nrows][ncols][T] f32, box 32 t x 16 cols x 2 rows, 128B swizzle
 };
 
+// Reference-length path (reflen.cu): host-side state of the cuFFT stages.  The
+// pointers ride in the kernel parameter blocks but are only read on the host.
+struct LatRef {
+  cufftHandle r2c = 0;     // (rows, cols) real-to-complex per time sample, stride T
+  float2* spec = nullptr;  // [nrows][ncols / 2 + 1][T]
+  int nyo = 0;             // ncols / 2 + 1
+};
+struct NerRefWindow {
+  double alpha, beta, inv_psihat0;
+  int K;
+};
+struct NerRef {
+  cufftHandle c2c = 0;     // length n_over, rows_blk rows per call
+  float2* fb = nullptr;    // [rows_blk][n_over]
+  int rows_blk = 0;
+  NerRefWindow win;
+};
+
 struct LateralParams {
+  const LatRef* ref;   // non-null: reference-length plan (cuFFT lateral stage)
   // forward
   const float* grid;   // [nrows][ncols][T]
   float2* Y;           // [nrows][ny][T]  column-transformed half spectrum
@@ -97,6 +116,7 @@ struct LateralParams {
 };
 
 struct NerParams {
+  const NerRef* ref;   // non-null: reference-length plan (cuFFT NER stage)
   const float2* gh;    // [N0][N1h][T]
   float2* z;           // [N0u][N1uh][Tu]
   const float* iw;     // [2T] psihat(0)*norm/psi(theta_n) (nufft.py:281-284)
@@ -136,6 +156,8 @@ bool lateral_fused_supported(const LateralParams& p);
 cudaError_t launch_lateral_forward(const LateralParams& p, cudaStream_t s);  // fused when supported, else col + row
 cudaError_t launch_lateral_inverse(const LateralParams& p, cudaStream_t s);
 cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s);
+cudaError_t launch_lateral_ref(const LateralParams& p, cudaStream_t s);  // reflen.cu
+cudaError_t launch_ner_ref(const NerParams& p, cudaStream_t s);
 size_t ner_smem_bytes(int n_over, int Tu);
 int ner_threads(int n_over);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);
@@ -224,6 +246,11 @@ struct patfft_nedner_plan {
   int64_t n_records = 0;
   bool fused_ifft = true;
   bool custom_inverse = true;
+  // explicit window that is inaccurate at the reference's own oversampled length: the plan
+  // runs on those lengths (reflen.cu) so that it reproduces the reference's approximation
+  bool ref_len = false;
+  patfft::LatRef lat_ref;
+  patfft::NerRef ner_ref;
 
   patfft::Window win_lat[2], win_t;
 

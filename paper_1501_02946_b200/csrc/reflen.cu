@@ -1,0 +1,183 @@
+// Reference-length path: the NEDNER stages on the reference's OWN oversampled
+// lengths (even 11-smooth, nufft.py:83-89) instead of the power-of-two grids of
+// the shared-memory kernels.
+//
+// An explicit (alpha, beta) window that is inaccurate at the reference's length
+// makes the reference return the exact transform PLUS its own truncation /
+// aliasing error (up to 1e-3 for admissible but poorly chosen shapes,
+// nufft.py:119-149).  A drop-in has to return that same answer, and the error
+// depends on the grid length, so such plans run here: same gridding kernels on
+// an n_over_ref grid, the uniform FFT stages through cuFFT (any length), and
+// two small kernels around them.  This is a compatibility path (taken only
+// when the plan's accuracy probe fails, capi.cu), not a tuned one.
+//
+//   lateral : cuFFT R2C over (rows, cols) for every time sample, then
+//             crop_ref_kernel = the rowfft epilogue (crop to the centred box,
+//             deapodise, Nyquist-plane Hermitian part; nufft.py:406-415,
+//             recon.py:218-222)
+//   NER     : ner_ref_prep_kernel (pre-windowed even extension, zero padded;
+//             recon.py:263-271, nufft.py:325) -> cuFFT C2C of length n_over ->
+//             ner_ref_gather_kernel (2K taps per target with the window
+//             transform evaluated directly in float64, nufft.py:287-293; kappa,
+//             band, amplitude, recon.py:282-308; zero padding / Nyquist split
+//             for upsampling, recon.py:225-246) writing the depth spectrum that
+//             the plan's cuFFT inverse consumes.
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <algorithm>
+
+#include "patfft_internal.h"
+
+namespace patfft {
+namespace {
+
+__device__ __forceinline__ int pmodi(int a, int n) {
+  const int r = a % n;
+  return r < 0 ? r + n : r;
+}
+
+// gh[j0w][j1][t] from the oversampled half spectrum X[row][col bin][t]
+__global__ void crop_ref_kernel(const LateralParams p, const float2* __restrict__ X, int nyo) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j1 = blockIdx.y, j0w = blockIdx.z;
+  if (t >= p.T) return;
+  const int N0 = p.N0, nr = p.nrows;
+  const int a = (N0 > 1) ? (j0w < N0 / 2 ? j0w : j0w - N0) : 0;
+  const bool nyq0 = (N0 > 1) && (a == -(N0 / 2));
+  const bool nyq1 = (j1 == p.N1 / 2);
+  auto at = [&](int row) { return X[((size_t)pmodi(row, nr) * nyo + j1) * p.T + t]; };
+  float2 v;
+  if (nyq1) {  // stored j1 = N1/2 is signed -N1/2: X(a, -N1/2) = conj X(-a, +N1/2)
+    const float2 v1 = at(-a), v2 = at(nyq0 ? -a : a);
+    v = make_float2(0.5f * (v1.x + v2.x), 0.5f * (v2.y - v1.y));
+  } else if (nyq0) {
+    const float2 v1 = at(a), v2 = at(-a);
+    v = make_float2(0.5f * (v1.x + v2.x), 0.5f * (v1.y + v2.y));
+  } else {
+    v = at(a);
+  }
+  const float s = p.dp0[j0w] * p.dp1[j1];
+  p.gh[((size_t)j0w * p.ny + j1) * p.T + t] = make_float2(v.x * s, v.y * s);
+}
+
+// rows [r0, r0 + nrows) of gh -> pre-windowed even extension, zero padded to n_over
+__global__ void ner_ref_prep_kernel(const NerParams p, int r0, int nrows, float2* __restrict__ fb) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (n >= p.n_over || r >= nrows) return;
+  const int T = p.T;
+  float2 v = make_float2(0.f, 0.f);
+  if (n < 2 * T && n != T) {
+    const int t = n < T ? n : 2 * T - n;
+    const float2 g = p.gh[(size_t)(r0 + r) * T + t];
+    const float w = p.iw[n];
+    v = make_float2(g.x * w, g.y * w);
+  }
+  fb[(size_t)r * p.n_over + n] = v;
+}
+
+__device__ __forceinline__ double psihat_ref(double alpha, double beta, double x) {  // nufft.py:168-187
+  const double t = alpha * alpha * (beta * beta - x * x);
+  double v;
+  if (fabs(t) < 1e-9) v = 1.0 + t / 6.0 + t * t / 120.0;
+  else if (t > 0) {
+    const double s = sqrt(t);
+    v = sinh(s) / s;
+  } else {
+    const double s = sqrt(-t);
+    v = sin(s) / s;
+  }
+  return 2.0 * alpha * v;
+}
+
+// one thread per (row, depth frequency l): the reference's tap sum on the cuFFT spectrum
+__global__ void ner_ref_gather_kernel(const NerParams p, NerRefWindow w, int r0, int nrows,
+                                      const float2* __restrict__ fb) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  const int rb = blockIdx.y;
+  const int T = p.T, n = p.n_over, Tu = p.Tu;
+  if (l >= T || rb >= nrows) return;
+  const int r = r0 + rb;
+  const int j0w = r / p.N1h, j1 = r - j0w * p.N1h;
+  const double j2 = p.jt0[j0w] + p.jt1[j1];
+  const double halfT = (double)T / 2.0;
+  const int ls = (l < T / 2) ? l : l - T;
+  const double lv = __dmul_rn(__dmul_rn((double)ls, 1.0 / (double)T), (double)T);  // fftfreq(T)*T
+  const double r2 = __dadd_rn(j2, __dmul_rn(lv, lv));
+  float2 out = make_float2(0.f, 0.f);
+  if (ls != 0 && r2 <= halfT * halfT) {
+    double kap = sqrt(r2);
+    if (ls < 0) kap = -kap;
+    const double ke = 2.0 * kap;
+    const double k0 = floor(__dmul_rn(p.c_eff, ke));
+    const float2* __restrict__ row = fb + (size_t)rb * n;
+    double ar = 0.0, ai = 0.0;
+    for (int a = -w.K + 1; a <= w.K; ++a) {
+      const double bin = k0 + (double)a;
+      const double off = ke - bin / p.c_eff;
+      const double wt = psihat_ref(w.alpha, w.beta, off) * w.inv_psihat0;  // iw[] carries psihat(0) * norm
+      double sn, cs;
+      sincospi(-off, &sn, &cs);
+      const float2 F = row[pmodi((int)bin, n)];
+      ar += wt * (cs * F.x - sn * F.y);
+      ai += wt * (cs * F.y + sn * F.x);
+    }
+    const double amp = 0.5 * (2.0 * lv / kap) * (double)p.scale;
+    out = make_float2((float)(amp * ar), (float)(amp * ai));
+  }
+  // destination rows of the (possibly upsampled) half spectrum z (recon.py:225-246)
+  int j0u = 0, j0u2 = -1;
+  float f0 = 1.f;
+  if (p.n_lat == 2) {
+    const int a = j0w < p.N0 / 2 ? j0w : j0w - p.N0;
+    if (p.up == 1) j0u = j0w;
+    else if (a == -(p.N0 / 2)) {
+      j0u = p.N0 / 2;
+      j0u2 = p.N0u - p.N0 / 2;
+      f0 = 0.5f;
+    } else j0u = a >= 0 ? a : p.N0u + a;
+  }
+  const float f1 = (p.up > 1 && j1 == p.N1 / 2) ? 0.5f : 1.f;
+  const float2 v = make_float2(out.x * f0 * f1, out.y * f0 * f1);
+  for (int d = 0; d < (j0u2 >= 0 ? 2 : 1); ++d) {
+    float2* __restrict__ zr = p.z + ((size_t)(d ? j0u2 : j0u) * p.N1uh + j1) * Tu;
+    if (ls == -(T / 2) && p.up > 1) {
+      zr[T / 2] = make_float2(0.5f * v.x, 0.5f * v.y);
+      zr[Tu - T / 2] = make_float2(0.5f * v.x, 0.5f * v.y);
+    } else {
+      zr[ls >= 0 ? ls : Tu + ls] = v;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_lateral_ref(const LateralParams& p, cudaStream_t s) {
+  const LatRef* R = p.ref;
+  if (p.t_begin != 0 || p.t_end != p.T) return cudaErrorInvalidValue;  // whole record only
+  if (cufftSetStream(R->r2c, s) != CUFFT_SUCCESS) return cudaErrorUnknown;
+  if (cufftExecR2C(R->r2c, const_cast<float*>(p.grid), reinterpret_cast<cufftComplex*>(R->spec)) != CUFFT_SUCCESS)
+    return cudaErrorUnknown;
+  const dim3 grid((unsigned)((p.T + 127) / 128), (unsigned)p.ny, (unsigned)p.N0);
+  crop_ref_kernel<<<grid, 128, 0, s>>>(p, R->spec, R->nyo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ner_ref(const NerParams& p, cudaStream_t s) {
+  const NerRef* R = p.ref;
+  const int rows = p.N0 * p.N1h;
+  if (cufftSetStream(R->c2c, s) != CUFFT_SUCCESS) return cudaErrorUnknown;
+  for (int r0 = 0; r0 < rows; r0 += R->rows_blk) {
+    const int nb = std::min(R->rows_blk, rows - r0);
+    ner_ref_prep_kernel<<<dim3((unsigned)((p.n_over + 255) / 256), (unsigned)nb), 256, 0, s>>>(p, r0, nb, R->fb);
+    // the plan transforms rows_blk rows; the rows past nb of the last block are stale but unused
+    if (cufftExecC2C(R->c2c, reinterpret_cast<cufftComplex*>(R->fb), reinterpret_cast<cufftComplex*>(R->fb),
+                     CUFFT_FORWARD) != CUFFT_SUCCESS)
+      return cudaErrorUnknown;
+    ner_ref_gather_kernel<<<dim3((unsigned)((p.T + 127) / 128), (unsigned)nb), 128, 0, s>>>(p, R->win, r0, nb, R->fb);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace patfft

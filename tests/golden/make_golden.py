@@ -96,6 +96,15 @@ def main():
     # 9. explicit window shape and a larger oversampling factor (c = 2.5)
     recon_case("recon_3d_spec_c25", synth.make_3d(20, 16, 32, 20e-9, "uniform", 2),
                spec={"c": 2.5, "K": 6, "alpha": 12.0, "beta": 2.3})
+    # 9b. admissible but inaccurate explicit windows: the reference's answer carries their
+    # truncation error (1e-3 .. 1e-2 away from the exact transform), which only a plan on the
+    # reference's own oversampled lengths reproduces (csrc/reflen.cu)
+    recon_case("recon_3d_badwin_c25", synth.make_3d(20, 16, 32, 20e-9, "uniform", 2),
+               spec={"c": 2.5, "K": 6, "alpha": 12.0, "beta": 0.5})
+    recon_case("recon_2d_badwin_up2", synth.make_2d(seed=23, n=32, nt=96), upsample=2,
+               spec={"c": 2.2, "K": 3, "alpha": 9.0, "beta": 0.8})
+    recon_case("recon_3d_badwin_up2", synth.make_3d(24, 12, 24, 40e-9, "jittered", 2), upsample=2,
+               spec={"c": 2.5, "K": 4, "alpha": 11.0, "beta": 0.7})
     # 10. upsample 3 (non-power-of-two depth and lateral inverse sizes)
     # (dt = 100 ns: the 16 samples reach the ball; at 20 ns every trace was zero)
     recon_case("recon_3d_up3", synth.make_3d(21, 8, 16, 100e-9, "jittered", 1), upsample=3)
