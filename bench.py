@@ -387,6 +387,30 @@ def run_sharded_arm(args):
     vox = _voxels(rec)
     value = vox / (ms_step / 1e3)
 
+    # roofline of the rank's dominant kernel (the gridding of its time slice), timed alone on the
+    # stream it is launched on; algorithmic bytes 4 * Tr * (M + nrows * ncols)
+    sp_times = []
+    for _ in range(max(3, args.steps)):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.wait_stream(torch.cuda.current_stream(dev))
+        a.record(st)
+        with torch.cuda.stream(st):
+            sh.stages.spread(d_slice, st.cuda_stream)
+        b.record(st)
+        b.synchronize()
+        sp_times.append(a.elapsed_time(b))
+    t = torch.tensor([float(np.mean(sp_times[1:]))], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    spread_ms = float(t.item())
+    n_over = [1 << int(np.ceil(np.log2(2 * n))) for n in rec.n_lateral]
+    spread_bytes = 4.0 * tr * (rec.samples.shape[0] + int(np.prod(n_over)))
+    peak, peak_kind = _peaks()
+    roofline = {"kernel": "spread (per rank: absmax_kernel + spread_tc16_kernel on the rank's time slice)",
+                "bound": "hbm", "achieved": spread_bytes / (spread_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": spread_bytes / (spread_ms / 1e3) / 1e9 / peak, "peak_source": peak_kind, "traffic": None,
+                "algorithmic_bytes": spread_bytes, "launch_ms": spread_ms}
+
     # e2e: pinned f64 host slice -> device -> f32, sharded run, image slice -> pinned f64 host
     pin_in = torch.from_numpy(host_slice).pin_memory()
     pin_out = torch.empty(sh.layout.image_slice_shape(), dtype=torch.float64).pin_memory()
@@ -411,7 +435,7 @@ def run_sharded_arm(args):
             "vs_baseline": None, "dtype": "f32/c64", "data": "synthetic (seeded, BASELINE config shapes)",
             "config": dict(_config_json(args, rec, world), parallelism=f"sharded x{world}: time-sliced NED, "
                            "pipelined all-to-all, row-sliced NER, pipelined all-to-all, time-sliced lateral inverse"),
-            "clocks": clk,
+            "clocks": clk, "roofline": roofline,
             "e2e": {"value": vox / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * host_slice.size * world,
                     "d2h_bytes_per_step": 8 * int(np.prod(pin_out.shape)) * world, "ms_per_step": 1e3 * e2e_s},
             "gpu_launches": (4 + 2 * sh.C + sh.B) * args.steps,

@@ -188,6 +188,21 @@ int patfft_nedner_shard_lateral(patfft_nedner_plan* plan, int t_begin, int t_end
 int patfft_nedner_shard_ner_rows(patfft_nedner_plan* plan, const void* gh_recv, int in_tchunk, int row_begin,
                                  int row_end, void* z_block, void* stream);
 
+/* General multi-GPU schedule (any even N_t, any upsample, any lateral size the plan supports;
+ * paper_1501_02946_b200/parallel.py, GeneralShardedNedNer): a SLICED plan runs the NED stages on a
+ * time slice of t_slice samples and the lateral inverse on a depth slice of upsample * t_slice
+ * samples, with the same kernels as the single-GPU plan:
+ *   patfft_nedner_shard_forward : samples_slice [M][t_slice] -> gh [rows_total][t_slice]
+ *   patfft_nedner_slice_ner     : rows [row_begin, row_end) with the full N_t, [rows][N_t]
+ *                                 -> their rows of z_full = [N0u * N1uh][Tu] (depth-inverted;
+ *                                 recon.py:225-246 row placement, Nyquist rows written twice)
+ *   patfft_nedner_shard_inverse : z_slice [N0u * N1uh][upsample * t_slice] -> image slice
+ * The exchanges between them (rows <-> time slices) belong to the caller. */
+int patfft_nedner_plan_create_slice(const patfft_nedner_desc* desc, const double* grid_positions,
+                                    const double* sensor_scale, int device, int t_slice, patfft_nedner_plan** out);
+int patfft_nedner_slice_ner(patfft_nedner_plan* plan, const void* gh_rows, int row_begin, int row_end, void* z_full,
+                            void* stream);
+
 /* ---- forward model: the reference's forward_fourier (forward.py:105-166) --
  * Full-grid sensor traces of an initial pressure field on an
  * (N0, N1, N_t) or (N, N_t) grid (time/depth fastest, dt = dz / c):

@@ -109,3 +109,64 @@ class NumpyStages:
         if self.nlat == 1:
             img = img[0]
         image_slice.copy_(image_slice.new_tensor(img.astype(np.float32)))
+
+
+class NumpySliceStages(NumpyStages):
+    """CPU model of the general schedule's stages (GpuSliceStages /
+    patfft_nedner_slice_ner): same layouts and sign convention, any even N_t,
+    any upsample (recon.py:225-246 row placement and Nyquist splits)."""
+
+    def __init__(self, positions, weights, n_time, dt, sound_speed, dx, n_lateral, out_dims, upsample, spec, layout):
+        super().__init__(positions, weights, n_time, dt, sound_speed, dx, n_lateral, out_dims, spec, 0, 1)
+        self.L = layout
+        self.up = int(upsample)
+
+    def forward(self, samples_slice, gh_part, stream=0):
+        s = samples_slice.detach().cpu().numpy().astype(np.float64) * self.scale[:, None]
+        gh = O.NedOracle(self.dims, *self.spec).execute(self.gpos, s.astype(np.complex128), wrapped=True)
+        b = gh
+        for ax in range(self.nlat):
+            b = np.roll(np.flip(b, axis=ax), 1, axis=ax)
+        sym = 0.5 * (gh + np.conj(b))
+        if self.nlat == 1:
+            sym = sym[None]
+        half = sym[:, : self.N1h, :].reshape(self.rows_total, s.shape[1]) * self.sign[:, None]
+        gh_part.copy_(gh_part.new_tensor(np.ascontiguousarray(half, dtype=np.complex64).view(np.float32).reshape(
+            self.rows_total, s.shape[1], 2)))
+
+    def ner(self, gh_rows, row_begin, row_end, z_full, stream=0):
+        L, up = self.L, self.up
+        rows = gh_rows.detach().cpu().numpy().reshape(row_end - row_begin, self.T * 2).view(np.complex64)
+        fh = O.fhat_rows(rows.astype(np.complex128), self.j2[row_begin:row_end], self.T, self.spec)
+        if up > 1:
+            fh = O.zero_pad_axis(fh, 1, up)
+        z = np.fft.ifft(fh, axis=-1) * (self.T * up) / (self.N0 * self.N1 * self.T)
+        zf = z_full.detach().cpu().numpy().reshape(L.rows_out_total, L.Tu * 2).view(np.complex64).copy()
+        for i, r in enumerate(range(row_begin, row_end)):
+            j0w, j1 = divmod(r, self.N1h)
+            f = 0.5 if (up > 1 and j1 == self.N1 // 2) else 1.0
+            if self.nlat != 2:
+                dst = [0]
+            elif up == 1:
+                dst = [j0w]
+            else:
+                a = j0w if j0w < self.N0 // 2 else j0w - self.N0
+                if a == -(self.N0 // 2):
+                    dst, f = [self.N0 // 2, L.N0u - self.N0 // 2], 0.5 * f
+                else:
+                    dst = [a if a >= 0 else L.N0u + a]
+            for j in dst:
+                zf[j * L.N1uh + j1] = f * z[i]
+        z_full.copy_(z_full.new_tensor(zf.view(np.float32).reshape(L.rows_out_total, L.Tu, 2)))
+
+    def inverse(self, z_slice, image_slice, stream=0):
+        L = self.L
+        tur = z_slice.shape[1]
+        z = z_slice.detach().cpu().numpy().reshape(L.rows_out_total, tur * 2).view(np.complex64).astype(np.complex128)
+        z = z.reshape(L.N0u, L.N1uh, tur)
+        if self.nlat == 2:
+            z = np.fft.ifft(z, axis=0) * L.N0u
+        img = np.fft.irfft(z, n=L.N1u, axis=1) * L.N1u
+        if self.nlat == 1:
+            img = img[0]
+        image_slice.copy_(image_slice.new_tensor(img.astype(np.float32)))

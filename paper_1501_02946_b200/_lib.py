@@ -64,6 +64,9 @@ _SIGS = {
     "patfft_nedner_shard_spread": (ctypes.c_int, [_P, _P, _P]),
     "patfft_nedner_shard_lateral": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, _P]),
     "patfft_nedner_shard_ner_rows": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P]),
+    "patfft_nedner_plan_create_slice": (ctypes.c_int, [ctypes.POINTER(NednerDesc), _D, _D, ctypes.c_int, ctypes.c_int,
+                                                       ctypes.POINTER(_P)]),
+    "patfft_nedner_slice_ner": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, _P, _P]),
     "patfft_ner_plan_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                               ctypes.c_double, ctypes.c_int, ctypes.POINTER(_P)]),
     "patfft_ner_plan_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),

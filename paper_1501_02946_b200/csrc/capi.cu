@@ -211,8 +211,11 @@ const char* patfft_version(void) { return "patfft-b200 0.2.0 (sm_100a)"; }
 // mode 0: NEDNER (scattered sensors, reconstruct_nedner)
 // mode 1: equispaced grid + NER NUFFT (reconstruct_equispaced, recon.py:345-355)
 // mode 2: equispaced grid + linear interpolation (reconstruct_interp_fft, recon.py:382-389)
+// slice_T > 0 (mode 0, world 1): a sliced plan for the general multi-GPU schedule -- the NED stages
+// and the lateral inverse work on a time / depth slice of slice_T (x upsample) samples, the NER on
+// any row range with the full N_t (patfft_nedner_slice_ner); no size restrictions beyond the plan's.
 static int create_plan(const patfft_nedner_desc* d, const double* gpos, const double* sscale, int device, int rank,
-                       int world, int mode, const int64_t* gidx, patfft_nedner_plan** out) {
+                       int world, int mode, const int64_t* gidx, patfft_nedner_plan** out, int slice_T = 0) {
   if (!d || !out || ((mode == 0 || mode == 3) && (!gpos || !sscale)) || ((mode == 1 || mode == 2) && !gidx))
     return fail(PATFFT_ERR_PARAMETER, "null argument");
   if (world < 1 || rank < 0 || rank >= world) return fail(PATFFT_ERR_PARAMETER, "invalid rank / world size");
@@ -420,6 +423,13 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   P->row_begin = P->row_starts[rank];
   P->rows_mine = P->row_starts[rank + 1] - P->row_begin;
   P->Tr = P->T / world;
+  if (slice_T > 0) {
+    if (mode != 0 || world != 1) return fail(PATFFT_ERR_PARAMETER, "sliced plans are NEDNER plans of one rank");
+    if (slice_T > P->T || slice_T % 2) return fail(PATFFT_ERR_PARAMETER, "time slice must be even and at most N_t");
+    if (P->ref_len) return fail(PATFFT_ERR_UNSUPPORTED, "reference-length windows run on one GPU");
+    P->Tr = slice_T;
+    P->sliced = true;
+  }
   if (world > 1) {
     if (mode != 0) return fail(PATFFT_ERR_UNSUPPORTED, "sharding is implemented for the NEDNER path");
     if (P->up != 1) return fail(PATFFT_ERR_UNSUPPORTED, "sharded reconstruction requires upsample == 1");
@@ -820,8 +830,8 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     }
   }
   if ((rc = dalloc(&P->d_Y, (size_t)nrows * P->N1h * T))) return rc;
-  if ((rc = dalloc(&P->d_lat_flags, 2 * ((size_t)T / 32 + 2)))) return rc;
-  if (world == 1) {
+  if ((rc = dalloc(&P->d_lat_flags, 2 * ((size_t)T / 16 + 2)))) return rc;
+  if (world == 1 && !P->sliced) {
     if ((rc = dalloc(&P->d_gh, (size_t)P->N0 * P->N1h * T))) return rc;
     if ((rc = dalloc(&P->d_z, (size_t)P->N0u * P->N1uh * P->Tu))) return rc;
   }
@@ -858,7 +868,8 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     } else {
       n[0] = P->N1u; inem[0] = P->N1uh; onem[0] = P->N1u;
     }
-    CUFFT_TRY(cufftPlanMany(&P->fft_c2r, rank, n, inem, P->Tu, 1, onem, P->Tu, 1, CUFFT_C2R, P->Tu));
+    const int tus = P->sliced ? P->up * P->Tr : P->Tu;  // depth samples the lateral inverse works on
+    CUFFT_TRY(cufftPlanMany(&P->fft_c2r, rank, n, inem, tus, 1, onem, tus, 1, CUFFT_C2R, tus));
     P->have_c2r = true;
   }
   if (!P->fused_ifft && mode != 3) {
@@ -964,7 +975,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   L.N1 = P->N1;
   L.z = P->d_z;
   L.out = nullptr;
-  L.Tu = world == 1 ? P->Tu : P->Tr;
+  L.Tu = P->sliced ? P->up * P->Tr : (world == 1 ? P->Tu : P->Tr);
   L.N0u = P->N0u;
   L.N1u = P->N1u;
   L.N1uh = P->N1uh;
@@ -1054,6 +1065,42 @@ int patfft_equispaced_plan_create(const patfft_nedner_desc* d, const int64_t* gr
 int patfft_nedner_plan_create_sharded(const patfft_nedner_desc* d, const double* gpos, const double* sscale,
                                       int device, int rank, int world, patfft_nedner_plan** out) {
   return create_plan(d, gpos, sscale, device, rank, world, 0, nullptr, out);
+}
+
+int patfft_nedner_plan_create_slice(const patfft_nedner_desc* d, const double* gpos, const double* sscale,
+                                    int device, int t_slice, patfft_nedner_plan** out) {
+  if (t_slice < 2) return fail(PATFFT_ERR_PARAMETER, "time slice must hold at least 2 samples");
+  return create_plan(d, gpos, sscale, device, 0, 1, 0, nullptr, out, t_slice);
+}
+
+// NER + depth inverse of lateral rows [row_begin, row_end) (full N_t each, [rows][N_t] complex64)
+// into the rows of z_full = [N0u * N1uh][Tu] they map to (recon.py:225-246: one row, or two for the
+// lateral Nyquist split).  z_full must have been zero-filled once by the caller when the depth
+// inverse is fused (upsample > 1 leaves rows no rank writes); the cuFFT depth inverse (Tu not a
+// power of two) re-zeroes and transforms all of z_full on every call.
+int patfft_nedner_slice_ner(patfft_nedner_plan* P, const void* gh_rows, int row_begin, int row_end, void* z_full,
+                            void* stream) {
+  if (!P || !gh_rows || !z_full) return fail(PATFFT_ERR_PARAMETER, "null argument");
+  if (!P->sliced) return fail(PATFFT_ERR_PARAMETER, "not a sliced plan");
+  if (row_begin < 0 || row_end > P->rows_total || row_begin >= row_end)
+    return fail(PATFFT_ERR_PARAMETER, "row range outside the lateral spectrum");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+  NerParams q = P->ner;
+  q.gh = static_cast<const float2*>(gh_rows) - (ptrdiff_t)row_begin * P->T;  // indexed by the global row
+  q.z = static_cast<float2*>(z_full);
+  q.in_row_off = row_begin;
+  q.rows_launch = row_end - row_begin;
+  if (!P->fused_ifft)
+    CUDA_TRY(cudaMemsetAsync(z_full, 0, sizeof(float2) * (size_t)P->N0u * P->N1uh * P->Tu, st));
+  CUDA_TRY(launch_ner(q, P->K2t, P->poly_degree, st));
+  if (!P->fused_ifft) {
+    CUFFT_TRY(cufftSetStream(P->fft_l, st));
+    CUFFT_TRY(cufftExecC2C(P->fft_l, reinterpret_cast<cufftComplex*>(z_full), reinterpret_cast<cufftComplex*>(z_full),
+                           CUFFT_INVERSE));
+  }
+  return PATFFT_OK;
 }
 
 int patfft_nedner_shard_info(const patfft_nedner_plan* P, int64_t info[8]) {
@@ -1166,7 +1213,12 @@ int patfft_nedner_shard_inverse(patfft_nedner_plan* P, const void* z_recv, float
   LateralParams L = P->lat;
   L.z = static_cast<float2*>(const_cast<void*>(z_recv));
   L.out = image_slice;
-  CUDA_TRY(launch_lateral_inverse(L, st));
+  if (P->custom_inverse) {
+    CUDA_TRY(launch_lateral_inverse(L, st));
+  } else {  // sliced plans with lateral sizes the shared-memory kernels do not cover
+    CUFFT_TRY(cufftSetStream(P->fft_c2r, st));
+    CUFFT_TRY(cufftExecC2R(P->fft_c2r, reinterpret_cast<cufftComplex*>(L.z), image_slice));
+  }
   return PATFFT_OK;
 }
 

@@ -531,11 +531,18 @@ int fused_slots() {
 }
 }  // namespace
 
+// transforms per tile of the single-launch form: 16 (64 KB tiles at 512 points, 2 CTAs/SM) or 8
+// (PATFFT_LAT_FUSED_PLOG=3: 32 KB tiles, 4 CTAs/SM)
+int fused_plog() {
+  const char* e = std::getenv("PATFFT_LAT_FUSED_PLOG");
+  return e && std::atoi(e) == 3 ? 3 : 4;
+}
+
 bool lateral_fused_supported(const LateralParams& p) {
-  const int len = p.t_end - p.t_begin;
+  const int len = p.t_end - p.t_begin, ch = 2 << fused_plog();
   return fused_slots() > 0 && !p.ref && p.f_flags && !p.cplx && p.nrows == p.ncols &&
-         (p.nrows == 128 || p.nrows == 256 || p.nrows == 512) && plog_for(p.nrows) == 4 && len >= 64 &&
-         (int64_t)std::min(fused_slots(), (len + 31) / 32) * 32 <= (int64_t)p.y_capacity;
+         (p.nrows == 128 || p.nrows == 256 || p.nrows == 512) && len >= 64 &&
+         (int64_t)std::min(fused_slots(), (len + ch - 1) / ch) * ch <= (int64_t)p.y_capacity;
 }
 
 cudaError_t launch_lateral_forward(const LateralParams& p0, cudaStream_t s) {
@@ -545,12 +552,13 @@ cudaError_t launch_lateral_forward(const LateralParams& p0, cudaStream_t s) {
     return e != cudaSuccess ? e : launch_lateral_row(p0, s);
   }
   LateralParams p = p0;
-  p.f_chunks = (p.t_end - p.t_begin + 31) / 32;
+  const int plog = fused_plog(), ch = 2 << plog;
+  p.f_chunks = (p.t_end - p.t_begin + ch - 1) / ch;
   p.f_slots = std::min(fused_slots(), p.f_chunks);
   cudaError_t err = cudaMemsetAsync(p.f_flags, 0, sizeof(int) * 2 * (size_t)p.f_chunks, s);
   if (err != cudaSuccess) return err;
   const unsigned grid = (unsigned)((p.f_chunks + 1) * (p.nrows + 2 * p.ny));
-  const size_t smem = ((size_t)p.nrows << 4) * sizeof(float2);
+  const size_t smem = ((size_t)p.nrows << plog) * sizeof(float2);
   auto run = [&](auto k, int thr) {
     err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err == cudaSuccess) {
@@ -558,6 +566,14 @@ cudaError_t launch_lateral_forward(const LateralParams& p0, cudaStream_t s) {
       err = cudaGetLastError();
     }
   };
+  if (plog == 3) {
+    switch (p.nrows) {
+      case 128: run(latfused_kernel<3, 7>, nth_for(7, 3)); break;
+      case 256: run(latfused_kernel<3, 8>, nth_for(8, 3)); break;
+      default: run(latfused_kernel<3, 9>, nth_for(9, 3)); break;
+    }
+    return err;
+  }
   switch (p.nrows) {
     case 128: run(latfused_kernel<4, 7>, nth_for(7, 4)); break;
     case 256: run(latfused_kernel<4, 8>, nth_for(8, 4)); break;

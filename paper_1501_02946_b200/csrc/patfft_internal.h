@@ -249,6 +249,9 @@ struct patfft_nedner_plan {
   // explicit window that is inaccurate at the reference's own oversampled length: the plan
   // runs on those lengths (reflen.cu) so that it reproduces the reference's approximation
   bool ref_len = false;
+  // sliced plan (general multi-GPU schedule): NED stages / lateral inverse on Tr (x up) samples,
+  // NER on caller-provided row ranges with the full N_t
+  bool sliced = false;
   patfft::LatRef lat_ref;
   patfft::NerRef ner_ref;
 

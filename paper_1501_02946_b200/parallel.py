@@ -308,3 +308,245 @@ class ShardedNedNer:
             w.wait()
         st.inverse(self.z_recv, self.image, s)
         return self.image
+
+
+# ---------------------------------------------------------------------------
+# General schedule: any even N_t, any upsample, any lateral size of the plan
+# ---------------------------------------------------------------------------
+
+class SliceLayout:
+    """Partition of the general schedule: time (and depth) ranges with even
+    boundaries -- the lateral kernels pack two time samples per transform --
+    and the lateral rows of the half spectrum, split as evenly as possible.
+    ``out_rows(q)``: the rows of the (upsampled) half spectrum ``z`` that rank
+    q's NER writes (recon.py:225-246: a lateral Nyquist row lands twice)."""
+
+    def __init__(self, n_lat, out_dims, n_time, world, upsample=1):
+        if n_time % 2 or n_time // 2 < world:
+            raise ValueError("general sharding needs an even N_t with at least 2 samples per rank")
+        self.n_lat, self.world, self.up, self.T = n_lat, world, int(upsample), int(n_time)
+        self.N0 = out_dims[0] if n_lat == 2 else 1
+        self.N1 = out_dims[-1]
+        self.N1h = self.N1 // 2 + 1
+        self.N0u = self.N0 * self.up if n_lat == 2 else 1
+        self.N1u = self.N1 * self.up
+        self.N1uh = self.N1u // 2 + 1
+        self.Tu = self.T * self.up
+        self.rows_total = self.N0 * self.N1h
+        self.rows_out_total = self.N0u * self.N1uh
+        self.t_starts = [2 * ((q * (self.T // 2)) // world) for q in range(world + 1)]
+        self.row_starts = [q * self.rows_total // world for q in range(world + 1)]
+
+    def t_range(self, q):
+        return self.t_starts[q], self.t_starts[q + 1]
+
+    def tu_range(self, q):
+        return self.up * self.t_starts[q], self.up * self.t_starts[q + 1]
+
+    def t_slice_max(self):
+        return max(self.t_starts[q + 1] - self.t_starts[q] for q in range(self.world))
+
+    def out_rows(self, q):
+        rows = []
+        for r in range(self.row_starts[q], self.row_starts[q + 1]):
+            j0w, j1 = divmod(r, self.N1h)
+            if self.n_lat != 2:
+                j0u = [0]
+            elif self.up == 1:
+                j0u = [j0w]
+            else:
+                a = j0w if j0w < self.N0 // 2 else j0w - self.N0
+                j0u = [self.N0 // 2, self.N0u - self.N0 // 2] if a == -(self.N0 // 2) else [a if a >= 0 else self.N0u + a]
+            rows += [j * self.N1uh + j1 for j in j0u]
+        return rows
+
+    def image_slice_shape(self, q):
+        a, b = self.tu_range(q)
+        return ((self.N0u, self.N1u) if self.n_lat == 2 else (self.N1u,)) + (b - a,)
+
+
+class GpuSliceStages:
+    """Per-rank stages of the general schedule on the B200 (sliced C plan)."""
+
+    def __init__(self, positions, weights, n_time, dt, sound_speed, dx, n_lateral, out_dims, upsample, spec, t_slice,
+                 device):
+        lib = _lib.load()
+        positions = np.atleast_2d(np.asarray(positions, dtype=np.float64))
+        n_lateral = tuple(int(n) for n in np.atleast_1d(n_lateral))
+        if positions.shape[1] != len(n_lateral):
+            positions = positions.T
+        weights = np.asarray(weights, dtype=np.float64).ravel()
+        nlat = len(out_dims)
+        scale = np.ascontiguousarray(weights / dx ** nlat)
+        gpos = np.ascontiguousarray((positions / dx) * (np.asarray(out_dims, float) / np.asarray(n_lateral, float)))
+        dy = sound_speed * dt
+        desc = _lib.NednerDesc()
+        desc.n_lat = nlat
+        desc.out_dims[0] = out_dims[0]
+        desc.out_dims[1] = out_dims[-1] if nlat == 2 else 0
+        desc.n_time = int(n_time)
+        desc.upsample = int(upsample)
+        desc.n_sensors = positions.shape[0]
+        ratios = [n_time * dy / (n * dx) for n in n_lateral]
+        desc.lat_ratio[0] = ratios[0]
+        desc.lat_ratio[1] = ratios[-1]
+        desc.spec_c = float(spec.c)
+        desc.spec_K = int(spec.K)
+        desc.spec_alpha = math.nan if spec.alpha is None else float(spec.alpha)
+        desc.spec_beta = math.nan if spec.beta is None else float(spec.beta)
+        h = ctypes.c_void_p()
+        _lib.check(lib.patfft_nedner_plan_create_slice(
+            ctypes.byref(desc), gpos.ctypes.data_as(_lib._D), scale.ctypes.data_as(_lib._D), int(device), int(t_slice),
+            ctypes.byref(h)))
+        self._lib = lib
+        self._h = h
+
+    def forward(self, samples_slice, gh_part, stream=0):
+        _lib.check(self._lib.patfft_nedner_shard_forward(self._h, ctypes.c_void_p(samples_slice.data_ptr()),
+                                                         ctypes.c_void_p(gh_part.data_ptr()), ctypes.c_void_p(stream or 0)))
+
+    def ner(self, gh_rows, row_begin, row_end, z_full, stream=0):
+        _lib.check(self._lib.patfft_nedner_slice_ner(self._h, ctypes.c_void_p(gh_rows.data_ptr()), int(row_begin),
+                                                     int(row_end), ctypes.c_void_p(z_full.data_ptr()),
+                                                     ctypes.c_void_p(stream or 0)))
+
+    def inverse(self, z_slice, image_slice, stream=0):
+        _lib.check(self._lib.patfft_nedner_shard_inverse(self._h, ctypes.c_void_p(z_slice.data_ptr()),
+                                                         ctypes.c_void_p(image_slice.data_ptr()),
+                                                         ctypes.c_void_p(stream or 0)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.patfft_nedner_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class GeneralShardedNedNer:
+    """One reconstruction across the ranks of a torch.distributed group, for
+    every case the reference handles on one process: any even N_t (uneven
+    time slices with even boundaries), any ``upsample`` (recon.py:392-394),
+    any lateral size.  ``ShardedNedNer`` is the pipelined fast path for
+    power-of-two N_t / world and upsample 1; this class trades its in-place
+    receive layouts for plain packing copies:
+
+    1. NED + lateral FFT of the rank's time slice (no communication);
+    2. rows of every slice to their owner (grouped send/recv), assembled
+       into ``[rows_mine][N_t]``;
+    3. NER + depth inverse of the owned rows into their rows of the
+       (upsampled, zero-padded) half spectrum;
+    4. depth slices of those rows to their owners, scattered into
+       ``[N0u * N1uh][upsample * slice]`` (rows nobody owns stay zero);
+    5. lateral inverse of the rank's depth slice.
+
+    ``run`` takes ``samples[:, t0:t1]`` of the rank's ``layout.t_range(rank)``
+    and returns ``image[..., up*t0:up*t1]`` (a buffer reused by the next call
+    unless ``out=`` is given).
+    """
+
+    def __init__(self, positions, weights, n_time, dt, sound_speed, dx, n_lateral, out_dims=None, upsample=1,
+                 spec: WindowSpec | None = None, group=None, device=None, stages=None, torch_device=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.group = torch, dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        n_lateral = tuple(int(n) for n in np.atleast_1d(n_lateral))
+        dims = _out_dims(n_lateral, out_dims)
+        if int(upsample) != upsample or upsample < 1:
+            raise ValueError("upsample must be a positive integer")
+        spec = spec if spec is not None else WindowSpec()
+        self.layout = L = SliceLayout(len(dims), dims, int(n_time), self.world, int(upsample))
+        if torch_device is None:
+            torch_device = torch.device("cuda", torch.cuda.current_device()) if device is None else \
+                torch.device("cuda", device)
+        self.tdev = torch_device
+        t0, t1 = L.t_range(self.rank)
+        if stages is None:
+            stages = GpuSliceStages(positions, weights, n_time, dt, sound_speed, dx, n_lateral, dims, int(upsample),
+                                    spec, t1 - t0, torch_device.index)
+        self.stages = stages
+        f32 = dict(dtype=torch.float32, device=torch_device)
+        P, rm = self.world, L.row_starts[self.rank + 1] - L.row_starts[self.rank]
+        self.rm = rm
+        self.gh_part = torch.empty(L.rows_total, t1 - t0, 2, **f32)
+        self.gh_rows = torch.empty(rm, L.T, 2, **f32)
+        self.z_full = torch.zeros(L.rows_out_total, L.Tu, 2, **f32)   # rows of other ranks stay zero
+        u0, u1 = L.tu_range(self.rank)
+        self.z_slice = torch.zeros(L.rows_out_total, u1 - u0, 2, **f32)  # rows nobody writes stay zero
+        self.image = torch.empty(L.image_slice_shape(self.rank), **f32)
+        self.out_idx = [torch.tensor(L.out_rows(q), dtype=torch.long, device=torch_device) for q in range(P)]
+        self.cuda_stream = torch.cuda.Stream(device=torch_device) if torch_device.type == "cuda" else None
+
+    def _exchange(self, sends, recvs):
+        dist = self.dist
+        recvs[self.rank].copy_(sends[self.rank])
+        ops = []
+        for q in range(self.world):
+            if q != self.rank:
+                ops.append(dist.P2POp(dist.isend, sends[q], q, group=self.group))
+                ops.append(dist.P2POp(dist.irecv, recvs[q], q, group=self.group))
+        for w in (dist.batch_isend_irecv(ops) if ops else []):
+            w.wait()
+
+    def run(self, samples_slice, out=None):
+        if self.cuda_stream is None:
+            img = self._run(samples_slice, 0)
+        else:
+            torch = self.torch
+            cur = torch.cuda.current_stream(self.tdev)
+            self.cuda_stream.wait_stream(cur)
+            with torch.cuda.stream(self.cuda_stream):
+                img = self._run(samples_slice, self.cuda_stream.cuda_stream)
+            cur.wait_stream(self.cuda_stream)
+        if out is not None:
+            out.copy_(img)
+            return out
+        return img
+
+    def _run(self, samples_slice, s):
+        torch, L, P, me = self.torch, self.layout, self.world, self.rank
+        st = self.stages
+        st.forward(samples_slice, self.gh_part, s)
+        # rows of my time slice -> their owners; theirs -> columns [t0, t1) of my rows
+        sends = [self.gh_part[L.row_starts[q]:L.row_starts[q + 1]] for q in range(P)]   # contiguous row blocks
+        recvs = [torch.empty(self.rm, L.t_starts[q + 1] - L.t_starts[q], 2, dtype=torch.float32, device=self.tdev)
+                 for q in range(P)]
+        self._exchange(sends, recvs)
+        for q in range(P):
+            self.gh_rows[:, L.t_starts[q]:L.t_starts[q + 1]] = recvs[q]
+        st.ner(self.gh_rows, L.row_starts[me], L.row_starts[me + 1], self.z_full, s)
+        # depth slices of my output rows -> their owners, scattered into z_slice at their rows
+        mine = self.z_full.index_select(0, self.out_idx[me])
+        sends = [mine[:, L.up * L.t_starts[q]:L.up * L.t_starts[q + 1]].contiguous() for q in range(P)]
+        u0, u1 = L.tu_range(me)
+        recvs = [torch.empty(len(self.out_idx[q]), u1 - u0, 2, dtype=torch.float32, device=self.tdev) for q in range(P)]
+        self._exchange(sends, recvs)
+        for q in range(P):
+            self.z_slice.index_copy_(0, self.out_idx[q], recvs[q])
+        st.inverse(self.z_slice, self.image, s)
+        return self.image
+
+
+def sharded_nedner(positions, weights, n_time, dt, sound_speed, dx, n_lateral, out_dims=None, upsample=1, spec=None,
+                   **kw):
+    """The fastest multi-GPU schedule that covers the request: ``ShardedNedNer``
+    (pipelined, in-place layouts) for upsample 1, power-of-two N_t / world and
+    lateral / depth grids, else ``GeneralShardedNedNer``."""
+    import torch.distributed as dist
+
+    n_lateral_t = tuple(int(n) for n in np.atleast_1d(n_lateral))
+    dims = _out_dims(n_lateral_t, out_dims)
+    world = dist.get_world_size(kw.get("group"))
+    pow2 = all(n & (n - 1) == 0 for n in dims) and n_time & (n_time - 1) == 0
+    if upsample == 1 and pow2 and ShardLayout.supported(n_time, world) and n_time // world >= 32:
+        return ShardedNedNer(positions, weights, n_time, dt, sound_speed, dx, n_lateral, out_dims=out_dims, spec=spec,
+                             **kw)
+    return GeneralShardedNedNer(positions, weights, n_time, dt, sound_speed, dx, n_lateral, out_dims=out_dims,
+                                upsample=upsample, spec=spec, **kw)

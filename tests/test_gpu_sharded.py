@@ -117,3 +117,62 @@ def test_pipelined_shard_stages_match_single_gpu(world, chunks, blocks):
     err = rel_l2(got, want)
     print(f"pipelined world {world} (pieces {C}, row blocks {blocks}): rel-L2 vs single GPU {err:.2e}")
     assert err <= 1e-6
+
+
+@pytest.mark.parametrize("world,case", [(3, "2d_nt96_up2"), (2, "3d_up2"), (3, "3d_outdims_nt40"), (4, "3d_up3")])
+def test_general_schedule_stages_match_single_gpu(world, case):
+    """The general multi-GPU schedule (sliced C plans: any even N_t, any upsample, uneven time
+    slices; parallel.GeneralShardedNedNer's layouts) with the ranks emulated one after another on
+    one GPU, against the single-GPU reconstruction and the oracle."""
+    import torch
+
+    from oracle import nedner_oracle as O
+    from paper_1501_02946_b200.parallel import GpuSliceStages, SliceLayout
+    from paper_1501_02946_b200.recon import _out_dims
+    from test_sharded_gloo import _general_case
+
+    rec, out_dims, up = _general_case(case)
+    want = pb.reconstruct_nedner(rec.as_record(), out_dims=out_dims, upsample=up).values
+    nl = tuple(rec.n_lateral)
+    dims = _out_dims(nl, out_dims)
+    T = rec.samples.shape[1]
+    L = SliceLayout(len(dims), dims, T, world, up)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    s = stream.cuda_stream
+    f32 = dict(dtype=torch.float32, device=dev)
+    stages = [GpuSliceStages(rec.positions, rec.weights, T, rec.dt, rec.sound_speed, rec.dx, nl, dims, up,
+                             pb.WindowSpec(), L.t_starts[q + 1] - L.t_starts[q], 0) for q in range(world)]
+    samples = torch.tensor(rec.samples, dtype=torch.float32, device=dev)
+    rs = L.row_starts
+    gh_part = []
+    for q in range(world):
+        t0, t1 = L.t_range(q)
+        g = torch.empty(L.rows_total, t1 - t0, 2, **f32)
+        stages[q].forward(samples[:, t0:t1].contiguous(), g, s)
+        gh_part.append(g)
+    z_full = []
+    for q in range(world):
+        rows = torch.cat([gh_part[p][rs[q]:rs[q + 1]] for p in range(world)], dim=1).contiguous()  # [rows_q][T]
+        z = torch.zeros(L.rows_out_total, L.Tu, 2, **f32)
+        stages[q].ner(rows, rs[q], rs[q + 1], z, s)
+        z_full.append(z)
+    idx = [torch.tensor(L.out_rows(p), dtype=torch.long, device=dev) for p in range(world)]
+    imgs = []
+    for q in range(world):
+        u0, u1 = L.tu_range(q)
+        zs = torch.zeros(L.rows_out_total, u1 - u0, 2, **f32)
+        for p in range(world):
+            zs.index_copy_(0, idx[p], z_full[p].index_select(0, idx[p])[:, u0:u1].contiguous())
+        img = torch.empty(L.image_slice_shape(q), **f32)
+        stages[q].inverse(zs, img, s)
+        imgs.append(img)
+    torch.cuda.synchronize()
+    got = torch.cat(imgs, dim=-1).double().cpu().numpy()
+    torch.cuda.set_stream(torch.cuda.default_stream(dev))
+    oracle, _ = O.reconstruct_nedner(rec.positions, rec.weights, rec.samples, rec.dt, rec.sound_speed, rec.dx,
+                                     rec.n_lateral, out_dims=out_dims, upsample=up)
+    e1, e2 = rel_l2(got, want), rel_l2(got, oracle)
+    print(f"general schedule world {world} {case}: rel-L2 vs single GPU {e1:.2e}, vs oracle {e2:.2e}")
+    assert got.shape == want.shape and e1 <= 5e-6 and e2 <= 1e-4
