@@ -31,6 +31,9 @@ using fft::TileAddr;
 #ifndef PATFFT_LAT_FUSED
 #define PATFFT_LAT_FUSED 1  // colfft/rowfft: last FFT pass evaluated inside the crop/unpack epilogue
 #endif
+#ifndef PATFFT_LAT_FUSED_MAXR
+#define PATFFT_LAT_FUSED_MAXR 1  // largest log2 radix of a last pass that is folded into the colfft unpack
+#endif
 #ifndef PATFFT_LAT_ROWPTR
 #define PATFFT_LAT_ROWPTR 1  // colfft/rowfft first pass: one base pointer + running row offset per item
 #endif
@@ -109,7 +112,10 @@ __device__ __forceinline__ void colfft_body(const LateralParams& p, float2* __re
     return (t < p.t_end) ? __ldcs(reinterpret_cast<const float2*>(src + (size_t)row * T + t)) : make_float2(0.f, 0.f);
   };
   constexpr int LLAST = LC > 0 ? fft::LastPassLogh<(LC > 0 ? LC : 1), 4, false>::value : 0;
-  constexpr bool FUSED = PATFFT_LAT_FUSED && LC > 0 && LLAST > 0;
+  // the last pass is folded into the unpack only when it is short: a radix-2^r fold costs 2^r
+  // complex MACs for each of the 2 ny outputs kept, a radix-16 one three times the pass it replaces
+  // (cfg3's 256-point columns: colfft 0.089 -> see DESIGN.md 4)
+  constexpr bool FUSED = PATFFT_LAT_FUSED && LC > 0 && LLAST > 0 && (LC - LLAST) <= PATFFT_LAT_FUSED_MAXR;
   if constexpr (LC > 0 && PATFFT_LAT_ROWPTR) {
     fft::fft_ct_loaded<false, LC, 4, false, PLOG, nth_for(LC, PLOG), FUSED>(
         sm, p.tw, tid, fft::TileC<PLOG>(), fft::rows_ld<GMODE>([&](int row, int q) -> const float2* {

@@ -5,7 +5,7 @@ tag=$1; shift
 mkdir -p gpurun_out
 env "$@" timeout 600 ncu --cache-control none --clock-control none --csv \
   --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum,lts__t_sectors_srcunit_tex_op_read.sum \
-  --log-file gpurun_out/dram_$tag.csv python tools/profile_step.py --iters 3 > gpurun_out/dram_$tag.log 2>&1 || tail -3 gpurun_out/dram_$tag.log
+  --log-file gpurun_out/dram_$tag.csv python tools/profile_step.py --iters 3 ${PROFILE_ARGS} > gpurun_out/dram_$tag.log 2>&1 || tail -3 gpurun_out/dram_$tag.log
 python - gpurun_out/dram_$tag.csv "$tag" <<'PY'
 import csv, sys, collections
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
