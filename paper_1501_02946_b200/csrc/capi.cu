@@ -265,15 +265,31 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     Window tmp;
     if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, ceff_ref_min, &tmp, &err))  // nufft.py:362
       return fail(PATFFT_ERR_PARAMETER, err);
+    // ... and per axis (nufft.py:363) and for the NerPlan of length 2 N_t (nufft.py:277-279): a window
+    // the reference itself refuses is a ParameterError here too, with its message
+    for (int a = 0; a < d->n_lat && mode != 1 && mode != 2; ++a)
+      if (!resolve_window(c, K, d->spec_alpha, d->spec_beta,
+                          double(even_fast_len(c * d->out_dims[a])) / d->out_dims[a], &tmp, &err))
+        return fail(PATFFT_ERR_PARAMETER, err);
+    if (mode != 2 && mode != 3 &&
+        !resolve_window(c, K, d->spec_alpha, d->spec_beta, double(even_fast_len(c * 2.0 * P->T)) / (2.0 * P->T), &tmp,
+                        &err))
+      return fail(PATFFT_ERR_PARAMETER, err);
   }
+  // A window that is admissible at the reference's effective oversampling (checked above) can be
+  // inadmissible at the GPU's larger power-of-two one (alpha must exceed c_eff, nufft.py:125-127):
+  // such a plan runs on the reference's lengths (reflen.cu) instead of being refused.
+  const bool can_ref_len = mode == 0 && world == 1;
   int n_over_lat[2] = {1, 1};
   for (int a = 0; a < d->n_lat; ++a) {
     int64_t n = next_pow2((int64_t)std::ceil(c * d->out_dims[a]));
     if (n < 4) n = 4;
     if (n > 16384) return fail(PATFFT_ERR_UNSUPPORTED, "GPU path supports oversampled lateral grids up to 16384");
     n_over_lat[a] = (int)n;
-    if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n) / d->out_dims[a], &P->win_lat[a], &err))
-      return fail(PATFFT_ERR_PARAMETER, err);
+    if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n) / d->out_dims[a], &P->win_lat[a], &err)) {
+      if (!can_ref_len) return fail(PATFFT_ERR_UNSUPPORTED, err + " (at the GPU's power-of-two oversampled length)");
+      P->ref_len = true;
+    }
   }
   P->mode = mode;
   if (mode == 1 || mode == 2) {  // the full grid itself is the lateral FFT input: no oversampling, no window
@@ -300,54 +316,79 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     return fail(PATFFT_ERR_UNSUPPORTED, "GPU NER supports oversampled depth lengths up to 16384 (N_t <= 4096 at c=2)");
   P->n_over_t = (int)n_over_t;
   if (mode != 2 && mode != 3 &&
-      !resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_t) / n_ext, &P->win_t, &err))
-    return fail(PATFFT_ERR_PARAMETER, err);
+      !resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_t) / n_ext, &P->win_t, &err)) {
+    if (!can_ref_len) return fail(PATFFT_ERR_UNSUPPORTED, err + " (at the GPU's power-of-two oversampled length)");
+    P->ref_len = true;
+  }
   P->fused_ifft = is_pow2(P->Tu) && P->Tu <= 16384;
 
-  // An explicit alpha/beta fixes the window in frequency units; the GPU grids
-  // are powers of two, so when its effective oversampling differs from the
-  // reference's (even 11-smooth length) the same (alpha, beta, K) can cover a
-  // different part of the window.  Probe the accuracy at the GPU sizes.  If it
-  // is lost there but the window is accurate at the reference's own length,
-  // the reference's result is the exact transform to within that accuracy, so
-  // the GPU computes the same transform with the window resolved for its own
-  // oversampling (same K, alpha/beta as nufft.py:139-149 would pick) -- checked
-  // as accurate too.  Otherwise refuse loudly instead of returning a silently
-  // different answer.
-  if ((mode == 0 || mode == 3) && (!std::isnan(d->spec_alpha) || !std::isnan(d->spec_beta))) {
+  // Reproducing the reference's answer.  The GPU grids are powers of two, the reference's are even
+  // 11-smooth lengths (nufft.py:83-89), and the fast kernels use identities that hold to the
+  // window's accuracy only (a half-bin shifted interpolation grid, one interpolation for +-l, the
+  // half spectrum: at targets with an integer c*kappa the reference's floor() picks tap windows for
+  // +kappa and -kappa that are not mirror images, and its Hermitian symmetrisation averages them,
+  // recon.py:218-222).  So the fast path needs a window that makes the transform exact to well
+  // below the parity bar (float64 probe, window_relative_error) at the reference's length AND at
+  // the GPU's:
+  //  * inaccurate at the reference's length (small K, or a poorly chosen explicit alpha / beta): the
+  //    reference's answer carries that window's approximation error, which depends on the grid
+  //    length and on the tap window -- the plan runs on the reference's lengths with the reference's
+  //    own tap sums (reflen.cu);
+  //  * accurate there but an explicit (alpha, beta) loses accuracy at the GPU's length: the window is
+  //    resolved for the GPU's oversampling (same K, alpha / beta as nufft.py:139-149 picks) if that
+  //    is accurate, else the plan runs on the reference's lengths too.
+  // Plans that cannot run on the reference's lengths (sharded, standalone NedPlan) refuse instead of
+  // returning a different answer.
+  if (can_ref_len) {  // PATFFT_FORCE_REF_LEN=1: every plan on the reference's lengths (testing)
+    const char* e = std::getenv("PATFFT_FORCE_REF_LEN");
+    if (e && std::atoi(e) != 0) P->ref_len = true;
+  }
+  const bool explicit_window = !std::isnan(d->spec_alpha) || !std::isnan(d->spec_beta);
+  // (the default family -- auto alpha / beta, K >= 6, c >= 2 -- is exact to ~1e-11: no probe)
+  if ((mode == 0 || mode == 3) && !P->ref_len && (explicit_window || K < 6 || c < 2.0)) {
     struct Probe { Window* w; int n, n_over, n_over_ref; };
     std::vector<Probe> probes;
     for (int a = 0; a < d->n_lat; ++a)
       probes.push_back({&P->win_lat[a], d->out_dims[a], n_over_lat[a], even_fast_len(c * d->out_dims[a])});
     if (mode != 3) probes.push_back({&P->win_t, n_ext, P->n_over_t, even_fast_len(c * n_ext)});
     constexpr double kWinTol = 1e-6;
-    for (const Probe& pr : probes) {
-      if (pr.n_over == pr.n_over_ref || pr.n_over > 8192) continue;
-      double e = window_relative_error(*pr.w, pr.n, pr.n_over);
-      Window wref, wsub;
-      if (!(e <= kWinTol) && pr.n_over_ref <= 8192 &&
-          resolve_window(c, K, d->spec_alpha, d->spec_beta, double(pr.n_over_ref) / pr.n, &wref, &err) &&
-          window_relative_error(wref, pr.n, pr.n_over_ref) <= kWinTol &&
-          resolve_window(c, K, NAN, NAN, double(pr.n_over) / pr.n, &wsub, &err) &&
-          window_relative_error(wsub, pr.n, pr.n_over) <= kWinTol) {
-        *pr.w = wsub;
-        e = 0.0;
+    // the accuracy depends on (c_eff, K, alpha, beta), hardly on the length: long axes are probed at 256
+    auto accuracy = [](Window w, int n, int n_over) {
+      if (n > 256) {
+        n_over = (int)std::lround(double(n_over) / n * 256.0);
+        n = 256;
+        w.c_eff = double(n_over) / n;
       }
-      if (!(e <= kWinTol) && mode == 0 && world == 1) {
-        // the reference's own answer carries this window's approximation error, which depends on
-        // the grid length: run the plan on the reference's lengths (reflen.cu)
+      return window_relative_error(w, n, n_over);
+    };
+    for (const Probe& pr : probes) {
+      Window wref, wsub;
+      if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(pr.n_over_ref) / pr.n, &wref, &err))
+        return fail(PATFFT_ERR_PARAMETER, err);
+      const double e_ref = accuracy(wref, pr.n, pr.n_over_ref);
+      double e = e_ref;
+      if (e_ref <= kWinTol && pr.n_over != pr.n_over_ref) {
+        e = accuracy(*pr.w, pr.n, pr.n_over);
+        if (!(e <= kWinTol) && explicit_window && resolve_window(c, K, NAN, NAN, double(pr.n_over) / pr.n, &wsub, &err) &&
+            accuracy(wsub, pr.n, pr.n_over) <= kWinTol) {
+          *pr.w = wsub;
+          e = 0.0;
+        }
+      }
+      if (e <= kWinTol) continue;
+      if (can_ref_len) {
         P->ref_len = true;
         break;
       }
-      if (!(e <= kWinTol)) {
-        char buf[320];
-        std::snprintf(buf, sizeof buf,
-                      "window (c=%g, K=%d, alpha=%g, beta=%g) loses accuracy at the GPU's power-of-two oversampled "
-                      "length %d (reference uses %d; probe error %.2e): use the default alpha/beta or a c with c*N a "
-                      "power of two",
-                      c, K, pr.w->alpha, pr.w->beta, pr.n_over, pr.n_over_ref, e);
-        return fail(PATFFT_ERR_UNSUPPORTED, buf);
-      }
+      if (mode == 3 && pr.n_over == pr.n_over_ref) continue;  // same grid, same gridding: same answer
+      char buf[400];
+      std::snprintf(buf, sizeof buf,
+                    "window (c=%g, K=%d, alpha=%g, beta=%g) is not accurate enough (probe error %.2e at the "
+                    "reference's oversampled length %d, GPU length %d) for a plan that cannot run on the "
+                    "reference's lengths (sharded / standalone NedPlan): its answer would differ from the "
+                    "reference's; use a larger K or the default alpha/beta",
+                    c, K, wref.alpha, wref.beta, e, pr.n_over_ref, pr.n_over);
+      return fail(PATFFT_ERR_UNSUPPORTED, buf);
     }
   }
   if (P->ref_len) {
@@ -896,6 +937,8 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     const int rows = P->N0 * P->N1h;
     nr.rows_blk = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)rows, 32768, ((int64_t)1 << 25) / P->n_over_t}));
     if ((rc = dalloc(&nr.fb, (size_t)nr.rows_blk * P->n_over_t))) return rc;
+    if ((rc = dalloc(&nr.ghd, (size_t)rows * T))) return rc;
+    lr.ghd = nr.ghd;
     int nl[1] = {P->n_over_t};
     CUFFT_TRY(cufftPlanMany(&nr.c2c, 1, nl, nl, 1, P->n_over_t, nl, 1, P->n_over_t, CUFFT_C2C, nr.rows_blk));
     nr.win = NerRefWindow{wt.alpha, wt.beta, 1.0 / psh0, wt.K};
@@ -1925,6 +1968,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->ner_ref.c2c) cufftDestroy(P->ner_ref.c2c);
   if (P->lat_ref.spec) cudaFree(P->lat_ref.spec);
   if (P->ner_ref.fb) cudaFree(P->ner_ref.fb);
+  if (P->ner_ref.ghd) cudaFree(P->ner_ref.ghd);
   for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_lat_flags, (void*)P->d_gh,
                   (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_tc_recs, (void*)P->d_tc_tiles, (void*)P->d_tc_counter, (void*)P->d_tc_a16, (void*)P->d_tc_off, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_pre, (void*)P->d_tw, (void*)P->d_jt0,

@@ -75,6 +75,7 @@ struct SpreadParams {
 struct LatRef {
   cufftHandle r2c = 0;     // (rows, cols) real-to-complex per time sample, stride T
   float2* spec = nullptr;  // [nrows][ncols / 2 + 1][T]
+  float2* ghd = nullptr;   // = NerRef::ghd
   int nyo = 0;             // ncols / 2 + 1
 };
 struct NerRefWindow {
@@ -84,6 +85,7 @@ struct NerRefWindow {
 struct NerRef {
   cufftHandle c2c = 0;     // length n_over, rows_blk rows per call
   float2* fb = nullptr;    // [rows_blk][n_over]
+  float2* ghd = nullptr;   // [N0][N1h][T] difference rows of the lateral Nyquist planes (reflen.cu)
   int rows_blk = 0;
   NerRefWindow win;
 };

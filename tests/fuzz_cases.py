@@ -1,0 +1,63 @@
+"""Seeded random reconstruction problems of odd shapes for the parity sweep
+(tests/test_gpu_fuzz.py, tools/fuzz_parity.py): 2D / 3D, non-power-of-two sizes,
+out_dims != n_lateral, upsample 1-3, sensors on the aperture edge, windows with any
+c / K and auto or explicit admissible (alpha, beta)."""
+import math
+
+import numpy as np
+
+from paper_1501_02946_b200 import synth
+
+SIZES = [8, 12, 16, 20, 24, 32, 40, 48, 64]
+
+
+def draw(seed):
+    rng = np.random.default_rng(seed)
+    nlat = int(rng.integers(1, 3))
+    nl = tuple(int(rng.choice(SIZES)) for _ in range(nlat))
+    nt = int(rng.choice([16, 24, 32, 40, 48, 64, 96, 128, 192]))
+    up = int(rng.choice([1, 1, 1, 2, 3]))
+    dt = float(rng.choice([20e-9, 40e-9, 60e-9]))
+    m = int(np.prod(nl))
+    half = np.asarray(nl, float) * synth.PITCH / 2
+    pos = rng.uniform(-half, half, size=(m, nlat))
+    if rng.random() < 0.3:  # some sensors exactly on the aperture edges
+        k = rng.integers(0, m, size=max(1, m // 20))
+        pos[k, 0] = rng.choice([-half[0], half[0]], size=k.size)
+    depth = nt * synth.SOUND_SPEED * dt
+    if nlat == 2:
+        balls = [(rng.uniform(-0.5, 0.5) * half[0], rng.uniform(-0.5, 0.5) * half[1], rng.uniform(0.2, 0.7) * depth,
+                  rng.uniform(0.2e-3, 0.6e-3), rng.uniform(0.5, 1.0)) for _ in range(3)]
+        samples = synth.ball_traces(pos, nt, dt, synth.SOUND_SPEED, balls)
+    else:
+        t = np.arange(nt) * dt
+        dist = np.hypot(pos[:, 0] - 0.3e-3, 0.4 * depth)
+        samples = np.exp(-((t[None, :] - dist[:, None] / synth.SOUND_SPEED) ** 2) / (2 * (2 * dt) ** 2))
+    samples = samples + 1e-3 * rng.standard_normal(samples.shape)
+    w = np.full(m, float(np.prod(np.asarray(nl) * synth.PITCH)) / m)
+    out_dims = None
+    if rng.random() < 0.3:
+        out_dims = tuple(int(rng.choice([s for s in SIZES if s <= 2 * x])) for x in nl)
+    c = float(rng.choice([1.5, 2.0, 2.0, 2.5, 3.0]))
+    K = int(rng.integers(2, 9))
+    alpha = beta = None
+    if rng.random() < 0.4:
+        lo, hi = max(c, math.pi) * 1.02, math.pi * (2 * c - 1) * 0.98
+        if hi > lo:
+            alpha = float(rng.uniform(lo, hi))
+            beta = float(rng.uniform(0.3, 1.2) * K / c)
+    return dict(positions=pos, weights=w, samples=samples, dt=dt, n_lateral=nl, out_dims=out_dims, upsample=up,
+                c=c, K=K, alpha=alpha, beta=beta,
+                desc=f"seed {seed}: nl={nl} nt={nt} up={up} out_dims={out_dims} c={c} K={K} alpha={alpha} beta={beta}")
+
+
+def window_dynamic_range(case):
+    """psi(0) / psi(pi) of the explicit window: the deapodisation and the NER pre-window amplify the
+    float32 rounding of the gridding / FFTs by this factor towards the Nyquist frequencies (4.6 for
+    the reference's default window)."""
+    if case["alpha"] is None or case["beta"] is None:
+        return 1.0
+    from scipy.special import i0
+
+    a, b = case["alpha"], case["beta"]
+    return float(i0(b * a) / i0(b * math.sqrt(max(a * a - math.pi ** 2, 0.0))))
