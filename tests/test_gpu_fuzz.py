@@ -44,3 +44,26 @@ def test_gpu_random_shapes_and_windows_match_oracle(seed0):
         assert got.values.shape == want.shape and err <= tol, f"{cs['desc']}: rel-L2 {err:.2e}"
         worst, n = max(worst, err), n + 1
     print(f"fuzz seeds {seed0}..{seed0 + 39}: {n} reconstructions, worst rel-L2 {worst:.2e}")
+
+
+def test_gpu_fast_path_random_problems_match_oracle():
+    """Power-of-two problems on the fast kernels: random layouts (uniform, clustered, sensors on a
+    few grid lines), more sensors than grid points, amplitudes 1e-30 .. 1e30, a few sensors 1e4
+    louder or quieter, out_dims, upsample, K = 4 / 6 / 8."""
+    from fuzz_cases import draw_fast
+
+    worst = 0.0
+    for seed in range(5000, 5030):
+        cs = draw_fast(seed)
+        spec = (cs["c"], cs["K"], None, None)
+        want, _ = O.reconstruct_nedner(cs["positions"], cs["weights"], cs["samples"], cs["dt"], synth.SOUND_SPEED,
+                                       synth.PITCH, cs["n_lateral"], out_dims=cs["out_dims"], upsample=cs["upsample"],
+                                       spec=spec)
+        rec = pb.SensorRecord(cs["positions"], cs["weights"], cs["samples"], cs["dt"], synth.SOUND_SPEED, synth.PITCH,
+                              cs["n_lateral"])
+        got = pb.reconstruct_nedner(rec, out_dims=cs["out_dims"], upsample=cs["upsample"], spec=pb.WindowSpec(*spec))
+        err = rel_l2(got.values, want)
+        print(f"{err:.2e} {cs['desc']}")
+        assert got.values.shape == want.shape and err <= 1e-4, f"{cs['desc']}: rel-L2 {err:.2e}"
+        worst = max(worst, err)
+    print(f"fast-path fuzz: worst rel-L2 {worst:.2e}")
