@@ -279,7 +279,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // A window that is admissible at the reference's effective oversampling (checked above) can be
   // inadmissible at the GPU's larger power-of-two one (alpha must exceed c_eff, nufft.py:125-127):
   // such a plan runs on the reference's lengths (reflen.cu) instead of being refused.
-  const bool can_ref_len = mode == 0 && world == 1;
+  const bool can_ref_len = (mode == 0 || mode == 1) && world == 1;  // (mode 1: the NER axis only)
   int n_over_lat[2] = {1, 1};
   for (int a = 0; a < d->n_lat; ++a) {
     int64_t n = next_pow2((int64_t)std::ceil(c * d->out_dims[a]));
@@ -345,10 +345,10 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   }
   const bool explicit_window = !std::isnan(d->spec_alpha) || !std::isnan(d->spec_beta);
   // (the default family -- auto alpha / beta, K >= 6, c >= 2 -- is exact to ~1e-11: no probe)
-  if ((mode == 0 || mode == 3) && !P->ref_len && (explicit_window || K < 6 || c < 2.0)) {
+  if ((mode == 0 || mode == 1 || mode == 3) && !P->ref_len && (explicit_window || K < 6 || c < 2.0)) {
     struct Probe { Window* w; int n, n_over, n_over_ref; };
     std::vector<Probe> probes;
-    for (int a = 0; a < d->n_lat; ++a)
+    for (int a = 0; a < d->n_lat && mode != 1; ++a)
       probes.push_back({&P->win_lat[a], d->out_dims[a], n_over_lat[a], even_fast_len(c * d->out_dims[a])});
     if (mode != 3) probes.push_back({&P->win_t, n_ext, P->n_over_t, even_fast_len(c * n_ext)});
     constexpr double kWinTol = 1e-6;
@@ -392,7 +392,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     }
   }
   if (P->ref_len) {
-    for (int a = 0; a < d->n_lat; ++a) {
+    for (int a = 0; a < d->n_lat && mode == 0; ++a) {
       n_over_lat[a] = even_fast_len(c * d->out_dims[a]);
       if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_lat[a]) / d->out_dims[a], &P->win_lat[a],
                           &err))

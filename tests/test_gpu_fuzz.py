@@ -67,3 +67,37 @@ def test_gpu_fast_path_random_problems_match_oracle():
         assert got.values.shape == want.shape and err <= 1e-4, f"{cs['desc']}: rel-L2 {err:.2e}"
         worst = max(worst, err)
     print(f"fast-path fuzz: worst rel-L2 {worst:.2e}")
+
+
+def test_gpu_equispaced_and_interp_random_problems_match_oracle():
+    """reconstruct_equispaced (NER on the time axis only; any window, incl. inaccurate ones ->
+    reference lengths) and reconstruct_interp_fft on shuffled complete grids."""
+    worst = 0.0
+    for seed in range(7000, 7040):
+        rng = np.random.default_rng(seed)
+        nlat = int(rng.integers(1, 3))
+        nl = tuple(int(rng.choice([8, 16, 32])) for _ in range(nlat))
+        nt = int(rng.choice([16, 32, 64, 128]))
+        up = int(rng.choice([1, 1, 2, 3]))
+        dt = float(rng.choice([20e-9, 40e-9]))
+        axes = [(np.arange(n) - n // 2) * synth.PITCH for n in nl]
+        mesh = np.meshgrid(*axes, indexing="ij")
+        pos = np.stack([m.ravel() for m in mesh], axis=-1)
+        pos = pos[rng.permutation(pos.shape[0])]
+        samples = rng.standard_normal((pos.shape[0], nt)) * np.exp(-np.arange(nt) / (0.3 * nt))[None, :]
+        w = np.full(pos.shape[0], float(np.prod([n * synth.PITCH for n in nl])) / pos.shape[0])
+        c = float(rng.choice([1.5, 2.0, 2.0, 2.5]))
+        K = int(rng.integers(2, 9))
+        rec = pb.SensorRecord(pos, w, samples, dt, synth.SOUND_SPEED, synth.PITCH, nl)
+        for kind in ("nufft", "interp"):
+            want, _ = O.reconstruct_equispaced(pos, samples, dt, synth.SOUND_SPEED, synth.PITCH, nl, upsample=up,
+                                               spec=(c, K, None, None), time_eval=kind)
+            if kind == "nufft":
+                got = pb.reconstruct_equispaced(rec, upsample=up, spec=pb.WindowSpec(c=c, K=K))
+            else:
+                got = pb.reconstruct_interp_fft(rec, upsample=up)
+            err = rel_l2(got.values, want)
+            assert got.values.shape == want.shape and err <= 1e-4, \
+                f"seed {seed} {kind}: nl={nl} nt={nt} up={up} c={c} K={K}: rel-L2 {err:.2e}"
+            worst = max(worst, err)
+    print(f"equispaced / interp fuzz: worst rel-L2 {worst:.2e}")

@@ -124,14 +124,33 @@ def test_general_schedule_stages_match_single_gpu(world, case):
     """The general multi-GPU schedule (sliced C plans: any even N_t, any upsample, uneven time
     slices; parallel.GeneralShardedNedNer's layouts) with the ranks emulated one after another on
     one GPU, against the single-GPU reconstruction and the oracle."""
+    from test_sharded_gloo import _general_case
+
+    rec, out_dims, up = _general_case(case)
+    _emulate_general_schedule(world, rec, out_dims, up, f"{case}")
+
+
+@pytest.mark.parametrize("seed", range(9000, 9012))
+def test_general_schedule_random_problems(seed):
+    """Random shapes (tests/fuzz_cases.py, default window) at random world sizes."""
+    from fuzz_cases import draw
+
+    cs = draw(seed)
+    rng = np.random.default_rng(seed)
+    nt = cs["samples"].shape[1]
+    world = int(rng.integers(2, min(6, nt // 2) + 1))
+    rec = synth.SyntheticRecord(cs["positions"], cs["weights"], cs["samples"], cs["dt"], synth.SOUND_SPEED, synth.PITCH,
+                                cs["n_lateral"])
+    _emulate_general_schedule(world, rec, cs["out_dims"], cs["upsample"], cs["desc"])
+
+
+def _emulate_general_schedule(world, rec, out_dims, up, what):
     import torch
 
     from oracle import nedner_oracle as O
     from paper_1501_02946_b200.parallel import GpuSliceStages, SliceLayout
     from paper_1501_02946_b200.recon import _out_dims
-    from test_sharded_gloo import _general_case
 
-    rec, out_dims, up = _general_case(case)
     want = pb.reconstruct_nedner(rec.as_record(), out_dims=out_dims, upsample=up).values
     nl = tuple(rec.n_lateral)
     dims = _out_dims(nl, out_dims)
@@ -174,5 +193,5 @@ def test_general_schedule_stages_match_single_gpu(world, case):
     oracle, _ = O.reconstruct_nedner(rec.positions, rec.weights, rec.samples, rec.dt, rec.sound_speed, rec.dx,
                                      rec.n_lateral, out_dims=out_dims, upsample=up)
     e1, e2 = rel_l2(got, want), rel_l2(got, oracle)
-    print(f"general schedule world {world} {case}: rel-L2 vs single GPU {e1:.2e}, vs oracle {e2:.2e}")
+    print(f"general schedule world {world} {what}: rel-L2 vs single GPU {e1:.2e}, vs oracle {e2:.2e}")
     assert got.shape == want.shape and e1 <= 5e-6 and e2 <= 1e-4
