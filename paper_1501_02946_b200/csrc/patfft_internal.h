@@ -59,7 +59,8 @@ struct SpreadParams {
   const int4* tc_tiles = nullptr;   // per tile (launch order): {first record, records (multiple of 16), row0, col0}
   int tc_ntiles = 0, tc_nonempty = 0;  // tiles (the non-empty ones first, longest first)
   int tc_n = 0, tc_tblocks = 0;       // time samples per block, time blocks per launch
-  int* tc_counter = nullptr;          // [0] work-item counter, [1] |sample| max bits (zeroed before each launch)
+  int* tc_counter = nullptr;          // 8 ints: work counters, |sample| max bits, redo flag, scale hint (spread_tc.cu)
+  int tc_pass = 0, tc_track = 0, tc_scale_src = 1;  // fp16 gridding: launch 0 / 1, record the max, scale source slot
   // fp16 two-term operands (kind::f16): records pre-scaled by 2^tc_wexp at plan
   // time, samples by a power of two from their max per launch, undone in the epilogue
   int tc_f16 = 0, tc_wexp = 0;
@@ -272,7 +273,7 @@ struct patfft_nedner_plan {
   float* d_recs = nullptr;
   float* d_tc_recs = nullptr;   // tensor-core gridding records (spread_tc.cu)
   int4* d_tc_tiles = nullptr;
-  int* d_tc_counter = nullptr;  // 2 ints
+  int* d_tc_counter = nullptr;  // 8 ints (zero-initialised: no scale hint yet)
   uint4* d_tc_a16 = nullptr;
   bool tc_tma_store = false;
   CUtensorMap tc_gmap;

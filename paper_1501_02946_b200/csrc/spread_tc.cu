@@ -467,6 +467,10 @@ __global__ void absmax_kernel(const float* __restrict__ s, int M, int T, int tb,
   if (lane == 0 && m) atomicMax(out, m);
 }
 
+// p.tc_counter slots (ints): work-item counters of the two launches, max |sample| bits seen, redo flag
+// (zeroed before every gridding) and the scale hint, which persists from call to call
+constexpr int kCtrWork0 = 0, kCtrSeen = 1, kCtrWork1 = 2, kCtrRedo = 3, kCtrHint = 4;
+
 // Work items of the fp16 kernel, resolved by thread 0 into a shared ring:
 // {tile's first record / 16, stages, row0, col0, time block}; stages == 0
 // marks the end.  Thread 0 claims items two ahead (atomicAdd result and the
@@ -496,11 +500,11 @@ __device__ __forceinline__ int4 item16_tile(const SpreadParams& p, int w) {
   return w < p.tc_nonempty * p.tc_tblocks ? __ldg(&p.tc_tiles[w / p.tc_tblocks]) : make_int4(0, 0, 0, 0);
 }
 // next item into ring slot k: B's resolved item; B <- C (issue its tile load); C <- new claim
-__device__ __forceinline__ void claim16(const SpreadParams& p, Claimer16& q, Item16* ring, int k) {
+__device__ __forceinline__ void claim16(const SpreadParams& p, Claimer16& q, Item16* ring, int k, int* counter) {
   ring[k & (kRing - 1)] = item16_make(p, q.wb, q.tb_);
   q.wb = q.wc;
   q.tb_ = item16_tile(p, q.wb);
-  q.wc = atomicAdd(p.tc_counter, 1);
+  q.wc = atomicAdd(counter, 1);
 }
 struct Cursor16 {
   int k, c;  // ring position, stage within the item
@@ -563,6 +567,10 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q4 = warp & 3;
+  // speculative sample scale (go_tc16): the second launch runs only when the check after the first
+  // one found the scale hint in the wrong binade
+  if (p.tc_pass == 1 && p.tc_counter[kCtrRedo] == 0) return;
+  int* const work_counter = p.tc_counter + (p.tc_pass == 1 ? kCtrWork1 : kCtrWork0);
 
   // ---- empty tiles (no sensor meets them): zeros
   for (int i = p.tc_nonempty + blockIdx.x; i < p.tc_ntiles; i += gridDim.x) {
@@ -576,9 +584,9 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
   Cursor16 cur, cs, cr;  // stage being built, loads (+2, warp 1), offsets (+3, thread 0)
   Claimer16 claim;
   if (tid == 0) {
-    const int w0 = atomicAdd(p.tc_counter, 1);
-    claim.wb = atomicAdd(p.tc_counter, 1);
-    claim.wc = atomicAdd(p.tc_counter, 1);
+    const int w0 = atomicAdd(work_counter, 1);
+    claim.wb = atomicAdd(work_counter, 1);
+    claim.wc = atomicAdd(work_counter, 1);
     ring[0] = item16_make(p, w0, item16_tile(p, w0));
     claim.tb_ = item16_tile(p, claim.wb);
   }
@@ -610,7 +618,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
   // scales: samples by 2^es (max |s| * 2^es < 2^14), output by 2^-(wexp + es)
   float s_scale, o_scale;
   {
-    const float mx = __uint_as_float(p.tc_counter[1]);
+    const float mx = __uint_as_float(p.tc_counter[p.tc_scale_src]);
     int es = 0;
     if (mx > 0.f && mx <= 3.4e38f) {
       int e;
@@ -633,7 +641,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
     if (!c16_valid(cr) || ++cr.c < cr.it.nch) return;
     ++cr.k;
     cr.c = 0;
-    claim16(p, claim, ring, cr.k);
+    claim16(p, claim, ring, cr.k, work_counter);
     cr.it = ring[cr.k & (kRing - 1)];
   };
   // warp 1 (all lanes, uniform cursor): A operands and the 16 sample rows of stage g,
@@ -670,6 +678,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
 
   // B builder: thread = (time sample tq and tq + N/2, sensor octet ko)
   const int tq = tid % NH, ko = tid / NH;
+  float seen_max = 0.f;
 
   auto epilogue = [&](int g) {
     const int t0 = p.t_begin + cur.it.tb * N;
@@ -754,6 +763,9 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
         float w[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) w[j] = sr[(8 * kb + j) * N + n];
+        if (p.tc_track)  // max |sample| of everything this launch grids (checked against the scale hint)
+          seen_max = fmaxf(seen_max, fmaxf(fmaxf(fmaxf(fabsf(w[0]), fabsf(w[1])), fmaxf(fabsf(w[2]), fabsf(w[3]))),
+                                           fmaxf(fmaxf(fabsf(w[4]), fabsf(w[5])), fmaxf(fabsf(w[6]), fabsf(w[7])))));
         uint4 bh, bl;
         split_f16x8_scaled(w, s_scale, bh, bl);
         *reinterpret_cast<uint4*>(bo + kb * B_LBO + n * 16) = bh;
@@ -813,8 +825,22 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
     if (cur.c == cur.it.nch - 1) epilogue(g);
     c16_next(cur, ring);
   }
+  if (p.tc_track) {
+    const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(seen_max));  // non-negative floats order as uints
+    if (lane == 0 && mb) atomicMax(reinterpret_cast<unsigned*>(p.tc_counter + kCtrSeen), mb);
+  }
   if (p.tc_tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
+
+// After the first gridding launch: is the scale hint it used in the binade of the maximum it saw?
+// (Same exponent field <=> the launch used exactly the scale the max pass would have given, so the
+// result does not depend on the hint's history.)  Otherwise the second launch redoes the gridding.
+__global__ void check_scale_kernel(int* __restrict__ ctr) {
+  const unsigned seen = (unsigned)ctr[kCtrSeen], hint = (unsigned)ctr[kCtrHint];
+  const bool ok = seen == 0 || (seen >> 23) == (hint >> 23);
+  ctr[kCtrRedo] = ok ? 0 : 1;
+  if (seen) ctr[kCtrHint] = (int)seen;
 }
 
 template <int N>
@@ -832,11 +858,38 @@ cudaError_t go_tc16(const SpreadParams& p, cudaStream_t s) {
   SpreadParams q = p;
   q.tc_tblocks = (p.t_end - p.t_begin) / N;
   const int blocks = std::min(q.tc_ntiles * q.tc_tblocks, 2 * sms);
-  if ((err = cudaMemsetAsync(q.tc_counter, 0, 2 * sizeof(int), s))) return err;
-  absmax_kernel<<<4 * sms, 256, 0, s>>>(p.samples, p.tc_m, p.T, p.t_begin, p.t_end,
-                                        reinterpret_cast<unsigned*>(q.tc_counter + 1));
+  if ((err = cudaMemsetAsync(q.tc_counter, 0, kCtrHint * sizeof(int), s))) return err;  // all but the hint
+  if (blocks <= 0 || q.tc_tblocks <= 0) return cudaSuccess;
+  // The sample scale 2^es needs max |sample| of the launch.  PATFFT_TC16_SPECULATE=0: a max pass first
+  // (one extra read of the samples, 47 us at cfg4).  Default: the launch uses the maximum the
+  // previous launch of this plan saw as a hint, records the maximum it sees itself, and a one-thread
+  // check compares their binades; only if they differ (first call, data of another magnitude) a
+  // second launch redoes the gridding with the right scale -- otherwise it exits at once.  Same
+  // scale either way, so the result is bit-identical to the max-pass form.
+  static const bool speculate = [] {
+    const char* e = std::getenv("PATFFT_TC16_SPECULATE");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  if (!speculate) {
+    absmax_kernel<<<4 * sms, 256, 0, s>>>(p.samples, p.tc_m, p.T, p.t_begin, p.t_end,
+                                          reinterpret_cast<unsigned*>(q.tc_counter + kCtrSeen));
+    if ((err = cudaGetLastError())) return err;
+    q.tc_scale_src = kCtrSeen;
+    q.tc_track = 0;
+    q.tc_pass = 0;
+    k<<<blocks, kThreadsTC, smem, s>>>(q);
+    return cudaGetLastError();
+  }
+  q.tc_scale_src = kCtrHint;
+  q.tc_track = 1;
+  q.tc_pass = 0;
+  k<<<blocks, kThreadsTC, smem, s>>>(q);
   if ((err = cudaGetLastError())) return err;
-  if (blocks > 0 && q.tc_tblocks > 0) k<<<blocks, kThreadsTC, smem, s>>>(q);
+  check_scale_kernel<<<1, 1, 0, s>>>(q.tc_counter);
+  if ((err = cudaGetLastError())) return err;
+  q.tc_track = 0;
+  q.tc_pass = 1;
+  k<<<blocks, kThreadsTC, smem, s>>>(q);
   return cudaGetLastError();
 }
 

@@ -204,6 +204,32 @@ def test_gpu_single_launch_lateral_matches_two_kernel_form(nl, nt, slots):
     assert err <= TOL
 
 
+def test_gpu_gridding_scale_hint_history_does_not_change_results():
+    """fp16 gridding: the sample scale is speculated from the previous call's maximum and verified
+    on the device (spread_tc.cu, check_scale_kernel); a wrong guess re-runs the gridding.  Whatever
+    the history of a plan -- first call, data 1e6 louder, 1e-9 quieter, zeros, back again -- each
+    volume is bit-identical to the one a fresh plan returns (whose first call always re-runs)."""
+    s = synth.make_3d(4, 256, 128, 80e-9, "clustered", 20, sigma=8e-3)  # cfg4's layout: fp16 form
+    def mk():
+        os.environ["PATFFT_SPREAD_F16_MIN_ITEMS"] = "0"  # the fp16 form even for this short record
+        try:
+            return pb.NedNerPlan(s.positions, s.weights, 128, s.dt, s.sound_speed, s.dx, s.n_lateral)
+        finally:
+            os.environ.pop("PATFFT_SPREAD_F16_MIN_ITEMS", None)
+
+    plan = mk()
+    assert plan.window_info()["lateral_taps"] == 8
+    scales = [1.0, 1.0, 1e6, 3e6, 1e-9, 0.0, 1.0, 1.9, 2.1]
+    outs = [plan.execute(s.samples * a)[0].copy() for a in scales]
+    for a, got in zip(scales, outs):
+        fresh = mk().execute(s.samples * a)[0]
+        assert np.array_equal(got, fresh), f"scale {a}: result depends on the plan's history"
+    want, _ = O.reconstruct_nedner(s.positions, s.weights, s.samples, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    err = rel_l2(outs[0], want)
+    print(f"scale-hint history: 9 calls bit-identical to fresh plans, rel-L2 vs oracle {err:.3e}")
+    assert err <= TOL and not np.any(outs[5])
+
+
 def test_gpu_window_selection():
     """Auto (alpha, beta) windows with K > 4 run with the float32-grade 8 taps;
     explicit windows and K <= 4 keep what was asked (nufft.py:133-149)."""
