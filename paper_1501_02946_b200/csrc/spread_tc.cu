@@ -471,6 +471,14 @@ __global__ void absmax_kernel(const float* __restrict__ s, int M, int T, int tb,
 // (zeroed before every gridding) and the scale hint, which persists from call to call
 constexpr int kCtrWork0 = 0, kCtrSeen = 1, kCtrWork1 = 2, kCtrRedo = 3, kCtrHint = 4;
 
+// The sample scale is 2^(14 - 4 b) with b = ceil(e / 4) the 4-binade bucket of max |sample| in
+// [2^(e-1), 2^e): the scaled maximum lies in [2^10, 2^14).  Quantising the exponent makes a scale
+// hint from the previous call (go_tc16) valid for a 16x range of maxima instead of 2x.
+__host__ __device__ __forceinline__ int scale_bucket(unsigned float_bits) {
+  const int e = (int)((float_bits >> 23) & 0xffu) - 126;  // frexp exponent of a normal float
+  return e >= 0 ? (e + 3) / 4 : -((-e) / 4);              // ceil(e / 4)
+}
+
 // Work items of the fp16 kernel, resolved by thread 0 into a shared ring:
 // {tile's first record / 16, stages, row0, col0, time block}; stages == 0
 // marks the end.  Thread 0 claims items two ahead (atomicAdd result and the
@@ -620,11 +628,7 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
   {
     const float mx = __uint_as_float(p.tc_counter[p.tc_scale_src]);
     int es = 0;
-    if (mx > 0.f && mx <= 3.4e38f) {
-      int e;
-      frexpf(mx, &e);
-      es = 14 - e;
-    }
+    if (mx > 0.f && mx <= 3.4e38f) es = 14 - 4 * scale_bucket(p.tc_counter[p.tc_scale_src]);
     es = min(es, 126 - p.tc_wexp);
     s_scale = ldexpf(1.f, es);
     o_scale = ldexpf(1.f, -(p.tc_wexp + es));
@@ -833,12 +837,12 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
 }
 
-// After the first gridding launch: is the scale hint it used in the binade of the maximum it saw?
-// (Same exponent field <=> the launch used exactly the scale the max pass would have given, so the
+// After the first gridding launch: is the scale hint it used in the 4-binade bucket of the maximum it
+// saw?  (Same bucket <=> the launch used exactly the scale the max pass would have given, so the
 // result does not depend on the hint's history.)  Otherwise the second launch redoes the gridding.
 __global__ void check_scale_kernel(int* __restrict__ ctr) {
   const unsigned seen = (unsigned)ctr[kCtrSeen], hint = (unsigned)ctr[kCtrHint];
-  const bool ok = seen == 0 || (seen >> 23) == (hint >> 23);
+  const bool ok = seen == 0 || (hint != 0 && scale_bucket(seen) == scale_bucket(hint));
   ctr[kCtrRedo] = ok ? 0 : 1;
   if (seen) ctr[kCtrHint] = (int)seen;
 }
@@ -863,7 +867,7 @@ cudaError_t go_tc16(const SpreadParams& p, cudaStream_t s) {
   // The sample scale 2^es needs max |sample| of the launch.  PATFFT_TC16_SPECULATE=0: a max pass first
   // (one extra read of the samples, 47 us at cfg4).  Default: the launch uses the maximum the
   // previous launch of this plan saw as a hint, records the maximum it sees itself, and a one-thread
-  // check compares their binades; only if they differ (first call, data of another magnitude) a
+  // check compares their 4-binade buckets; only if they differ (first call, data 16x off) a
   // second launch redoes the gridding with the right scale -- otherwise it exits at once.  Same
   // scale either way, so the result is bit-identical to the max-pass form.
   static const bool speculate = [] {
