@@ -406,7 +406,7 @@ def run_sharded_arm(args):
     n_over = [1 << int(np.ceil(np.log2(2 * n))) for n in rec.n_lateral]
     spread_bytes = 4.0 * tr * (rec.samples.shape[0] + int(np.prod(n_over)))
     peak, peak_kind = _peaks()
-    roofline = {"kernel": "spread (per rank: absmax_kernel + spread_tc16_kernel on the rank's time slice)",
+    roofline = {"kernel": "spread (per rank: spread_tc16_kernel on the rank's time slice + scale check)",
                 "bound": "hbm", "achieved": spread_bytes / (spread_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": spread_bytes / (spread_ms / 1e3) / 1e9 / peak, "peak_source": peak_kind, "traffic": None,
                 "algorithmic_bytes": spread_bytes, "launch_ms": spread_ms}
@@ -438,8 +438,8 @@ def run_sharded_arm(args):
             "clocks": clk, "roofline": roofline,
             "e2e": {"value": vox / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * host_slice.size * world,
                     "d2h_bytes_per_step": 8 * int(np.prod(pin_out.shape)) * world, "ms_per_step": 1e3 * e2e_s},
-            "gpu_launches": (4 + 2 * sh.C + sh.B) * args.steps,
-            "gpu_launches_note": (f"per rank per step: absmax (sample scale of the fp16 gridding) + spread, colfft + "
+            "gpu_launches": (5 + 2 * sh.C + sh.B) * args.steps,
+            "gpu_launches_note": (f"per rank per step: spread + scale check + conditional re-spread (fp16 gridding), colfft + "
                                   f"rowfft per time piece ({sh.C} pieces), ner per row block ({sh.B} blocks), inv_col "
                                   f"+ inv_c2r (+1 flush outside the events); grouped NCCL send/recv per piece and per "
                                   f"block (none at world 1)"),
@@ -651,7 +651,12 @@ def run_gpu_arm(args):
     sp_ms = per["spread"]
     taps = 12 ** len(rec.n_lateral)
     useful = 2.0 * rec.positions.shape[0] * taps * rec.samples.shape[1]  # useful FLOPs: 2 x M x (2K)^d x T
-    spread = {"kernel": {2: "spread_tc16_kernel (tcgen05 kind::f16, two-term fp16 split) + absmax_kernel",
+    spec_on = os.environ.get("PATFFT_TC16_SPECULATE", "1") != "0"
+    spread = {"kernel": {2: "spread_tc16_kernel (tcgen05 kind::f16, two-term fp16 split) + "
+                            + ("check_scale_kernel + a second gridding launch that exits at once when the sample-scale "
+                               "hint of the plan's previous call was right (it is on every timed step: same record; "
+                               "a miss re-runs the gridding, +0.34 ms at cfg4, with bit-identical results)"
+                               if spec_on else "absmax_kernel"),
                          1: "spread_tc_kernel (tcgen05 3xTF32)"}.get(int(info[0]), "spread_tp_kernel (SIMT FP32)"),
               "launch_ms": sp_ms, "algorithmic_bytes": sbytes["spread"],
               "hbm": {"achieved": sbytes["spread"] / (sp_ms / 1e3) / 1e9, "peak": peak,

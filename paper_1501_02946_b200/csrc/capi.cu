@@ -2047,7 +2047,13 @@ int patfft_nedner_stage_bytes(const patfft_nedner_plan* P, double* bytes, int n)
 int patfft_nedner_launches_per_execute(const patfft_nedner_plan* P, int* own, int* library) {
   if (!P) return fail(PATFFT_ERR_PARAMETER, "null plan");
   int o = 4;  // spread, colfft, rowfft, ner
-  if (P->tc_ntiles > 0 && P->tc_f16) o += 1;  // absmax_kernel (sample scale of the fp16 gridding)
+  if (P->tc_ntiles > 0 && P->tc_f16) {
+    // fp16 gridding (spread_tc.cu, go_tc16): speculative sample scale = gridding + check_scale_kernel +
+    // a second gridding launch that exits at once unless the hint missed; PATFFT_TC16_SPECULATE=0:
+    // absmax_kernel + gridding
+    const char* e = std::getenv("PATFFT_TC16_SPECULATE");
+    o += (e && std::atoi(e) == 0) ? 1 : 2;
+  }
   int lib = 0;
   if (P->custom_inverse) o += (P->N0u > 1 ? 2 : 1);
   else lib += 1;  // cuFFT C2R (may be several kernels)
