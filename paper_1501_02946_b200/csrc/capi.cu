@@ -718,10 +718,11 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
       return e ? std::atoi(e) != 0 : true;
     }();
     // (the fp16 kernel's longer per-item pipeline only pays off with many work
-    // items: measured cfg4 (8192 items) 0.563 -> 0.481 ms, cfg3 (1024) even, cfg2 (128) 2.4x slower)
+    // items: measured cfg4 (8192 items) 0.563 -> 0.481 ms, cfg3 (1024) 0.074 -> 0.066 ms once the max
+    // pass was gone (0.193 -> 0.180 ms/step), cfg2 (128) 2.2x slower)
     const int64_t f16_min_items = [] {
       const char* e = std::getenv("PATFFT_SPREAD_F16_MIN_ITEMS");
-      return e ? std::atoll(e) : (int64_t)2048;
+      return e ? std::atoll(e) : (int64_t)1024;
     }();
     P->tc_f16 = (f16_on && (int64_t)P->tc_nonempty * (T / P->tc_n) >= f16_min_items) ? 1 : 0;
     if (P->tc_f16) {
