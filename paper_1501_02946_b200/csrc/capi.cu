@@ -111,6 +111,7 @@ void set_tc(const patfft_nedner_plan* P, SpreadParams& sp) {
   sp.tc_ntiles = P->tc_ntiles;
   sp.tc_nonempty = P->tc_nonempty;
   sp.tc_counter = P->d_tc_counter;
+  sp.tc_batch_scale = P->batch_scale ? 1 : 0;
   sp.tc_n = P->tc_n;
   sp.tc_f16 = P->tc_f16;
   sp.tc_wexp = P->tc_wexp;
@@ -1422,11 +1423,15 @@ static int execute_graphed(patfft_nedner_plan* P, int n_frames, const float* sam
                            cudaStream_t st) {
   const size_t in_sz = (size_t)P->M * P->T, out_sz = (size_t)P->N0u * P->N1u * P->Tu;
   auto enqueue = [&]() -> int {
-    for (int f = 0; f < n_frames; ++f) {
-      int rc = execute_device_locked(P, samples + f * in_sz, image + f * out_sz, st);
-      if (rc) return rc;
-    }
-    return PATFFT_OK;
+    // frames of one batch: one max pass over all of them gives the fp16 gridding's sample scale,
+    // instead of a per-frame hint that misses whenever the frames' maxima differ by 16x
+    const bool batch = n_frames > 1 && P->tc_ntiles > 0 && P->tc_f16 && P->mode == 0 && !P->profiling;
+    if (batch) CUDA_TRY(spread_tc16_batch_max(samples, (int64_t)n_frames * P->M, P->T, P->d_tc_counter, st));
+    P->batch_scale = batch;
+    int rc = PATFFT_OK;
+    for (int f = 0; f < n_frames && !rc; ++f) rc = execute_device_locked(P, samples + f * in_sz, image + f * out_sz, st);
+    P->batch_scale = false;
+    return rc;
   };
   if (P->profiling || !P->use_graphs) return enqueue();
   for (auto& g : P->graphs)

@@ -60,6 +60,7 @@ struct SpreadParams {
   int tc_ntiles = 0, tc_nonempty = 0;  // tiles (the non-empty ones first, longest first)
   int tc_n = 0, tc_tblocks = 0;       // time samples per block, time blocks per launch
   int* tc_counter = nullptr;          // 8 ints: work counters, |sample| max bits, redo flag, scale hint (spread_tc.cu)
+  int tc_batch_scale = 0;  // 1: the scale comes from the batch maximum (frames; spread_tc16_batch_max)
   int tc_pass = 0, tc_track = 0, tc_scale_src = 1;  // fp16 gridding: launch 0 / 1, record the max, scale source slot
   // fp16 two-term operands (kind::f16): records pre-scaled by 2^tc_wexp at plan
   // time, samples by a power of two from their max per launch, undone in the epilogue
@@ -146,6 +147,7 @@ struct NerParams {
 cudaError_t launch_spread(const SpreadParams& p, int K2, int R, int nblk, cudaStream_t s);
 cudaError_t launch_spread_tc(const SpreadParams& p, cudaStream_t s);
 cudaError_t spread_tc16_build(const float* recs, int nstages, void* a16, uint32_t* offs, cudaStream_t s);
+cudaError_t spread_tc16_batch_max(const float* samples, int64_t rows, int T, int* counters, cudaStream_t s);
 bool spread_tc_supported(int n_lat, int nrows, int ncols, int T);
 int spread_tc_block(int T);
 int spread_rows_per_group(int n_lat, int K2);
@@ -255,6 +257,7 @@ struct patfft_nedner_plan {
   // sliced plan (general multi-GPU schedule): NED stages / lateral inverse on Tr (x up) samples,
   // NER on caller-provided row ranges with the full N_t
   bool sliced = false;
+  bool batch_scale = false;  // set while the frames of one batch are enqueued (execute_graphed)
   patfft::LatRef lat_ref;
   patfft::NerRef ner_ref;
 

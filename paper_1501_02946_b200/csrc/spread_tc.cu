@@ -470,6 +470,7 @@ __global__ void absmax_kernel(const float* __restrict__ s, int M, int T, int tb,
 // p.tc_counter slots (ints): work-item counters of the two launches, max |sample| bits seen, redo flag
 // (zeroed before every gridding) and the scale hint, which persists from call to call
 constexpr int kCtrWork0 = 0, kCtrSeen = 1, kCtrWork1 = 2, kCtrRedo = 3, kCtrHint = 4;
+constexpr int kCtrBatch = 5;  // max |sample| over a batch of frames (spread_tc16_batch_max), set by the caller
 
 // The sample scale is 2^(14 - 4 b) with b = ceil(e / 4) the 4-binade bucket of max |sample| in
 // [2^(e-1), 2^e): the scaled maximum lies in [2^10, 2^14).  Quantising the exponent makes a scale
@@ -874,6 +875,13 @@ cudaError_t go_tc16(const SpreadParams& p, cudaStream_t s) {
     const char* e = std::getenv("PATFFT_TC16_SPECULATE");
     return e ? std::atoi(e) != 0 : true;
   }();
+  if (p.tc_batch_scale) {  // frames of one batch share the scale of the batch's maximum (one max pass per batch)
+    q.tc_scale_src = kCtrBatch;
+    q.tc_track = 0;
+    q.tc_pass = 0;
+    k<<<blocks, kThreadsTC, smem, s>>>(q);
+    return cudaGetLastError();
+  }
   if (!speculate) {
     absmax_kernel<<<4 * sms, 256, 0, s>>>(p.samples, p.tc_m, p.T, p.t_begin, p.t_end,
                                           reinterpret_cast<unsigned*>(q.tc_counter + kCtrSeen));
@@ -912,6 +920,15 @@ int spread_tc_block(int T) {
 cudaError_t spread_tc16_build(const float* recs, int nstages, void* a16, uint32_t* offs, cudaStream_t s) {
   if (nstages <= 0) return cudaSuccess;
   build_a16_kernel<<<std::min(nstages, 148 * 8), kThreadsTC, 0, s>>>(recs, nstages, static_cast<uint4*>(a16), offs);
+  return cudaGetLastError();
+}
+
+// max |sample| over `rows` sensor rows (all frames of a batch) into the plan's batch-scale slot
+cudaError_t spread_tc16_batch_max(const float* samples, int64_t rows, int T, int* counters, cudaStream_t s) {
+  cudaError_t err = cudaMemsetAsync(counters + kCtrBatch, 0, sizeof(int), s);
+  if (err) return err;
+  absmax_kernel<<<4 * 148, 256, 0, s>>>(samples, (int)std::min<int64_t>(rows, INT32_MAX), T, 0, T,
+                                        reinterpret_cast<unsigned*>(counters + kCtrBatch));
   return cudaGetLastError();
 }
 
