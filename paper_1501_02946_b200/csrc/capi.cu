@@ -280,7 +280,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // A window that is admissible at the reference's effective oversampling (checked above) can be
   // inadmissible at the GPU's larger power-of-two one (alpha must exceed c_eff, nufft.py:125-127):
   // such a plan runs on the reference's lengths (reflen.cu) instead of being refused.
-  const bool can_ref_len = (mode == 0 || mode == 1) && world == 1;  // (mode 1: the NER axis only)
+  const bool can_ref_len = (mode == 0 || mode == 1 || mode == 3) && world == 1;  // (1: NER axis only; 3: lateral only)
   int n_over_lat[2] = {1, 1};
   for (int a = 0; a < d->n_lat; ++a) {
     int64_t n = next_pow2((int64_t)std::ceil(c * d->out_dims[a]));
@@ -377,11 +377,11 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
         }
       }
       if (e <= kWinTol) continue;
+      if (mode == 3 && pr.n_over == pr.n_over_ref) continue;  // NedPlan: same grid, same gridding, same answer
       if (can_ref_len) {
         P->ref_len = true;
         break;
       }
-      if (mode == 3 && pr.n_over == pr.n_over_ref) continue;  // same grid, same gridding: same answer
       char buf[400];
       std::snprintf(buf, sizeof buf,
                     "window (c=%g, K=%d, alpha=%g, beta=%g) is not accurate enough (probe error %.2e at the "
@@ -393,7 +393,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     }
   }
   if (P->ref_len) {
-    for (int a = 0; a < d->n_lat && mode == 0; ++a) {
+    for (int a = 0; a < d->n_lat && (mode == 0 || mode == 3); ++a) {
       n_over_lat[a] = even_fast_len(c * d->out_dims[a]);
       if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_lat[a]) / d->out_dims[a], &P->win_lat[a],
                           &err))
@@ -401,10 +401,12 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     }
     P->nrows = d->n_lat == 2 ? n_over_lat[0] : 1;
     P->ncols = n_over_lat[d->n_lat - 1];
-    P->n_over_t = even_fast_len(c * n_ext);
-    if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(P->n_over_t) / n_ext, &P->win_t, &err))
-      return fail(PATFFT_ERR_PARAMETER, err);
-    P->fused_ifft = false;  // the gather kernel writes the depth spectrum, cuFFT inverts it
+    if (mode != 3) {
+      P->n_over_t = even_fast_len(c * n_ext);
+      if (!resolve_window(c, K, d->spec_alpha, d->spec_beta, double(P->n_over_t) / n_ext, &P->win_t, &err))
+        return fail(PATFFT_ERR_PARAMETER, err);
+      P->fused_ifft = false;  // the gather kernel writes the depth spectrum, cuFFT inverts it
+    }
   }
   // ---- float32-grade windows ----------------------------------------------
   // The reference's default window (K = 6, auto alpha/beta) makes each NUFFT
@@ -935,6 +937,10 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     } else {
       n[0] = ncols; inem[0] = ncols; onem[0] = lr.nyo;
     }
+    if (mode == 3) {  // NedPlan: complex values, T / 2 complex per grid point, no NER
+      CUFFT_TRY(cufftPlanMany(&lr.c2c, rank, n, inem, T / 2, 1, inem, T / 2, 1, CUFFT_C2C, T / 2));
+      P->lat.ref = &P->lat_ref;
+    } else {
     CUFFT_TRY(cufftPlanMany(&lr.r2c, rank, n, inem, T, 1, onem, T, 1, CUFFT_R2C, T));
     NerRef& nr = P->ner_ref;
     const int rows = P->N0 * P->N1h;
@@ -947,6 +953,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
     nr.win = NerRefWindow{wt.alpha, wt.beta, 1.0 / psh0, wt.K};
     q.ref = &P->ner_ref;
     P->lat.ref = &P->lat_ref;
+    }
   }
 
   // ---- kernel parameter blocks --------------------------------------------
@@ -1091,11 +1098,16 @@ int patfft_ned_execute(patfft_nedner_plan* P, const double* values, double* out,
   L.ny = P->N1;
   L.t_begin = 0;
   L.t_end = P->T;
-  CUDA_TRY(launch_lateral_col(L, st));
-  L.T = B;  // rowfft works on complex columns
-  L.t_end = B;
-  L.ys = B;
-  CUDA_TRY(launch_lateral_row(L, st));
+  if (L.ref) {  // inaccurate window: the reference's grid lengths (reflen.cu)
+    L.gh = P->d_gh;
+    CUDA_TRY(launch_lateral_ref_cplx(L, B, st));
+  } else {
+    CUDA_TRY(launch_lateral_col(L, st));
+    L.T = B;  // rowfft works on complex columns
+    L.t_end = B;
+    L.ys = B;
+    CUDA_TRY(launch_lateral_row(L, st));
+  }
   CUDA_TRY(launch_f32_to_f64(reinterpret_cast<const float*>(P->d_gh), P->d_out64, 2 * out_c, st));
   CUDA_TRY(cudaMemcpyAsync(out, P->d_out64, 2 * out_c * sizeof(double), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -1972,6 +1984,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->have_c2r) cufftDestroy(P->fft_c2r);
   if (P->have_l) cufftDestroy(P->fft_l);
   if (P->lat_ref.r2c) cufftDestroy(P->lat_ref.r2c);
+  if (P->lat_ref.c2c) cufftDestroy(P->lat_ref.c2c);
   if (P->ner_ref.c2c) cufftDestroy(P->ner_ref.c2c);
   if (P->lat_ref.spec) cudaFree(P->lat_ref.spec);
   if (P->ner_ref.fb) cudaFree(P->ner_ref.fb);

@@ -46,6 +46,50 @@ __device__ __forceinline__ float2 cospi_sinpi_api(float r) {
   }
 }
 
+// ---- reference-length form (windows whose approximation error the reference's answer carries, see
+// capi.cu / reflen.cu): pre-window + zero padding to the reference's n_over, cuFFT, and the
+// reference's own tap sum per target (nufft.py:287-293, floor() bins, window transform in float64)
+__global__ void nerplan_ref_prep_kernel(const NerApiParams p, int r0, int nrows, float2* __restrict__ fb) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+  if (k >= p.n_over || r >= nrows) return;
+  float2 v = make_float2(0.f, 0.f);
+  if (k < p.n) {
+    const float2 g = p.u[(size_t)(r0 + r) * p.n + k];
+    const float w = p.iw[k];
+    v = make_float2(g.x * w, g.y * w);
+  }
+  fb[(size_t)r * p.n_over + k] = v;
+}
+
+__global__ void nerplan_ref_gather_kernel(const NerApiParams p, int r0, int nrows, const float2* __restrict__ fb,
+                                          double alpha, double beta, double inv_psihat0, int K) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, rb = blockIdx.y;
+  if (i >= p.m || rb >= nrows) return;
+  const int r = r0 + rb;
+  const double ke = p.shared ? p.kap[i] : p.kap[(size_t)r * p.m + i];
+  const double k0 = floor(__dmul_rn(p.c_eff, ke));
+  const float2* __restrict__ row = fb + (size_t)rb * p.n_over;
+  double ar = 0.0, ai = 0.0;
+  for (int a = -K + 1; a <= K; ++a) {
+    const double bin = k0 + (double)a;
+    const double off = ke - bin / p.c_eff;
+    const double t = alpha * alpha * (beta * beta - off * off);  // nufft.py:168-187
+    double v;
+    if (fabs(t) < 1e-9) v = 1.0 + t / 6.0 + t * t / 120.0;
+    else if (t > 0) v = sinh(sqrt(t)) / sqrt(t);
+    else v = sin(sqrt(-t)) / sqrt(-t);
+    const double wt = 2.0 * alpha * v * inv_psihat0;  // iw[] carries psihat(0) * norm
+    double sn, cs;
+    sincospi(-off, &sn, &cs);
+    int b = (int)fmod(bin, (double)p.n_over);
+    if (b < 0) b += p.n_over;
+    const float2 F = row[b];
+    ar += wt * (cs * F.x - sn * F.y);
+    ai += wt * (cs * F.y + sn * F.x);
+  }
+  p.out[(size_t)r * p.m + i] = make_float2((float)ar, (float)ai);
+}
+
 template <int K2, int D>
 __global__ void __launch_bounds__(512) nerplan_kernel(const NerApiParams p) {
   extern __shared__ float2 sbuf[];
@@ -204,6 +248,11 @@ struct patfft_ner_plan {
   std::mutex mu;
   int n = 0, n_over = 0, K2 = 12, degree = 8;
   Window win;
+  // reference-length form: n_over is the reference's even 11-smooth length, cuFFT transforms ref_blk rows at a time
+  bool ref_len = false;
+  cufftHandle ref_c2c = 0;
+  float2* d_ref_fb = nullptr;
+  int ref_blk = 0;
   NerApiParams prm{};
   float* d_iw = nullptr;
   float2* d_tw = nullptr;
@@ -238,6 +287,24 @@ int launch_nerplan(patfft_ner_plan* P, const float2* u, const double* kap, int r
   q.rows = rows;
   q.m = m;
   q.shared = shared;
+  if (P->ref_len) {
+    if (cufftSetStream(P->ref_c2c, s) != CUFFT_SUCCESS) return api_fail(PATFFT_ERR_CUDA, "cufftSetStream");
+    const double psh0 = kb_psihat(P->win, 0.0);
+    for (int r0 = 0; r0 < rows; r0 += P->ref_blk) {
+      const int nb = std::min(P->ref_blk, rows - r0);
+      nerplan_ref_prep_kernel<<<dim3((unsigned)((P->n_over + 255) / 256), (unsigned)nb), 256, 0, s>>>(q, r0, nb,
+                                                                                                   P->d_ref_fb);
+      if (cufftExecC2C(P->ref_c2c, reinterpret_cast<cufftComplex*>(P->d_ref_fb),
+                       reinterpret_cast<cufftComplex*>(P->d_ref_fb), CUFFT_FORWARD) != CUFFT_SUCCESS)
+        return api_fail(PATFFT_ERR_CUDA, "cufftExecC2C");
+      if (m > 0)
+        nerplan_ref_gather_kernel<<<dim3((unsigned)((m + 127) / 128), (unsigned)nb), 128, 0, s>>>(
+            q, r0, nb, P->d_ref_fb, P->win.alpha, P->win.beta, 1.0 / psh0, P->win.K);
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return api_fail(PATFFT_ERR_CUDA, cudaGetErrorString(e));
+    return PATFFT_OK;
+  }
   int threads = P->n_over / 16;
   threads = std::max(64, std::min(512, threads));
   const size_t smem = (size_t)P->n_over * sizeof(float2);
@@ -368,19 +435,40 @@ int patfft_ner_plan_create(int n, double c, int K, double alpha, double beta, in
   P->K2 = 2 * K;
   std::string err;
   if (!resolve_window(c, K, alpha, beta, double(no) / n, &P->win, &err)) return api_fail(PATFFT_ERR_PARAMETER, err);
+  // The fast kernel (power-of-two length, rotated input) returns the exact transform when the window
+  // is accurate; the reference's answer with an inaccurate window (small K, poor alpha / beta) depends
+  // on its own even 11-smooth length and tap sums, so such plans run the reference-length form.
   const int nref = even_fast_len(c * n);
-  if ((!std::isnan(alpha) || !std::isnan(beta)) && nref != no && no <= 8192) {
-    const double e = window_relative_error(P->win, n, (int)no);
-    if (!(e <= 1e-6))
-      return api_fail(PATFFT_ERR_UNSUPPORTED,
-                      "window loses accuracy at the GPU's power-of-two oversampled length (use default alpha/beta)");
+  const bool explicit_window = !std::isnan(alpha) || !std::isnan(beta);
+  if (explicit_window || K < 6 || c < 2.0) {
+    auto accuracy = [](Window w, int len, int len_over) {
+      if (len > 256) {
+        len_over = (int)std::lround(double(len_over) / len * 256.0);
+        len = 256;
+        w.c_eff = double(len_over) / len;
+      }
+      return window_relative_error(w, len, len_over);
+    };
+    Window wref;
+    if (!resolve_window(c, K, alpha, beta, double(nref) / n, &wref, &err)) return api_fail(PATFFT_ERR_PARAMETER, err);
+    if (!(accuracy(wref, n, nref) <= 1e-6) || (nref != no && !(accuracy(P->win, n, (int)no) <= 1e-6))) {
+      P->ref_len = true;
+      P->win = wref;
+      P->n_over = nref;
+    }
   }
   const double s0 = kb_psihat(P->win, 0.0), norm = 1.0 / (2.0 * M_PI * P->win.c_eff);
   std::vector<float> iw(n);
   for (int k = 0; k < n; ++k) iw[k] = (float)(s0 * norm / kb_psi(P->win, 2.0 * M_PI * k / n - M_PI));
   const std::vector<float2> tw = make_twiddles();
   P->degree = 8;
-  if (fit_ner_poly_public(P->win, 8, P->prm.poly) > 2e-8) {
+  if (P->ref_len) {
+    P->ref_blk = (int)std::max<int64_t>(1, std::min<int64_t>(4096, ((int64_t)1 << 24) / P->n_over));
+    API_CUDA(cudaMalloc(&P->d_ref_fb, (size_t)P->ref_blk * P->n_over * sizeof(float2)));
+    int nl[1] = {P->n_over};
+    if (cufftPlanMany(&P->ref_c2c, 1, nl, nl, 1, P->n_over, nl, 1, P->n_over, CUFFT_C2C, P->ref_blk) != CUFFT_SUCCESS)
+      return api_fail(PATFFT_ERR_CUDA, "cufftPlanMany (reference-length NerPlan)");
+  } else if (fit_ner_poly_public(P->win, 8, P->prm.poly) > 2e-8) {
     P->degree = 12;
     if (fit_ner_poly_public(P->win, 12, P->prm.poly) > 1e-6)
       return api_fail(PATFFT_ERR_UNSUPPORTED, "window transform not representable by the tap polynomials");
@@ -394,7 +482,7 @@ int patfft_ner_plan_create(int n, double c, int K, double alpha, double beta, in
   q.iw = P->d_iw;
   q.tw = P->d_tw;
   q.n = n;
-  q.n_over = (int)no;
+  q.n_over = P->n_over;  // (the reference's length in the reference-length form)
   int L = 0;
   while ((1 << L) < no) ++L;
   q.L = L;
@@ -454,6 +542,8 @@ void patfft_ner_plan_destroy(patfft_ner_plan* P) {
   for (void* p : {(void*)P->d_iw, (void*)P->d_tw, (void*)P->d_u64, (void*)P->d_u, (void*)P->d_k, (void*)P->d_o,
                   (void*)P->d_o64})
     if (p) cudaFree(p);
+  if (P->d_ref_fb) cudaFree(P->d_ref_fb);
+  if (P->ref_c2c) cufftDestroy(P->ref_c2c);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
 }
@@ -473,6 +563,11 @@ int patfft_forward_plan_create(int n_lat, const int32_t* n_lateral, int n_time, 
   F->device = device;
   int rc = patfft_ner_plan_create(n_time, c, K, alpha, beta, device, &F->ner);
   if (rc) return rc;
+  if (F->ner->ref_len)
+    return api_fail(PATFFT_ERR_UNSUPPORTED,
+                    "the GPU forward model needs a window that makes the transform exact to 1e-6 (K >= 4 at c >= 2 "
+                    "with the default alpha/beta): with this one the reference's answer carries the window's own "
+                    "approximation error");
   if (F->ner->n_over < 2 * n_time)
     return api_fail(PATFFT_ERR_UNSUPPORTED, "GPU forward model needs an oversampling factor >= 2");
   F->n_lat = n_lat;

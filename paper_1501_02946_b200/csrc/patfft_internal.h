@@ -76,6 +76,7 @@ struct SpreadParams {
 // pointers ride in the kernel parameter blocks but are only read on the host.
 struct LatRef {
   cufftHandle r2c = 0;     // (rows, cols) real-to-complex per time sample, stride T
+  cufftHandle c2c = 0;     // NedPlan: (rows, cols) complex in place, stride T / 2
   float2* spec = nullptr;  // [nrows][ncols / 2 + 1][T]
   float2* ghd = nullptr;   // = NerRef::ghd
   int nyo = 0;             // ncols / 2 + 1
@@ -163,6 +164,7 @@ cudaError_t launch_lateral_inverse(const LateralParams& p, cudaStream_t s);
 cudaError_t launch_ner(const NerParams& p, int K2, int degree, cudaStream_t s);
 cudaError_t launch_lateral_ref(const LateralParams& p, cudaStream_t s);  // reflen.cu
 cudaError_t launch_ner_ref(const NerParams& p, cudaStream_t s);
+cudaError_t launch_lateral_ref_cplx(const LateralParams& p, int B, cudaStream_t s);
 size_t ner_smem_bytes(int n_over, int Tu);
 int ner_threads(int n_over);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);

@@ -68,6 +68,23 @@ __global__ void crop_ref_kernel(const LateralParams p, const float2* __restrict_
   ghd[o] = make_float2(dv.x * s, dv.y * s);
 }
 
+// NedPlan (complex values, full spectrum): crop of the in-place C2C spectrum X[row][col][b], the
+// centred-grid sign (-1)^(j0+j1), deapodisation, centred or wrapped output order (nufft.py:406-417;
+// the rowfft epilogue of lateral.cu for p.cplx)
+__global__ void crop_ref_cplx_kernel(const LateralParams p, const float2* __restrict__ X, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j1 = blockIdx.y, j0w = blockIdx.z;
+  if (b >= B) return;
+  const int N0 = p.N0, N1 = p.N1;
+  const int j1s = j1 < N1 / 2 ? j1 : j1 - N1;
+  const int a = (N0 > 1) ? (j0w < N0 / 2 ? j0w : j0w - N0) : 0;
+  const float sg = ((a + j1s) & 1) ? -1.f : 1.f;
+  const float2 v = X[((size_t)pmodi(a, p.nrows) * p.ncols + pmodi(j1s, p.ncols)) * B + b];
+  const float s = sg * p.dp0[j0w] * p.dp1[j1];
+  const size_t o = p.centered ? (size_t)(a + N0 / 2) * N1 + (j1s + N1 / 2) : (size_t)j0w * N1 + j1;
+  p.gh[o * B + b] = make_float2(v.x * s, v.y * s);
+}
+
 // rows [r0, r0 + nrows) of gh -> pre-windowed even extension, zero padded to n_over
 __global__ void ner_ref_prep_kernel(const NerParams p, const float2* __restrict__ gh, int r0, int nrows,
                                     float2* __restrict__ fb) {
@@ -197,6 +214,19 @@ cudaError_t launch_lateral_ref(const LateralParams& p, cudaStream_t s) {
     return cudaErrorUnknown;
   const dim3 grid((unsigned)((p.T + 127) / 128), (unsigned)p.ny, (unsigned)p.N0);
   crop_ref_kernel<<<grid, 128, 0, s>>>(p, R->spec, R->nyo, R->ghd);
+  return cudaGetLastError();
+}
+
+// NedPlan on the reference's lengths: in-place C2C over (rows, cols) of the complex grid, then the crop
+cudaError_t launch_lateral_ref_cplx(const LateralParams& p, int B, cudaStream_t s) {
+  const LatRef* R = p.ref;
+  float2* X = reinterpret_cast<float2*>(const_cast<float*>(p.grid));
+  if (cufftSetStream(R->c2c, s) != CUFFT_SUCCESS) return cudaErrorUnknown;
+  if (cufftExecC2C(R->c2c, reinterpret_cast<cufftComplex*>(X), reinterpret_cast<cufftComplex*>(X), CUFFT_FORWARD) !=
+      CUFFT_SUCCESS)
+    return cudaErrorUnknown;
+  const dim3 grid((unsigned)((B + 127) / 128), (unsigned)p.N1, (unsigned)p.N0);
+  crop_ref_cplx_kernel<<<grid, 128, 0, s>>>(p, X, B);
   return cudaGetLastError();
 }
 

@@ -101,3 +101,54 @@ def test_gpu_equispaced_and_interp_random_problems_match_oracle():
                 f"seed {seed} {kind}: nl={nl} nt={nt} up={up} c={c} K={K}: rel-L2 {err:.2e}"
             worst = max(worst, err)
     print(f"equispaced / interp fuzz: worst rel-L2 {worst:.2e}")
+
+
+def test_gpu_standalone_plans_random_problems_match_oracle():
+    """NerPlan / NedPlan (any c, K incl. inaccurate auto windows -> reference lengths, shared and
+    per-row targets, a target with an integer c * kappa) and forward_fourier (accurate windows; it
+    refuses the others with DeviceError) against the oracle."""
+    from oracle import forward_oracle as FO
+
+    worst = {"ner": 0.0, "ned": 0.0, "fwd": 0.0}
+    refused = 0
+    for seed in range(4000, 4040):
+        rng = np.random.default_rng(seed)
+        c = float(rng.choice([1.5, 2.0, 2.0, 2.5, 3.0]))
+        K = int(rng.integers(2, 9))
+        spec = pb.WindowSpec(c=c, K=K)
+        nn = int(rng.choice([16, 24, 32, 48, 64, 96, 128, 256]))
+        rows, m = int(rng.integers(1, 6)), int(rng.integers(1, 40))
+        u = rng.standard_normal((rows, nn)) + 1j * rng.standard_normal((rows, nn))
+        ner = O.NerOracle(nn, c, K)
+        shared = rng.random() < 0.5
+        kap = rng.uniform(-ner.kappa_max, ner.kappa_max, size=(m,) if shared else (rows, m))
+        kap.flat[0] = float(np.round(kap.flat[0] * 2) / 2)
+        got = pb.NerPlan(nn, spec).execute(u, kap)
+        e = rel_l2(got, ner.shared(u, kap) if shared else ner.rows(u, kap))
+        assert e <= 1e-4, f"NerPlan seed {seed} n={nn} c={c} K={K}: {e:.2e}"
+        worst["ner"] = max(worst["ner"], e)
+        nl = tuple(int(rng.choice([8, 12, 16, 24, 32])) for _ in range(int(rng.integers(1, 3))))
+        M, nv = int(rng.integers(5, 200)), int(rng.choice([1, 3, 8]))
+        pos = rng.uniform(-0.5, 0.5, size=(M, len(nl))) * np.asarray(nl)
+        vals = rng.standard_normal((M, nv)) + 1j * rng.standard_normal((M, nv))
+        got = pb.NedPlan(nl, spec).execute(pos, vals)
+        e = rel_l2(got, O.NedOracle(nl, c, K).execute(pos, vals, wrapped=False))
+        assert e <= 1e-4, f"NedPlan seed {seed} nl={nl} c={c} K={K}: {e:.2e}"
+        worst["ned"] = max(worst["ned"], e)
+        fl = tuple(int(rng.choice([8, 16, 32])) for _ in range(int(rng.integers(1, 3))))
+        nt = int(rng.choice([16, 32, 64, 128]))
+        field = rng.standard_normal(fl + (nt,)) * np.exp(-np.arange(nt) / (0.4 * nt))
+        spacing = (synth.PITCH,) * len(fl) + (synth.PITCH * float(rng.choice([0.15, 0.3, 0.6])),)
+        try:
+            got = pb.forward_fourier(pb.ScalarField(field, spacing), synth.SOUND_SPEED, spec)
+        except pb.DeviceError:
+            refused += 1
+            assert K < 6 or c < 2.0  # only windows outside the default family may be refused
+            continue
+        want = FO.forward_fourier(field, spacing, synth.SOUND_SPEED, c, K)
+        ws = want[0] if isinstance(want, tuple) else want
+        e = rel_l2(got.samples, np.asarray(ws).reshape(got.samples.shape))
+        assert e <= 1e-4, f"forward seed {seed} fl={fl} nt={nt} c={c} K={K}: {e:.2e}"
+        worst["fwd"] = max(worst["fwd"], e)
+    print("standalone fuzz: worst rel-L2 " + ", ".join(f"{k} {v:.2e}" for k, v in worst.items())
+          + f"; forward model refused {refused} inaccurate windows")
