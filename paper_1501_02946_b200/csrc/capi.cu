@@ -1008,7 +1008,7 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   L.grid = P->d_grid;
   L.Y = P->d_Y;
   L.f_flags = P->d_lat_flags;
-  L.f_chunks = L.f_slots = 0;
+  L.f_chunks = L.f_slots = L.f_lead = 0;
   L.y_capacity = T;
   L.ys = T;
   L.yt0 = 0;
@@ -1029,6 +1029,18 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   L.z = P->d_z;
   L.out = nullptr;
   L.Tu = P->sliced ? P->up * P->Tr : (world == 1 ? P->Tu : P->Tr);
+  L.inv_ring = nullptr;
+  L.inv_flags = nullptr;
+  L.inv_capacity = 0;
+  if (P->custom_inverse && mode != 3 && P->N0u == P->N1u && P->N0u >= 64 && P->N0u <= 512 && L.Tu % 32 == 0) {
+    // single-launch inverse: 16 ring slots at most (PATFFT_INV_FUSED_SLOTS), 8.5 MB each at cfg4
+    const size_t slot = (size_t)P->N0u * P->N1uh * 32;
+    if ((rc = dalloc(&P->d_inv_ring, slot * (size_t)std::min(16, L.Tu / 32)))) return rc;
+    if ((rc = dalloc(&P->d_inv_flags, 2 * ((size_t)L.Tu / 32 + 2)))) return rc;
+    L.inv_ring = P->d_inv_ring;
+    L.inv_flags = P->d_inv_flags;
+    L.inv_capacity = L.Tu;
+  }
   L.N0u = P->N0u;
   L.N1u = P->N1u;
   L.N1uh = P->N1uh;
@@ -1989,7 +2001,7 @@ void patfft_nedner_plan_destroy(patfft_nedner_plan* P) {
   if (P->lat_ref.spec) cudaFree(P->lat_ref.spec);
   if (P->ner_ref.fb) cudaFree(P->ner_ref.fb);
   if (P->ner_ref.ghd) cudaFree(P->ner_ref.ghd);
-  for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_lat_flags, (void*)P->d_gh,
+  for (void* p : {(void*)P->d_samples, (void*)P->d_samples64, (void*)P->d_grid, (void*)P->d_Y, (void*)P->d_lat_flags, (void*)P->d_inv_ring, (void*)P->d_inv_flags, (void*)P->d_gh,
                   (void*)P->d_z, (void*)P->d_out, (void*)P->d_out64, (void*)P->d_recs, (void*)P->d_tc_recs, (void*)P->d_tc_tiles, (void*)P->d_tc_counter, (void*)P->d_tc_a16, (void*)P->d_tc_off, (void*)P->d_gidx, (void*)P->d_blk, (void*)P->d_blkgrp,
                   (void*)P->d_dp0, (void*)P->d_dp1, (void*)P->d_iw, (void*)P->d_pre, (void*)P->d_tw, (void*)P->d_jt0,
                   (void*)P->d_jt1})

@@ -71,6 +71,8 @@ using fft::TileAddr;
 __device__ __forceinline__ int lat_line() { return PATFFT_LAT_TFAST ? blockIdx.y : blockIdx.x; }
 __device__ __forceinline__ int lat_ttile() { return PATFFT_LAT_TFAST ? blockIdx.x : blockIdx.y; }
 
+int plog_for(int len);
+
 constexpr int nth_for(int L, int PLOG) {
   return ((L >= 4 ? (1 << (L - 4)) : 1) << PLOG) < 64 ? 64
          : (((L >= 4 ? (1 << (L - 4)) : 1) << PLOG) > 512 ? 512 : ((L >= 4 ? (1 << (L - 4)) : 1) << PLOG));
@@ -442,6 +444,87 @@ __global__ void __launch_bounds__(inv_lb_threads(PLOG, LC), inv_lb_minb(PLOG, LC
   for (int i = tid; i < n * P; i += nth) st(i >> PLOG, i & (P - 1), sm[ad(i >> PLOG, i & (P - 1))]);
 }
 
+// ---------------------------------------------------------------------------
+// Lateral inverse in ONE launch.  inv_col and inv_c2r are bound by HBM (80-85% of the peak), and
+// between them the half spectrum z makes a full round trip (0.27 GB written in place, 0.27 GB read
+// again at cfg4).  Here the column-inverse tiles write their output into a ring of kSlots chunk
+// buffers of 32 depth samples ([N0u][N1uh][32] each, 8.5 MB at cfg4) that stays in L2, and the C2R
+// tiles of the same launch read it from there: z is read once, the image written once.  Tiles are
+// laid out in rounds [column tiles of chunk r][C2R tiles of chunk r - 1] with the release / acquire
+// progress counters of latfused_kernel (dependencies only on lower block indices).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float4 ld_l2_v4(const float4* a) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a));
+  return v;
+}
+
+template <int PLOG, int LC>
+__global__ void __launch_bounds__(inv_lb_threads(PLOG, LC), inv_lb_minb(PLOG, LC)) invfused_kernel(const LateralParams p) {
+  extern __shared__ float2 sm[];
+  constexpr int P = 1 << PLOG, CH = 2 * P, NTH = nth_for(LC, PLOG);
+  const int tid = threadIdx.x;
+  const int T = p.Tu, n = 1 << LC, half = n / 2;
+  const int nc = 2 * p.N1uh, nr = p.N0u, per = nc + nr;
+  const int round = blockIdx.x / per, idx = blockIdx.x - round * per;
+  const size_t slot = (size_t)p.N0u * p.N1uh * CH, rr = (size_t)p.N1uh * CH;
+  if (idx < nc) {  // column inverse (along j0) of half-spectrum column j1, 16 depth samples
+    const int c = round;
+    if (c >= p.f_chunks) return;
+    const int j1 = idx >> 1, tl = (idx & 1) * P, t0 = c * CH + tl;
+    if (c >= p.f_slots) lat_wait(p.f_flags + p.f_chunks + (c - p.f_slots), nr);
+    float2* __restrict__ ring = p.inv_ring + (size_t)(c % p.f_slots) * slot;
+    const size_t rs = (size_t)p.N1uh * T;
+    fft::fft_ct_loaded_stored<true, LC, 4, false, PLOG, NTH>(
+        sm, p.tw, tid, fft::TileC<PLOG>(),
+        fft::rows_ld<1>([&](int row, int q) -> const float2* { return p.z + (size_t)row * rs + (size_t)j1 * T + t0 + q; },
+                        rs),
+        fft::rows_st([&](int row, int q) -> float2* { return ring + (size_t)row * rr + (size_t)j1 * CH + tl + q; }, rr));
+    lat_signal(p.f_flags + c);
+  } else {  // C2R (along j1) of image row n0, 32 depth samples as 16 packed pairs
+    const int c = round - p.f_lead;  // f_lead rounds behind the column tiles it consumes
+    if (c < 0) return;
+    const int n0 = idx - nc, t0 = c * CH;
+    lat_wait(p.f_flags + c, nc);
+    const float2* __restrict__ zr = p.inv_ring + (size_t)(c % p.f_slots) * slot + (size_t)n0 * rr;
+    float* __restrict__ out = p.out + (size_t)n0 * n * T;
+    auto ld = [&](int r, int q) {
+      const bool lo = r <= half;
+      const int k = lo ? r : n - r;
+      float4 v = ld_l2_v4(reinterpret_cast<const float4*>(zr + (size_t)k * CH + 2 * q));
+      if (k == 0 || k == half) {  // C2R semantics: self-conjugate bins are real
+        v.y = 0.f;
+        v.w = 0.f;
+      }
+      return lo ? make_float2(v.x - v.w, v.y + v.z) : make_float2(v.x + v.w, v.z - v.y);
+    };
+    fft::fft_ct_loaded_stored<true, LC, 4, false, PLOG, NTH>(
+        sm, p.tw, tid, fft::TileC<PLOG>(), ld, fft::rows_st([&](int row, int q) -> float2* {
+          return reinterpret_cast<float2*>(out + (size_t)row * T + t0 + 2 * q);
+        }, (size_t)(T / 2)));
+    lat_signal(p.f_flags + p.f_chunks + c);
+  }
+}
+
+// Ring slots; 0 (default) = the two-kernel form.  Measured at cfg4: 0.170 ms (6 slots, lead 3)
+// against 0.192 ms -- the launch is held back by its tile dependencies rather than sped up by the
+// halved HBM traffic -- and slower at cfg3 (0.029-0.056 vs 0.028 ms), so it stays an opt-in.
+int inv_fused_slots() {
+  const char* e = std::getenv("PATFFT_INV_FUSED_SLOTS");
+  return e ? std::max(0, std::min(16, std::atoi(e))) : 0;
+}
+
+int inv_fused_lead() {  // rounds between a chunk's column tiles and its C2R tiles
+  const char* e = std::getenv("PATFFT_INV_FUSED_LEAD");
+  return e ? std::max(1, std::atoi(e)) : 3;
+}
+
+bool inverse_fused_supported(const LateralParams& p) {
+  return inv_fused_slots() > 0 && p.inv_ring && p.inv_flags && p.N0u == p.N1u &&
+         (p.N0u == 64 || p.N0u == 128 || p.N0u == 256 || p.N0u == 512) && plog_for(p.N0u) == 4 && p.Tu % 32 == 0 &&
+         p.Tu / 32 >= 2 && p.Tu <= p.inv_capacity;
+}
+
 int tile_bytes() {
   static int b = [] {
     const char* e = std::getenv("PATFFT_TILE_KB");
@@ -588,7 +671,33 @@ cudaError_t launch_lateral_forward(const LateralParams& p0, cudaStream_t s) {
   return err;
 }
 
-cudaError_t launch_lateral_inverse(const LateralParams& p, cudaStream_t s) {
+cudaError_t launch_lateral_inverse(const LateralParams& p0, cudaStream_t s) {
+  if (inverse_fused_supported(p0)) {
+    LateralParams p = p0;
+    p.f_chunks = p.Tu / 32;
+    p.f_slots = std::min(inv_fused_slots(), p.f_chunks);
+    p.f_lead = std::max(1, std::min(inv_fused_lead(), p.f_slots - 1));
+    p.f_flags = p.inv_flags;
+    cudaError_t err = cudaMemsetAsync(p.f_flags, 0, sizeof(int) * 2 * (size_t)p.f_chunks, s);
+    if (err != cudaSuccess) return err;
+    const unsigned grid = (unsigned)((p.f_chunks + p.f_lead) * (2 * p.N1uh + p.N0u));
+    const size_t smem = ((size_t)p.N0u << 4) * sizeof(float2);
+    auto run = [&](auto k, int thr) {
+      err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (err == cudaSuccess) {
+        k<<<grid, thr, smem, s>>>(p);
+        err = cudaGetLastError();
+      }
+    };
+    switch (p.N0u) {
+      case 64: run(invfused_kernel<4, 6>, nth_for(6, 4)); break;
+      case 128: run(invfused_kernel<4, 7>, nth_for(7, 4)); break;
+      case 256: run(invfused_kernel<4, 8>, nth_for(8, 4)); break;
+      default: run(invfused_kernel<4, 9>, nth_for(9, 4)); break;
+    }
+    return err;
+  }
+  const LateralParams& p = p0;
   if (p.N0u > 1) {
     cudaError_t e = launch_inv_col(p, p.N0u, dim3((unsigned)p.N1uh, (unsigned)p.Tu), 1, s);
     if (e != cudaSuccess) return e;

@@ -110,13 +110,18 @@ struct LateralParams {
   // f_slots chunk buffers of 32 time samples; f_flags[c] counts the finished column
   // tiles of chunk c, f_flags[f_chunks + c] its finished row tiles
   int* f_flags;        // 2 * ceil(T / 32) ints (nullptr: two-kernel form only)
-  int f_chunks, f_slots;
+  int f_chunks, f_slots, f_lead;
   int y_capacity;      // time samples per (row, bin) the Y allocation holds
   int cplx;            // 1: NedPlan mode (complex values, full spectrum, no Hermitian fix-up)
   int centered;        // NedPlan output order
   // inverse
   float2* z;           // [N0u][N1uh][Tu]
   float* out;          // [N0u][N1u][Tu]
+  // single-launch inverse (lateral.cu, invfused_kernel): ring of chunk buffers [slots][N0u][N1uh][32],
+  // progress counters, and the depth length the counters were sized for (nullptr: two kernels)
+  float2* inv_ring;
+  int* inv_flags;
+  int inv_capacity;
   int Tu, N0u, N1u, N1uh, l0u, l1u;
 };
 
@@ -271,6 +276,8 @@ struct patfft_nedner_plan {
   float* d_grid = nullptr;      // [nrows][ncols][T]
   float2* d_Y = nullptr;        // [nrows][N1h][T]
   int* d_lat_flags = nullptr;   // progress counters of the single-launch lateral FFTs
+  float2* d_inv_ring = nullptr; // single-launch lateral inverse: L2-resident ring between its two FFTs
+  int* d_inv_flags = nullptr;
   float2* d_gh = nullptr;       // [N0][N1h][T]
   float2* d_z = nullptr;        // [N0u][N1uh][Tu]
   float* d_out = nullptr;       // [N0u][N1u][Tu] f32 (host path staging)

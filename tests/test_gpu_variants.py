@@ -204,6 +204,27 @@ def test_gpu_single_launch_lateral_matches_two_kernel_form(nl, nt, slots):
     assert err <= TOL
 
 
+@pytest.mark.parametrize("nl,nt,slots,lead", [((32, 32), 64, 2, 1), ((64, 64), 128, 6, 3), ((128, 128), 256, 4, 2)])
+def test_gpu_single_launch_inverse_matches_two_kernel_form(nl, nt, slots, lead):
+    """PATFFT_INV_FUSED_SLOTS > 0: the lateral inverse in one launch, the column-inverse output in an
+    L2-resident ring that the C2R tiles of the same launch read (lateral.cu, invfused_kernel).  Same
+    arithmetic per tile: bit-identical to the default two-kernel form."""
+    s = _rect_record(23 + nl[0], nl, nt, 20e-9, layout="jittered")
+    base = pb.NedNerPlan(s.positions, s.weights, nt, s.dt, s.sound_speed, s.dx, s.n_lateral)
+    ref = base.execute(s.samples)[0].copy()
+    os.environ["PATFFT_INV_FUSED_SLOTS"] = str(slots)
+    os.environ["PATFFT_INV_FUSED_LEAD"] = str(lead)
+    try:
+        plan = pb.NedNerPlan(s.positions, s.weights, nt, s.dt, s.sound_speed, s.dx, s.n_lateral)
+        got = plan.execute(s.samples)[0].copy()
+        got2 = plan.execute(s.samples)[0]
+    finally:
+        os.environ.pop("PATFFT_INV_FUSED_SLOTS", None)
+        os.environ.pop("PATFFT_INV_FUSED_LEAD", None)
+    assert np.array_equal(got, ref) and np.array_equal(got2, ref)
+    print(f"single-launch inverse {nl} Nt={nt} slots={slots} lead={lead}: bit-identical to the two-kernel form")
+
+
 def test_gpu_gridding_scale_hint_history_does_not_change_results():
     """fp16 gridding: the sample scale is speculated from the previous call's maximum and verified
     on the device (spread_tc.cu, check_scale_kernel); a wrong guess re-runs the gridding.  Whatever
