@@ -820,8 +820,8 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   if (P->tc_ntiles) {
     if ((rc = upload(&P->d_tc_recs, tcrec))) return rc;
     if ((rc = upload(&P->d_tc_tiles, tctiles))) return rc;
-    if ((rc = dalloc(&P->d_tc_counter, 8))) return rc;
-    CUDA_TRY(cudaMemset(P->d_tc_counter, 0, 8 * sizeof(int)));
+    if ((rc = dalloc(&P->d_tc_counter, 32))) return rc;
+    CUDA_TRY(cudaMemset(P->d_tc_counter, 0, 32 * sizeof(int)));
     if (P->tc_f16) {  // per-stage A operands (fp16 hi/lo) and sample row offsets, built on the device
       const int nst = (int)(P->tc_records / 16);
       if ((rc = dalloc(&P->d_tc_a16, (size_t)nst * 512))) return rc;

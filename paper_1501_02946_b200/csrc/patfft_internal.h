@@ -59,7 +59,7 @@ struct SpreadParams {
   const int4* tc_tiles = nullptr;   // per tile (launch order): {first record, records (multiple of 16), row0, col0}
   int tc_ntiles = 0, tc_nonempty = 0;  // tiles (the non-empty ones first, longest first)
   int tc_n = 0, tc_tblocks = 0;       // time samples per block, time blocks per launch
-  int* tc_counter = nullptr;          // 8 ints: work counters, |sample| max bits, redo flag, scale hint (spread_tc.cu)
+  int* tc_counter = nullptr;          // 32 ints: work counters, |sample| max bits, redo flag, batch max, scale hints (spread_tc.cu)
   int tc_batch_scale = 0;  // 1: the scale comes from the batch maximum (frames; spread_tc16_batch_max)
   int tc_pass = 0, tc_track = 0, tc_scale_src = 1;  // fp16 gridding: launch 0 / 1, record the max, scale source slot
   // fp16 two-term operands (kind::f16): records pre-scaled by 2^tc_wexp at plan
@@ -285,7 +285,7 @@ struct patfft_nedner_plan {
   float* d_recs = nullptr;
   float* d_tc_recs = nullptr;   // tensor-core gridding records (spread_tc.cu)
   int4* d_tc_tiles = nullptr;
-  int* d_tc_counter = nullptr;  // 8 ints (zero-initialised: no scale hint yet)
+  int* d_tc_counter = nullptr;  // 32 ints (zero-initialised: no scale hints yet)
   uint4* d_tc_a16 = nullptr;
   bool tc_tma_store = false;
   CUtensorMap tc_gmap;

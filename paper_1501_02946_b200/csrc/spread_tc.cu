@@ -469,8 +469,11 @@ __global__ void absmax_kernel(const float* __restrict__ s, int M, int T, int tb,
 
 // p.tc_counter slots (ints): work-item counters of the two launches, max |sample| bits seen, redo flag
 // (zeroed before every gridding) and the scale hint, which persists from call to call
-constexpr int kCtrWork0 = 0, kCtrSeen = 1, kCtrWork1 = 2, kCtrRedo = 3, kCtrHint = 4;
+constexpr int kCtrWork0 = 0, kCtrSeen = 1, kCtrWork1 = 2, kCtrRedo = 3;
 constexpr int kCtrBatch = 5;  // max |sample| over a batch of frames (spread_tc16_batch_max), set by the caller
+// scale hints: one per time block a launch may start at (launches over time chunks of one record --
+// the host-buffer path uploads and grids in chunks -- see different maxima; each keeps its own hint)
+constexpr int kCtrHint = 8, kHintSlots = 16;
 
 // The sample scale is 2^(14 - 4 b) with b = ceil(e / 4) the 4-binade bucket of max |sample| in
 // [2^(e-1), 2^e): the scaled maximum lies in [2^10, 2^14).  Quantising the exponent makes a scale
@@ -841,11 +844,11 @@ __global__ void __launch_bounds__(kThreadsTC, 2) spread_tc16_kernel(const __grid
 // After the first gridding launch: is the scale hint it used in the 4-binade bucket of the maximum it
 // saw?  (Same bucket <=> the launch used exactly the scale the max pass would have given, so the
 // result does not depend on the hint's history.)  Otherwise the second launch redoes the gridding.
-__global__ void check_scale_kernel(int* __restrict__ ctr) {
-  const unsigned seen = (unsigned)ctr[kCtrSeen], hint = (unsigned)ctr[kCtrHint];
+__global__ void check_scale_kernel(int* __restrict__ ctr, int hint_slot) {
+  const unsigned seen = (unsigned)ctr[kCtrSeen], hint = (unsigned)ctr[hint_slot];
   const bool ok = seen == 0 || (hint != 0 && scale_bucket(seen) == scale_bucket(hint));
   ctr[kCtrRedo] = ok ? 0 : 1;
-  if (seen) ctr[kCtrHint] = (int)seen;
+  if (seen) ctr[hint_slot] = (int)seen;
 }
 
 template <int N>
@@ -863,7 +866,7 @@ cudaError_t go_tc16(const SpreadParams& p, cudaStream_t s) {
   SpreadParams q = p;
   q.tc_tblocks = (p.t_end - p.t_begin) / N;
   const int blocks = std::min(q.tc_ntiles * q.tc_tblocks, 2 * sms);
-  if ((err = cudaMemsetAsync(q.tc_counter, 0, kCtrHint * sizeof(int), s))) return err;  // all but the hint
+  if ((err = cudaMemsetAsync(q.tc_counter, 0, 4 * sizeof(int), s))) return err;  // counters, seen, redo
   if (blocks <= 0 || q.tc_tblocks <= 0) return cudaSuccess;
   // The sample scale 2^es needs max |sample| of the launch.  PATFFT_TC16_SPECULATE=0: a max pass first
   // (one extra read of the samples, 47 us at cfg4).  Default: the launch uses the maximum the
@@ -892,12 +895,12 @@ cudaError_t go_tc16(const SpreadParams& p, cudaStream_t s) {
     k<<<blocks, kThreadsTC, smem, s>>>(q);
     return cudaGetLastError();
   }
-  q.tc_scale_src = kCtrHint;
+  q.tc_scale_src = kCtrHint + ((p.t_begin / N) % kHintSlots);
   q.tc_track = 1;
   q.tc_pass = 0;
   k<<<blocks, kThreadsTC, smem, s>>>(q);
   if ((err = cudaGetLastError())) return err;
-  check_scale_kernel<<<1, 1, 0, s>>>(q.tc_counter);
+  check_scale_kernel<<<1, 1, 0, s>>>(q.tc_counter, q.tc_scale_src);
   if ((err = cudaGetLastError())) return err;
   q.tc_track = 0;
   q.tc_pass = 1;
