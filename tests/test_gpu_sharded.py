@@ -67,18 +67,39 @@ def test_sharded_plan_rejects_unsupported_shapes():
 
 @pytest.mark.parametrize("world,chunks,blocks", [(2, 2, 3), (4, 2, 4), (8, 1, 2)])
 def test_pipelined_shard_stages_match_single_gpu(world, chunks, blocks):
-    """The pipelined stage entry points (whole-slice spread, lateral FFTs in time
-    pieces, NER in row blocks) with the exchange layouts of parallel.ShardedNedNer,
+    """The pipelined stage entry points (whole-slice spread, lateral FFTs in time pieces, NER in row
+    blocks) with the exchange layouts of parallel.ShardedNedNer,
     ranks emulated one after another on one GPU: bit-identical to one GPU."""
+    rec = synth.make_3d(50 + world, 64, 256, 20e-9, "clustered", 3, sigma=2e-3)
+    _emulate_pipelined(world, chunks, blocks, rec)
+
+
+@pytest.mark.parametrize("seed", range(9100, 9108))
+def test_pipelined_shard_stages_random_problems(seed):
+    """Random power-of-two problems (2D and 3D), world sizes, time pieces and row blocks."""
+    rng = np.random.default_rng(seed)
+    nt = int(rng.choice([128, 256, 512]))
+    world = int(rng.choice([2, 4, 8]))
+    tr = nt // world
+    chunks = int(rng.choice([1] + [c for c in (2, 4) if tr // c >= 32]))
+    blocks = int(rng.integers(1, 6))
+    if rng.random() < 0.25:
+        rec = synth.make_2d(seed=seed, n=int(rng.choice([32, 64, 128])), nt=nt)
+    else:
+        rec = synth.make_3d(seed, int(rng.choice([16, 32, 64])), nt, 20e-9, str(rng.choice(["uniform", "jittered", "clustered"])), 3,
+                            sigma=2e-3)
+    _emulate_pipelined(world, chunks, blocks, rec)
+
+
+def _emulate_pipelined(world, chunks, blocks, rec):
     import torch
 
     from paper_1501_02946_b200.parallel import GpuStages, ShardLayout
 
-    rec = synth.make_3d(50 + world, 64, 256, 20e-9, "clustered", 3, sigma=2e-3)
     want = pb.reconstruct_nedner(rec.as_record()).values
     nl = tuple(rec.n_lateral)
     T = rec.samples.shape[1]
-    L = ShardLayout(2, nl, T, world)
+    L = ShardLayout(len(nl), nl, T, world)
     C, Trc = chunks, L.Tr // chunks
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(device=dev)
@@ -115,8 +136,10 @@ def test_pipelined_shard_stages_match_single_gpu(world, chunks, blocks):
     got = torch.cat(imgs, dim=-1).double().cpu().numpy()
     torch.cuda.set_stream(torch.cuda.default_stream(dev))
     err = rel_l2(got, want)
-    print(f"pipelined world {world} (pieces {C}, row blocks {blocks}): rel-L2 vs single GPU {err:.2e}")
-    assert err <= 1e-6
+    print(f"pipelined {nl} Nt={T} world {world} (pieces {C}, row blocks {blocks}): rel-L2 vs single GPU {err:.2e}")
+    # (slices shorter than a tensor-core time block are gridded by the SIMT kernel: same answer to
+    #  float32 rounding, not bit for bit)
+    assert err <= (1e-6 if L.Tr >= 32 else 5e-6)
 
 
 @pytest.mark.parametrize("world,case", [(3, "2d_nt96_up2"), (2, "3d_up2"), (3, "3d_outdims_nt40"), (4, "3d_up3")])
