@@ -354,6 +354,12 @@ struct patfft_forward_plan {
   float2* d_spec = nullptr;        // [N0][N1h][T]
   cufftHandle r2c = 0, c2r = 0;
   bool have_r2c = false, have_c2r = false;
+  // power-of-two lateral grids: the reconstruction's own shared-memory lateral FFT kernels
+  // (lateral.cu) instead of cuFFT's stride-N_t transforms
+  bool custom_lateral = false;
+  float2* d_Y = nullptr;           // [N0][N1h][T] column-transformed half spectrum
+  float* d_ones = nullptr;         // max(N0, N1) ones: no deapodisation
+  LateralParams lat{};
 };
 
 namespace {
@@ -366,9 +372,19 @@ namespace {
 
 int launch_forward(patfft_forward_plan* F, const float* field, float* traces, cudaStream_t s) {
   patfft_ner_plan* P = F->ner;
-  API_CUFFT(cufftSetStream(F->r2c, s));
-  API_CUFFT(cufftSetStream(F->c2r, s));
-  API_CUFFT(cufftExecR2C(F->r2c, const_cast<float*>(field), reinterpret_cast<cufftComplex*>(F->d_spec)));
+  if (F->custom_lateral) {
+    // plain lateral FFT of the full grid: the column / row kernels with no oversampling, no crop
+    // and unit deapodisation (their Nyquist-plane Hermitian part is the identity on such a grid)
+    LateralParams L = F->lat;
+    L.grid = field;
+    cudaError_t e = launch_lateral_col(L, s);
+    if (e == cudaSuccess) e = launch_lateral_row(L, s);
+    if (e != cudaSuccess) return api_fail(PATFFT_ERR_CUDA, cudaGetErrorString(e));
+  } else {
+    API_CUFFT(cufftSetStream(F->r2c, s));
+    API_CUFFT(cufftSetStream(F->c2r, s));
+    API_CUFFT(cufftExecR2C(F->r2c, const_cast<float*>(field), reinterpret_cast<cufftComplex*>(F->d_spec)));
+  }
   FwdParams f{};
   f.q = P->prm;
   f.q.u = F->d_spec;
@@ -404,6 +420,13 @@ int launch_forward(patfft_forward_plan* F, const float* field, float* traces, cu
   }
 #undef PATFFT_FWD_CASE
   if (err != cudaSuccess) return api_fail(PATFFT_ERR_CUDA, cudaGetErrorString(err));
+  if (F->custom_lateral) {
+    LateralParams L = F->lat;
+    L.out = traces;
+    const cudaError_t e = launch_lateral_inverse(L, s);
+    if (e != cudaSuccess) return api_fail(PATFFT_ERR_CUDA, cudaGetErrorString(e));
+    return PATFFT_OK;
+  }
   API_CUFFT(cufftExecC2R(F->c2r, reinterpret_cast<cufftComplex*>(F->d_spec), traces));
   return PATFFT_OK;
 }
@@ -581,6 +604,41 @@ int patfft_forward_plan_create(int n_lat, const int32_t* n_lateral, int n_time, 
   API_CUDA(cudaMalloc(&F->d_j2, F->L * sizeof(double)));
   API_CUDA(cudaMemcpy(F->d_j2, j2, F->L * sizeof(double), cudaMemcpyHostToDevice));
   API_CUDA(cudaMalloc(&F->d_spec, F->Lh * n_time * sizeof(float2)));
+  auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
+  static const bool custom_on = [] {
+    const char* e = std::getenv("PATFFT_FORWARD_CUSTOM_FFT");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  if (custom_on && pow2(N1) && N1 >= 4 && N1 <= 16384 && (n_lat == 1 || (pow2(N0) && N0 >= 4 && N0 <= 16384))) {
+    F->custom_lateral = true;
+    const int mx = std::max(N0, N1);
+    std::vector<float> ones((size_t)mx, 1.0f);
+    API_CUDA(cudaMalloc(&F->d_ones, mx * sizeof(float)));
+    API_CUDA(cudaMemcpy(F->d_ones, ones.data(), mx * sizeof(float), cudaMemcpyHostToDevice));
+    API_CUDA(cudaMalloc(&F->d_Y, F->Lh * n_time * sizeof(float2)));
+    auto lg = [](int v) { int l = 0; while ((1 << l) < v) ++l; return l; };
+    LateralParams& L = F->lat;
+    L.ref = nullptr;
+    L.grid = nullptr;
+    L.Y = F->d_Y;
+    L.gh = F->d_spec;
+    L.tw = F->ner->d_tw;
+    L.dp0 = F->d_ones;
+    L.dp1 = F->d_ones;
+    L.T = n_time;
+    L.nrows = N0; L.lrows = lg(N0);
+    L.ncols = N1; L.lcols = lg(N1);
+    L.ny = F->N1h; L.N0 = N0; L.N1 = N1;
+    L.t_begin = 0; L.t_end = n_time;
+    L.ys = n_time; L.yt0 = 0; L.gs = n_time; L.gt0 = 0;
+    L.f_flags = nullptr; L.f_chunks = L.f_slots = L.f_lead = 0; L.y_capacity = n_time;
+    L.cplx = 0; L.centered = 0;
+    L.z = F->d_spec; L.out = nullptr;
+    L.inv_ring = nullptr; L.inv_flags = nullptr; L.inv_capacity = 0;
+    L.Tu = n_time; L.N0u = N0; L.N1u = N1; L.N1uh = F->N1h; L.l0u = lg(N0); L.l1u = lg(N1);
+    *out = F.release();
+    return PATFFT_OK;
+  }
   // lateral transforms of the [N0][N1][T] volume, time fastest: T interleaved batches
   int nr[2] = {N0, N1}, nc[2] = {N0, F->N1h};
   int* dims = n_lat == 2 ? nr : nr + 1;
@@ -625,7 +683,7 @@ void patfft_forward_plan_destroy(patfft_forward_plan* F) {
   if (F->ner && F->ner->stream) cudaStreamSynchronize(F->ner->stream);
   if (F->have_r2c) cufftDestroy(F->r2c);
   if (F->have_c2r) cufftDestroy(F->c2r);
-  for (void* p : {(void*)F->d_j2, (void*)F->d_field, (void*)F->d_f64, (void*)F->d_spec})
+  for (void* p : {(void*)F->d_j2, (void*)F->d_field, (void*)F->d_f64, (void*)F->d_spec, (void*)F->d_Y, (void*)F->d_ones})
     if (p) cudaFree(p);
   patfft_ner_plan_destroy(F->ner);
   delete F;

@@ -4,8 +4,8 @@
     python tools/bench_forward.py [--n 256] [--nt 1024] [--steps 20] [--warmup 3] [--no-cpu-baseline]
 
 One step = full-grid traces of one (n, n, nt) initial-pressure field:
-cuFFT R2C over the lateral plane, the fused NER-at-+-ky + depth-IFFT kernel
-(csrc/ner_api.cu forward_kernel), cuFFT C2R.  ``value`` is device-resident
+the lateral column / row FFT kernels of the reconstruction (cuFFT R2C on non-power-of-two grids), the fused NER-at-+-ky + depth-IFFT kernel
+(csrc/ner_api.cu forward_kernel), the lateral inverse kernels (cuFFT C2R otherwise).  ``value`` is device-resident
 (float32 field already in HBM, L2 flushed between steps, CUDA events on the
 plan stream); ``e2e`` is the host entry point (float64 field in, float64
 traces out, H2D/D2H inside).  The CPU baseline is the oracle restatement of
