@@ -313,8 +313,12 @@ static int create_plan(const patfft_nedner_desc* d, const double* gpos, const do
   // mode (3) has no NER at all
   const int64_t n_over_t = mode == 3 ? 2 : (mode == 2 ? n_ext : next_pow2((int64_t)std::ceil(c * n_ext)));
   if (mode == 2 && !is_pow2(n_ext)) return fail(PATFFT_ERR_UNSUPPORTED, "GPU interp path needs a power-of-two N_t");
-  if (n_over_t > 16384)
-    return fail(PATFFT_ERR_UNSUPPORTED, "GPU NER supports oversampled depth lengths up to 16384 (N_t <= 4096 at c=2)");
+  if (n_over_t > 16384) {
+    // longer than the shared-memory NER kernels hold: the cuFFT-based reference-length form has no such bound
+    if (!can_ref_len || mode == 3 || n_over_t > (int64_t)1 << 24)
+      return fail(PATFFT_ERR_UNSUPPORTED, "GPU NER supports oversampled depth lengths up to 16384 (N_t <= 4096 at c=2)");
+    P->ref_len = true;
+  }
   P->n_over_t = (int)n_over_t;
   if (mode != 2 && mode != 3 &&
       !resolve_window(c, K, d->spec_alpha, d->spec_beta, double(n_over_t) / n_ext, &P->win_t, &err)) {

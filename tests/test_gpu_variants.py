@@ -225,6 +225,25 @@ def test_gpu_single_launch_inverse_matches_two_kernel_form(nl, nt, slots, lead):
     print(f"single-launch inverse {nl} Nt={nt} slots={slots} lead={lead}: bit-identical to the two-kernel form")
 
 
+@pytest.mark.parametrize("nl,nt", [((8, 8), 8192), ((16,), 16384), ((8, 8), 6000)])
+def test_gpu_records_longer_than_the_shared_memory_ner(nl, nt):
+    """N_t > 4096 (oversampled depth length > 16384): beyond the shared-memory NER kernels, so the
+    plan runs the cuFFT-based reference-length form (csrc/reflen.cu); the reference has no bound."""
+    rng = np.random.default_rng(nt)
+    m = int(np.prod(nl))
+    half = np.asarray(nl, float) * synth.PITCH / 2
+    pos = rng.uniform(-half, half, size=(m, len(nl)))
+    t = np.arange(nt)
+    samples = np.exp(-((t[None, :] - rng.uniform(200, nt * 0.8, size=(m, 1))) ** 2) / 50.0)
+    samples += 1e-3 * rng.standard_normal((m, nt))
+    w = np.full(m, float(np.prod(np.asarray(nl) * synth.PITCH)) / m)
+    want, _ = O.reconstruct_nedner(pos, w, samples, 5e-9, synth.SOUND_SPEED, synth.PITCH, nl)
+    got = pb.reconstruct_nedner(pb.SensorRecord(pos, w, samples, 5e-9, synth.SOUND_SPEED, synth.PITCH, nl))
+    err = rel_l2(got.values, want)
+    print(f"long record {nl} Nt={nt}: rel-L2 {err:.3e}")
+    assert got.values.shape == want.shape and err <= TOL
+
+
 def test_gpu_gridding_scale_hint_history_does_not_change_results():
     """fp16 gridding: the sample scale is speculated from the previous call's maximum and verified
     on the device (spread_tc.cu, check_scale_kernel); a wrong guess re-runs the gridding.  Whatever
