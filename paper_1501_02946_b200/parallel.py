@@ -137,6 +137,28 @@ class GpuStages:
             pass
 
 
+def _host_staged(dist, group, tensor):
+    """CUDA tensors over a backend without device point-to-point (gloo): stage through the host.
+    NCCL, the product path, sends and receives the device buffers directly."""
+    return tensor.is_cuda and dist.get_backend(group) != "nccl"
+
+
+def _host_exchange(dist, group, rank, pairs):
+    """pairs[q] = (send view to rank q, recv view from rank q); synchronous, returns no work handles."""
+    sends = {q: sv.cpu() for q, (sv, _) in enumerate(pairs) if q != rank}
+    recvs = {q: rv.new_empty(rv.shape, device="cpu") for q, (_, rv) in enumerate(pairs) if q != rank}
+    ops = []
+    for q in sends:
+        ops.append(dist.P2POp(dist.isend, sends[q], q, group=group))
+        ops.append(dist.P2POp(dist.irecv, recvs[q], q, group=group))
+    for w in (dist.batch_isend_irecv(ops) if ops else []):
+        w.wait()
+    for q, (_, rv) in enumerate(pairs):
+        if q != rank:
+            rv.copy_(recvs[q])
+    return []
+
+
 def _pow2_at_most(n, cap):
     c = 1
     while c * 2 <= min(n, cap):
@@ -258,6 +280,8 @@ class ShardedNedNer:
         dist = self.dist
         snd, rcv = pairs[self.rank]
         rcv.copy_(snd)  # own share: a device copy on the compute stream
+        if _host_staged(dist, self.group, snd):
+            return _host_exchange(dist, self.group, self.rank, pairs)
         ops = []
         for q, (sv, rv) in enumerate(pairs):
             if q == self.rank:
@@ -479,7 +503,7 @@ class GeneralShardedNedNer:
         self.gh_rows = torch.empty(rm, L.T, 2, **f32)
         self.z_full = torch.zeros(L.rows_out_total, L.Tu, 2, **f32)   # rows of other ranks stay zero
         u0, u1 = L.tu_range(self.rank)
-        self.z_slice = torch.zeros(L.rows_out_total, u1 - u0, 2, **f32)  # rows nobody writes stay zero
+        self.z_slice = torch.zeros(L.rows_out_total, u1 - u0, 2, **f32)  # zero-padding rows: re-zeroed per run
         self.image = torch.empty(L.image_slice_shape(self.rank), **f32)
         self.out_idx = [torch.tensor(L.out_rows(q), dtype=torch.long, device=torch_device) for q in range(P)]
         self.cuda_stream = torch.cuda.Stream(device=torch_device) if torch_device.type == "cuda" else None
@@ -487,6 +511,9 @@ class GeneralShardedNedNer:
     def _exchange(self, sends, recvs):
         dist = self.dist
         recvs[self.rank].copy_(sends[self.rank])
+        if _host_staged(dist, self.group, sends[self.rank]):
+            _host_exchange(dist, self.group, self.rank, list(zip(sends, recvs)))
+            return
         ops = []
         for q in range(self.world):
             if q != self.rank:
@@ -528,6 +555,8 @@ class GeneralShardedNedNer:
         u0, u1 = L.tu_range(me)
         recvs = [torch.empty(len(self.out_idx[q]), u1 - u0, 2, dtype=torch.float32, device=self.tdev) for q in range(P)]
         self._exchange(sends, recvs)
+        if L.up > 1:  # the lateral inverse works in place: the zero-padding rows must be zero again
+            self.z_slice.zero_()
         for q in range(P):
             self.z_slice.index_copy_(0, self.out_idx[q], recvs[q])
         st.inverse(self.z_slice, self.image, s)
