@@ -109,6 +109,7 @@ class NumpyStages:
         if self.nlat == 1:
             img = img[0]
         image_slice.copy_(image_slice.new_tensor(img.astype(np.float32)))
+        z_recv.fill_(float("nan"))  # the CUDA stage transforms its input in place: nothing of it may be reused
 
 
 class NumpySliceStages(NumpyStages):
@@ -170,3 +171,4 @@ class NumpySliceStages(NumpyStages):
         if self.nlat == 1:
             img = img[0]
         image_slice.copy_(image_slice.new_tensor(img.astype(np.float32)))
+        z_slice.fill_(float("nan"))  # consumed in place by the CUDA stage
