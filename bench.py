@@ -348,9 +348,17 @@ def run_sharded_arm(args):
     from paper_1501_02946_b200.parallel import ShardedNedNer
 
     rank, world, local = _env_rank()
+    # PATFFT_DIST_BACKEND=gloo: the same arm with several ranks on ONE GPU (host-staged exchanges,
+    # parallel._host_exchange) -- a functional check of the multi-rank path where only one GPU exists
+    backend = os.environ.get("PATFFT_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     rec = make_workload(args.config, 0)[0]  # every rank: the same record, its own time slice
     T = rec.samples.shape[1]
