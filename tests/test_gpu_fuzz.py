@@ -37,6 +37,8 @@ def test_gpu_random_shapes_and_windows_match_oracle(seed0):
         rec = pb.SensorRecord(cs["positions"], cs["weights"], cs["samples"], cs["dt"], synth.SOUND_SPEED, synth.PITCH,
                               cs["n_lateral"])
         got = pb.reconstruct_nedner(rec, out_dims=cs["out_dims"], upsample=cs["upsample"], spec=pb.WindowSpec(*spec))
+        again = pb.reconstruct_nedner(rec, out_dims=cs["out_dims"], upsample=cs["upsample"], spec=pb.WindowSpec(*spec))
+        assert np.array_equal(got.values, again.values), f"{cs['desc']}: second call on the cached plan differs"
         err = rel_l2(got.values, want)
         # float32 limit: a window with psi(0) / psi(pi) in the hundreds amplifies the rounding of the
         # float32 gridding / FFTs by that factor at the Nyquist frequencies (default window: 4.6)
