@@ -154,3 +154,24 @@ def test_gpu_standalone_plans_random_problems_match_oracle():
         worst["fwd"] = max(worst["fwd"], e)
     print("standalone fuzz: worst rel-L2 " + ", ".join(f"{k} {v:.2e}" for k, v in worst.items())
           + f"; forward model refused {refused} inaccurate windows")
+
+
+def test_gpu_smallest_sizes_match_oracle():
+    """Even lengths from 2 on every axis (the reference's lower bound), upsample 1-3."""
+    worst, n = 0.0, 0
+    for nl in [(2,), (4,), (6,), (2, 2), (2, 4), (4, 2), (4, 6), (6, 6), (2, 8), (10, 2)]:
+        for nt in (2, 4, 6, 8, 10, 14):
+            for up in (1, 2, 3):
+                rng = np.random.default_rng(1000 * sum(nl) + 10 * nt + up)
+                m = max(3, int(np.prod(nl)))
+                half = np.asarray(nl, float) * synth.PITCH / 2
+                pos = rng.uniform(-half, half, size=(m, len(nl)))
+                samples = rng.standard_normal((m, nt))
+                w = np.full(m, float(np.prod(np.asarray(nl) * synth.PITCH)) / m)
+                want, _ = O.reconstruct_nedner(pos, w, samples, 20e-9, synth.SOUND_SPEED, synth.PITCH, nl, upsample=up)
+                got = pb.reconstruct_nedner(pb.SensorRecord(pos, w, samples, 20e-9, synth.SOUND_SPEED, synth.PITCH, nl),
+                                            upsample=up).values
+                err = rel_l2(got, want)
+                assert got.shape == want.shape and err <= 1e-4, f"nl={nl} nt={nt} up={up}: rel-L2 {err:.2e}"
+                worst, n = max(worst, err), n + 1
+    print(f"smallest sizes: {n} reconstructions, worst rel-L2 {worst:.2e}")
