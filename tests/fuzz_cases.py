@@ -46,6 +46,9 @@ def draw(seed):
         if hi > lo:
             alpha = float(rng.uniform(lo, hi))
             beta = float(rng.uniform(0.3, 1.2) * K / c)
+    if rng.random() < 0.5:  # non-uniform quadrature weights h_m (sum = aperture measure, recon.py:157-164)
+        w = rng.uniform(0.2, 1.8, size=m)
+        w *= float(np.prod(np.asarray(nl) * synth.PITCH)) / w.sum()
     return dict(positions=pos, weights=w, samples=samples, dt=dt, n_lateral=nl, out_dims=out_dims, upsample=up,
                 c=c, K=K, alpha=alpha, beta=beta,
                 desc=f"seed {seed}: nl={nl} nt={nt} up={up} out_dims={out_dims} c={c} K={K} alpha={alpha} beta={beta}")
@@ -101,6 +104,9 @@ def draw_fast(seed):
     if rng.random() < 0.3:
         out_dims = tuple(int(rng.choice([16, 32, 64])) for _ in nl)
     K = int(rng.choice([4, 6, 6, 8]))
+    if rng.random() < 0.5:
+        w = rng.uniform(0.2, 1.8, size=m)
+        w *= float(np.prod(np.asarray(nl) * synth.PITCH)) / w.sum()
     return dict(positions=pos, weights=w, samples=samples, dt=dt, n_lateral=nl, out_dims=out_dims, upsample=up,
                 c=2.0, K=K, alpha=None, beta=None,
                 desc=f"fast seed {seed}: nl={nl} M={m} {kind} nt={nt} up={up} out_dims={out_dims} K={K}")
