@@ -175,3 +175,33 @@ def test_gpu_smallest_sizes_match_oracle():
                 assert got.shape == want.shape and err <= 1e-4, f"nl={nl} nt={nt} up={up}: rel-L2 {err:.2e}"
                 worst, n = max(worst, err), n + 1
     print(f"smallest sizes: {n} reconstructions, worst rel-L2 {worst:.2e}")
+
+
+def test_gpu_batch_and_frames_paths_on_random_plans():
+    """execute_batch (pipelined host records) and execute_frames_device on plans of odd shapes,
+    upsample and reference-length windows: each record equals the single-call result."""
+    import torch
+
+    for seed in (1002, 1006, 1007, 1014, 1028, 2009, 5004, 5010):
+        cs = draw(seed) if seed < 5000 else __import__("fuzz_cases").draw_fast(seed)
+        spec = pb.WindowSpec(cs["c"], cs["K"], cs["alpha"], cs["beta"])
+        nt = cs["samples"].shape[1]
+        plan = pb.NedNerPlan(cs["positions"], cs["weights"], nt, cs["dt"], synth.SOUND_SPEED, synth.PITCH,
+                             cs["n_lateral"], out_dims=cs["out_dims"], upsample=cs["upsample"], spec=spec)
+        rng = np.random.default_rng(seed)
+        recs = [cs["samples"] * a + 1e-3 * rng.standard_normal(cs["samples"].shape) for a in (1.0, 37.0, 1e-5, 1.0)]
+        singles = [plan.execute(r)[0].copy() for r in recs]
+        outs, bad = plan.execute_batch(recs)
+        assert not any(bad)
+        for k, (a, b) in enumerate(zip(outs, singles)):
+            assert np.array_equal(a, b), f"{cs['desc']}: batch record {k} differs from the single call"
+        dev = torch.device("cuda", 0)
+        x = torch.tensor(np.stack(recs), dtype=torch.float32, device=dev)
+        y = torch.empty((len(recs),) + plan.out_shape, dtype=torch.float32, device=dev)
+        plan.execute_frames_device(len(recs), x.data_ptr(), y.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+        torch.cuda.synchronize(dev)
+        v = y.cpu().numpy().astype(np.float64)
+        for k in range(len(recs)):
+            e = rel_l2(v[k], singles[k])
+            assert e <= 2e-6, f"{cs['desc']}: frame {k} vs the single call {e:.2e}"
+    print("batch / frames paths: 8 plans x 4 records equal the single calls")
